@@ -1,0 +1,56 @@
+"""The CPU oracle against golden vectors produced by the real reference.
+
+Bit-exact: u, f, iters, converged, final_residual, r_ref.  Tolerance-only
+(BLAS order in the reference): avg_stress 1e-13 rel, energy residual 1e-10.
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+import golden_cases as gc
+from oracle import frb_oracle as orc
+
+FAST = [n for n in gc.names() if n not in ("random60", "c2_15cube_seed0")]
+
+
+def _check(case, r):
+    d = case.data
+    if case.singular:
+        assert r.status == orc.STATUS_SINGULAR
+        assert f"element {r.bad_element}:" in str(d["error"])
+        return
+    assert r.iters == int(d["iters"])
+    assert r.converged == bool(d["converged"])
+    assert np.array_equal(r.u, d["u"])
+    assert np.array_equal(r.f, d["f"])
+    assert r.residual == float(d["final_residual"])
+    ref_rref = float(d["r_ref"])
+    assert (math.isnan(r.r_ref) and math.isnan(ref_rref)) or r.r_ref == ref_rref
+    scale = max(np.max(np.abs(d["avg_stress"])), 1e-300)
+    assert np.max(np.abs(r.sigma - d["avg_stress"])) <= 1e-13 * scale
+    e = float(d["energy_residual"])
+    if math.isnan(e):
+        assert r.energy_residual is None
+    else:
+        assert abs(r.energy_residual - e) <= 1e-10 * max(abs(e), 1e-30)
+
+
+@pytest.mark.parametrize("name", FAST)
+def test_oracle_matches_reference_golden(name):
+    case = gc.load(name)
+    _check(case, orc.solve(case.network, case.F, case.cfg))
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name", ["random60", "c2_15cube_seed0"])
+def test_oracle_matches_reference_golden_long(name):
+    case = gc.load(name)
+    _check(case, orc.solve(case.network, case.F, case.cfg))
+
+
+def test_oracle_internal_forces_matches_solver_state():
+    case = gc.load("c1_7x7x8_uniax")
+    f = orc.internal_forces(case.network, case.data["u"])
+    assert np.array_equal(f, case.data["f"])
