@@ -1,0 +1,95 @@
+"""ctypes binding of the C-ABI in ``include/frb200.h`` (``lib/libfrb200.so``).
+
+The struct layouts below mirror the header field for field; ``tests/test_abi.py``
+checks sizes and that every declared symbol is exported.  Loading fails
+loudly: there is no CPU fallback for the solver.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "lib", "libfrb200.so")
+
+FRB_OK, FRB_E_INVALID, FRB_E_TOO_LARGE, FRB_E_CUDA, FRB_E_UNSUPPORTED = 0, -1, -2, -3, -4
+STATUS_CONVERGED, STATUS_MAX_ITERS, STATUS_SINGULAR = 0, 1, 2
+DAMPING_ADAPTIVE, DAMPING_FIXED = 0, 1
+
+EXPORTS = ("frb_abi_version", "frb_last_error", "frb_device_info", "frb_cta_smem_bytes",
+           "frb_solve_batch", "frb_internal_forces")
+
+
+class FrbConfig(C.Structure):
+    _fields_ = [("tol_rel", C.c_double), ("tol_abs", C.c_double), ("dt_safety", C.c_double),
+                ("damping_c", C.c_double), ("max_iters", C.c_int32), ("damping", C.c_int32),
+                ("energy_check_interval", C.c_int32), ("bc_ramp_iters", C.c_int32)]
+
+
+class FrbBatch(C.Structure):
+    _fields_ = [("n_problems", C.c_int32), ("smem_bytes", C.c_int32),
+                ("problems", C.c_void_p), ("order", C.c_void_p), ("X", C.c_void_p),
+                ("node_mass", C.c_void_p), ("inc_node", C.c_void_p), ("inc", C.c_void_p),
+                ("elem_ab", C.c_void_p), ("elem_L", C.c_void_p), ("elem_EA", C.c_void_p),
+                ("plans", C.c_void_p), ("u", C.c_void_p), ("f", C.c_void_p),
+                ("results", C.c_void_p), ("queue", C.c_void_p)]
+
+
+# frb_problem / frb_result as numpy record types (arrays of them are uploaded
+# / downloaded as raw bytes)
+PROBLEM_DTYPE = np.dtype([
+    ("node_base", "<i8"), ("elem_base", "<i8"), ("inc_base", "<i8"), ("plan_base", "<i8"),
+    ("n_nodes", "<i4"), ("n_free_nodes", "<i4"), ("n_elems", "<i4"), ("cluster", "<i4"),
+    ("dt", "<f8"), ("volume", "<f8"), ("F", "<f8", (9,)),
+])
+RESULT_DTYPE = np.dtype([
+    ("status", "<i4"), ("iters", "<i4"), ("bad_element", "<i4"), ("converged", "<i4"),
+    ("final_residual", "<f8"), ("r_ref", "<f8"), ("energy_residual", "<f8"),
+    ("avg_stress", "<f8", (9,)), ("energy", "<f8", (4,)),
+])
+assert PROBLEM_DTYPE.itemsize == 136 and RESULT_DTYPE.itemsize == 144
+
+
+class NativeError(RuntimeError):
+    def __init__(self, code: int, message: str):
+        super().__init__(f"libfrb200 error {code}: {message}")
+        self.code = code
+
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """Load libfrb200.so once; raise if it has not been built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: build it with `python -c 'import "
+                          "__graft_entry__ as g; g.build()'` (no CPU fallback exists)")
+    h = C.CDLL(LIB_PATH)
+    h.frb_abi_version.restype = C.c_int
+    h.frb_last_error.restype = C.c_char_p
+    h.frb_device_info.argtypes = [C.c_int] + [C.POINTER(C.c_int)] * 4
+    h.frb_cta_smem_bytes.restype = C.c_int64
+    h.frb_cta_smem_bytes.argtypes = [C.c_int32, C.c_int32, C.c_int32]
+    h.frb_solve_batch.argtypes = [C.POINTER(FrbBatch), C.POINTER(FrbConfig), C.c_int, C.c_int, C.c_void_p]
+    h.frb_internal_forces.argtypes = [C.POINTER(FrbBatch), C.c_void_p, C.c_void_p, C.c_void_p]
+    if h.frb_abi_version() != 1:
+        raise ImportError("libfrb200.so ABI version mismatch")
+    _lib = h
+    return h
+
+
+def check(rc: int):
+    if rc != FRB_OK:
+        raise NativeError(rc, lib().frb_last_error().decode(errors="replace"))
+
+
+def device_info(device: int = 0):
+    vals = [C.c_int() for _ in range(4)]
+    check(lib().frb_device_info(device, *[C.byref(v) for v in vals]))
+    return dict(n_sm=vals[0].value, smem_optin=vals[1].value, cc=(vals[2].value, vals[3].value))

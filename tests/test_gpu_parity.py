@@ -1,0 +1,140 @@
+"""CUDA path vs the reference golden vectors and the CPU oracle (B200).
+
+Bar: u, f, final_residual, r_ref bit-equal; iters and
+converged equal; avg_stress within 1e-13 of max|sigma| (BLAS order in the
+reference).  Every call goes through the C-ABI library.
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+import golden_cases as gc
+import paper_2305_07030_b200 as frb
+from paper_2305_07030_b200 import batch as fb
+from oracle import frb_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+SIGMA_RTOL = 1e-13
+NAMES = [n for n in gc.names() if n != "bar_singular"]
+
+
+def assert_matches(r, u_ref, iters, converged, residual, r_ref, sigma, label=""):
+    assert r.iters == iters, f"{label}: iters {r.iters} != {iters}"
+    assert r.converged == converged, label
+    assert np.array_equal(r.u, u_ref), f"{label}: u differs (max {np.abs(r.u - u_ref).max():.3e})"
+    assert r.final_residual == residual or (math.isnan(r.final_residual) and math.isnan(residual)), label
+    assert r.r_ref == r_ref or (math.isnan(r.r_ref) and math.isnan(r_ref)), label
+    scale = max(np.abs(sigma).max(), 1e-300)
+    assert np.abs(r.avg_stress - sigma).max() <= SIGMA_RTOL * scale, label
+
+
+def golden_expect(case):
+    d = case.data
+    return (d["u"], int(d["iters"]), bool(d["converged"]), float(d["final_residual"]),
+            float(d["r_ref"]), d["avg_stress"])
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_single_solve_matches_reference(cuda_device, name):
+    case = gc.load(name)
+    r = frb.dynamic_relaxation_solve(case.network, frb.AffineBC(case.F), case.cfg)
+    assert_matches(r, *golden_expect(case), label=name)
+    if case.cfg.energy_check_interval > 0:
+        e = float(case.data["energy_residual"])
+        assert abs(r.energy_residual - e) <= 1e-10 * max(abs(e), 1e-30)
+
+
+def test_final_forces_bit_equal(cuda_device):
+    for name in ("c1_7x7x8_uniax", "lat6_general_F", "random90_fixed"):
+        case = gc.load(name)
+        batch = frb.pack_batch([case.network], [frb.AffineBC(case.F)])
+        dres = batch.to_device().solve(case.cfg)
+        f_solver = dres.f.cpu().numpy().reshape(-1, 3)
+        f = np.empty_like(f_solver)
+        f[batch.problems[0].node_order] = f_solver
+        assert np.array_equal(f.reshape(-1), case.data["f"]), name
+
+
+def test_heterogeneous_batch_equals_single(cuda_device):
+    """All golden cases with the default config in one launch (mixed sizes,
+    loads, topologies); each must equal its reference result."""
+    cases = [gc.load(n) for n in NAMES]
+    cases = [c for c in cases if c.cfg == frb.SolverConfig()]
+    res = frb.solve_batch(frb.pack_batch([c.network for c in cases], [frb.AffineBC(c.F) for c in cases]))
+    for c, r in zip(cases, res):
+        assert_matches(r, *golden_expect(c), label=c.name)
+
+
+def test_singular_element_raises(cuda_device):
+    case = gc.load("bar_singular")
+    with pytest.raises(frb.SingularElementError, match="element 0: current length collapsed"):
+        frb.dynamic_relaxation_solve(case.network, frb.AffineBC(case.F), case.cfg)
+
+
+def test_singular_does_not_abort_siblings(cuda_device):
+    good = gc.load("lat5_shear")
+    bad = gc.load("bar_singular")
+    batch = frb.pack_batch([good.network, bad.network, good.network],
+                           [frb.AffineBC(good.F), frb.AffineBC(bad.F), frb.AffineBC(good.F)])
+    dres = batch.to_device().solve(frb.SolverConfig())
+    out = fb.results_to_solve_results(batch, dres, raise_singular=False)
+    assert out[1] is None
+    for r in (out[0], out[2]):
+        assert_matches(r, *golden_expect(good), label="sibling")
+
+
+@pytest.mark.parametrize("n,seed,load", [(6, 0, "uniax"), (7, 1, "biax"), (8, 2, "shear"),
+                                         (9, 3, "uniax"), (5, 4, "shear")])
+def test_random_lattices_vs_oracle(cuda_device, n, seed, load):
+    F = {"uniax": np.diag([1.1, 1, 1]), "biax": np.diag([1.1, 1.1, 1]),
+         "shear": np.eye(3) + 0.2 * np.outer([1, 0, 0], [0, 1, 0])}[load]
+    net = frb.generate_lattice(n, n + 1, n, 0.3, seed)
+    cfg = frb.SolverConfig()
+    r = frb.dynamic_relaxation_solve(net, frb.AffineBC(F), cfg)
+    o = orc.solve(net, F, cfg)
+    assert_matches(r, o.u, o.iters, o.converged, o.residual, o.r_ref, o.sigma, label=f"{n}/{seed}")
+
+
+def test_c2_batch_subset_vs_oracle(cuda_device):
+    """Config 2 networks (15^3, uniaxial) inside a 16-network batch."""
+    nets = [frb.generate_lattice(15, 15, 15, 0.3, s) for s in range(16)]
+    F = np.diag([1.1, 1.0, 1.0])
+    res = frb.solve_batch(frb.pack_batch(nets, [frb.AffineBC(F)] * 16))
+    for s in (0, 7):
+        o = orc.solve(nets[s], F, frb.SolverConfig())
+        assert_matches(res[s], o.u, o.iters, o.converged, o.residual, o.r_ref, o.sigma, label=f"seed{s}")
+    golden = gc.load("c2_15cube_seed0")
+    assert_matches(res[0], *golden_expect(golden), label="golden c2")
+
+
+def test_deterministic_rerun(cuda_device):
+    nets = [frb.generate_lattice(8, 8, 8, 0.3, s) for s in range(40)]
+    bcs = [frb.AffineBC(np.diag([1.1, 1.0, 1.0]))] * 40
+    batch = frb.pack_batch(nets, bcs)
+    a = frb.solve_batch(batch)
+    b = frb.solve_batch(batch, strategy=frb.TeamBatched(teams=7))
+    c = frb.solve_batch(batch, strategy=frb.SerialReference())
+    for x, y, z in zip(a, b, c):
+        assert x.iters == y.iters == z.iters
+        assert np.array_equal(x.u, y.u) and np.array_equal(x.u, z.u)
+        assert np.array_equal(x.avg_stress, y.avg_stress)
+
+
+def test_internal_forces_matches_reference(cuda_device):
+    case = gc.load("lat6_general_F")
+    f = frb.internal_forces(case.network, case.data["u"])
+    assert np.array_equal(f, case.data["f"])
+    assert frb.force_residual(f, 0) == 0.0
+    # translation invariance (SPEC.md invariants)
+    t = np.tile([0.3, -0.2, 0.5], case.network.n_nodes)
+    assert np.abs(frb.internal_forces(case.network, t)).max() < 1e-12
+
+
+def test_identity_deformation_converges_in_one(cuda_device):
+    net = frb.generate_lattice(6, 6, 6, 0.3, 1)
+    r = frb.dynamic_relaxation_solve(net, frb.AffineBC(np.eye(3)))
+    assert r.converged and r.iters == 1
+    assert not r.u.any() and not r.avg_stress.any()
