@@ -184,12 +184,14 @@ def _role_slots(node_of_elem: np.ndarray, n_nodes: int) -> np.ndarray:
 
 
 def _gather_sum(values: np.ndarray, slots: np.ndarray, n_nodes: int) -> np.ndarray:
-    """Per node: 0.0 + values[e1] + values[e2] + ... in slot order."""
+    """Per node: 0.0 + values[e1] + values[e2] + ... in slot order.
+
+    Padding slots (-1) read an appended +0.0 row; adding +0.0 is exact here
+    because a running sum that starts at +0.0 can never become -0.0."""
+    padded = np.concatenate([values, np.zeros((1,) + values.shape[1:])])
     acc = np.zeros((n_nodes,) + values.shape[1:])
     for s in range(slots.shape[1]):
-        col = slots[:, s]
-        ok = col >= 0
-        acc[ok] = acc[ok] + values[col[ok]]
+        acc = acc + padded[slots[:, s]]
     return acc
 
 

@@ -200,6 +200,14 @@ class Batch:
     max_leaves: int
     smem_bytes: int
     _packed_state: dict | None = field(default=None, repr=False)
+    pinned: dict | None = field(default=None, repr=False)
+
+    def pin(self) -> "Batch":
+        """Page-lock the packed arrays once so uploads are pure DMA."""
+        torch = _torch()
+        self.pinned = {k: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+                       for k, a in self.arrays.items()}
+        return self
 
     @property
     def n_problems(self) -> int:
@@ -333,9 +341,12 @@ class DeviceBatch:
         device = torch.device(device if device is not None else "cuda")
         t = {}
         for k, a in batch.arrays.items():
-            src = torch.from_numpy(np.ascontiguousarray(a))
-            if pin:
-                src = src.pin_memory()
+            if batch.pinned is not None:
+                src = batch.pinned[k]
+            else:
+                src = torch.from_numpy(np.ascontiguousarray(a))
+                if pin:
+                    src = src.pin_memory()
             t[k] = src.to(device, non_blocking=True)
         return cls(host=batch, device=device, t=t, desc_host=batch.desc.copy())
 
@@ -360,15 +371,14 @@ class DeviceBatch:
         b.queue = queue.data_ptr()
         return b
 
-    def solve(self, cfg: SolverConfig, strategy=None, stream=None) -> DeviceResults:
-        """Launch the persistent kernel; returns device-resident results
-        (asynchronous on the current torch stream)."""
+    def prepare(self, cfg: SolverConfig, strategy=None) -> "Launch":
+        """Allocate outputs and build the launch arguments once; the
+        returned Launch can be replayed (bench) or run once (solve)."""
         torch = _torch()
         strategy = strategy or TeamBatched()
         if isinstance(strategy, NaiveLoop):
             raise NotImplementedError("NaiveLoop per-operation dispatch is not provided on the B200 path")
-        need = max(64, 32 * math.ceil(8 * self.host.max_leaves / 32))
-        threads = need
+        threads = max(64, 32 * math.ceil(8 * self.host.max_leaves / 32))
         grid = 0
         if isinstance(strategy, TeamBatched):
             if strategy.team_size is not None:
@@ -387,13 +397,34 @@ class DeviceBatch:
         res = torch.zeros(self.host.n_problems * nat.RESULT_DTYPE.itemsize, dtype=torch.uint8, device=dev)
         queue = torch.zeros(1, dtype=torch.int32, device=dev)
         desc_t = self._desc_tensor(cfg)
-        fb = self.frb_batch(desc_t, u, f, res, queue)
-        fc = config_struct(cfg)
-        s = stream if stream is not None else torch.cuda.current_stream(dev)
-        nat.check(nat.lib().frb_solve_batch(C.byref(fb), C.byref(fc), threads, grid,
-                                            C.c_void_p(s.cuda_stream)))
-        self._keep = (desc_t, fb)
-        return DeviceResults(u=u, f=f, results=res, node_base=self.host.node_base)
+        return Launch(self, self.frb_batch(desc_t, u, f, res, queue), config_struct(cfg), threads, grid,
+                      DeviceResults(u=u, f=f, results=res, node_base=self.host.node_base),
+                      keep=(desc_t, queue))
+
+    def solve(self, cfg: SolverConfig, strategy=None, stream=None) -> DeviceResults:
+        """Launch the persistent kernel; returns device-resident results
+        (asynchronous on the current torch stream)."""
+        launch = self.prepare(cfg, strategy)
+        launch.run(stream)
+        return launch.out
+
+
+@dataclass
+class Launch:
+    dbatch: DeviceBatch
+    fb: nat.FrbBatch
+    fc: nat.FrbConfig
+    threads: int
+    grid: int
+    out: DeviceResults
+    keep: tuple = ()
+
+    def run(self, stream=None):
+        """One frb_solve_batch call (one kernel launch) on `stream`."""
+        torch = _torch()
+        s = stream if stream is not None else torch.cuda.current_stream(self.dbatch.device)
+        nat.check(nat.lib().frb_solve_batch(C.byref(self.fb), C.byref(self.fc), self.threads,
+                                            self.grid, C.c_void_p(s.cuda_stream)))
 
 
 def config_struct(cfg: SolverConfig) -> nat.FrbConfig:
