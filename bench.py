@@ -162,7 +162,7 @@ def cpu_sample(config: str, cores: int, per_core: int = 1):
         jobs = [((15, 15, 15), s, UNIAX) for s in range(cores * per_core)]
     ctx = mp.get_context("fork")
     with ctx.Pool(cores) as pool:
-        pool.map(_oracle_solve, jobs[:cores])  # warm the workers (imports)
+        pool.map(_oracle_solve, [((3, 3, 3), 0, UNIAX)] * cores)  # warm the workers (imports)
         t0 = time.perf_counter()
         out = pool.map(_oracle_solve, jobs)
         wall = time.perf_counter() - t0
