@@ -208,6 +208,7 @@ def main():
     ap.add_argument("--config", default="c2", choices=["c1", "c2", "c4", "c5"])
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--team-size", type=int, default=None, help="CTA size override (TeamBatched)")
     args = ap.parse_args()
     if args.warmup < 3:
         raise SystemExit("--warmup must be >= 3")
@@ -237,7 +238,8 @@ def main():
     setup_s = time.perf_counter() - t0
     batch.pin()
     dbatch = batch.to_device(dev)
-    launch = dbatch.prepare(cfg)
+    strategy = frb.TeamBatched(team_size=args.team_size)
+    launch = dbatch.prepare(cfg, strategy)
     flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
     P = batch.n_problems
     gathered = torch.empty(world * P * 9, dtype=torch.float64, device=dev)
@@ -289,7 +291,7 @@ def main():
 
     # ---- e2e through the public API (pinned host buffers -> results) ----
     def e2e_step():
-        return fb.results_to_solve_results(batch, batch.to_device(dev).solve(cfg))
+        return fb.results_to_solve_results(batch, batch.to_device(dev).solve(cfg, strategy))
     for _ in range(1):
         e2e_step()
     torch.cuda.synchronize(dev)
@@ -330,7 +332,7 @@ def main():
         "data": "synthetic (generate_lattice jittered lattices, same generator as the reference)",
         "config": {"workload": workload, "networks_per_gpu": P, "parallelism": f"shard{world}",
                    "l2": "flushed (256 MiB memset before every step)",
-                   "setup_s_per_rank": round(setup_s, 3)},
+                   "setup_s_per_rank": round(setup_s, 3), "cta_threads": launch.threads},
         "node_updates_per_s": world * node_updates / (elapsed / args.steps),
         "iters_mean": float(iters.mean()),
         "e2e": {"value": world * P / e2e_s, "unit": "networks/s", "h2d_bytes_per_step": int(h2d),

@@ -20,7 +20,7 @@ STATUS_CONVERGED, STATUS_MAX_ITERS, STATUS_SINGULAR = 0, 1, 2
 DAMPING_ADAPTIVE, DAMPING_FIXED = 0, 1
 
 EXPORTS = ("frb_abi_version", "frb_last_error", "frb_device_info", "frb_cta_smem_bytes",
-           "frb_solve_batch", "frb_internal_forces")
+           "frb_solve_batch", "frb_internal_forces", "frb_selftest_arith")
 
 
 class FrbConfig(C.Structure):
@@ -30,11 +30,13 @@ class FrbConfig(C.Structure):
 
 
 class FrbBatch(C.Structure):
-    _fields_ = [("n_problems", C.c_int32), ("smem_bytes", C.c_int32),
+    _fields_ = [("n_problems", C.c_int32), ("smem_bytes", C.c_int32), ("max_nf", C.c_int32),
+                ("pad0", C.c_int32),
                 ("problems", C.c_void_p), ("order", C.c_void_p), ("X", C.c_void_p),
                 ("node_mass", C.c_void_p), ("inc_node", C.c_void_p), ("inc", C.c_void_p),
                 ("elem_ab", C.c_void_p), ("elem_L", C.c_void_p), ("elem_EA", C.c_void_p),
-                ("plans", C.c_void_p), ("u", C.c_void_p), ("f", C.c_void_p),
+                ("plans", C.c_void_p), ("ell_other", C.c_void_p), ("ell_L", C.c_void_p),
+                ("ell_EA", C.c_void_p), ("u", C.c_void_p), ("f", C.c_void_p), ("work", C.c_void_p),
                 ("results", C.c_void_p), ("queue", C.c_void_p)]
 
 
@@ -42,15 +44,18 @@ class FrbBatch(C.Structure):
 # / downloaded as raw bytes)
 PROBLEM_DTYPE = np.dtype([
     ("node_base", "<i8"), ("elem_base", "<i8"), ("inc_base", "<i8"), ("plan_base", "<i8"),
+    ("ell_base", "<i8"), ("ellv_base", "<i8"),
     ("n_nodes", "<i4"), ("n_free_nodes", "<i4"), ("n_elems", "<i4"), ("cluster", "<i4"),
-    ("dt", "<f8"), ("volume", "<f8"), ("F", "<f8", (9,)),
+    ("ell_stride", "<i4"), ("ell_slots_a", "<i4"), ("ell_slots_b", "<i4"), ("flags", "<i4"),
+    ("dt", "<f8"), ("volume", "<f8"), ("ea", "<f8"), ("F", "<f8", (9,)),
 ])
+PF_EA_UNIFORM = 1
 RESULT_DTYPE = np.dtype([
     ("status", "<i4"), ("iters", "<i4"), ("bad_element", "<i4"), ("converged", "<i4"),
     ("final_residual", "<f8"), ("r_ref", "<f8"), ("energy_residual", "<f8"),
     ("avg_stress", "<f8", (9,)), ("energy", "<f8", (4,)),
 ])
-assert PROBLEM_DTYPE.itemsize == 136 and RESULT_DTYPE.itemsize == 144
+assert PROBLEM_DTYPE.itemsize == 176 and RESULT_DTYPE.itemsize == 144
 
 
 class NativeError(RuntimeError):
@@ -78,6 +83,7 @@ def lib() -> C.CDLL:
     h.frb_cta_smem_bytes.argtypes = [C.c_int32, C.c_int32, C.c_int32]
     h.frb_solve_batch.argtypes = [C.POINTER(FrbBatch), C.POINTER(FrbConfig), C.c_int, C.c_int, C.c_void_p]
     h.frb_internal_forces.argtypes = [C.POINTER(FrbBatch), C.c_void_p, C.c_void_p, C.c_void_p]
+    h.frb_selftest_arith.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]
     if h.frb_abi_version() != 1:
         raise ImportError("libfrb200.so ABI version mismatch")
     _lib = h

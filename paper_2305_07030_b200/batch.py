@@ -41,12 +41,13 @@ from .microsolver import (
 )
 from .network import AffineBC, FiberNetwork
 from .packed import PackedStorage
-from .plan import reduction_plan
+from .plan import PlanView, reduction_plan
 
 __all__ = ["Batch", "DeviceBatch", "ExecutionStrategy", "NaiveLoop", "SerialReference",
            "TeamBatched", "pack_batch", "solve_batch", "build_problem", "DeviceResults"]
 
-MAX_CTA_THREADS = 512
+MAX_CTA_THREADS = 1024
+MAX_DOFS_PER_THREAD = 8     # FRB_MAX_DOFS_PER_THREAD
 
 
 # ------------------------------------------------------------------ strategies
@@ -115,6 +116,11 @@ class Topology:
     elem_ab: np.ndarray          # (M, 2) int32 solver node ids
     plan: np.ndarray             # int32 flat pairwise plan for nf
     n_leaves: int
+    max_own: int                 # most DOFs one chain thread owns
+    ell_other: np.ndarray        # (SA+SB, S) int32 slot-major, -1 padding
+    ell_elem: np.ndarray         # (SA+SB, S) int32 element per slot (0 on padding)
+    ell_slots_a: int
+    ell_slots_b: int
 
 
 def _topology(network: FiberNetwork, node_rank: np.ndarray, n_free_nodes: int) -> Topology:
@@ -136,9 +142,28 @@ def _topology(network: FiberNetwork, node_rank: np.ndarray, n_free_nodes: int) -
     np.cumsum((na + nb)[:-1], out=first[1:])
     inc_node = np.stack([first, na | (nb << 16)], axis=1).astype(np.int32)
     plan = reduction_plan(3 * n_free_nodes)
+    # slot-major table for free nodes: slot k < SA is the k-th role-a
+    # incidence (ascending element), slot SA + k the k-th role-b incidence
+    snode, srole = node[order], role[order]
+    grp = snode.astype(np.int64) * 2 + srole
+    starts = np.flatnonzero(np.r_[True, grp[1:] != grp[:-1]])
+    rank = np.arange(len(grp)) - np.repeat(starts, np.diff(np.r_[starts, len(grp)]))
+    nfn = n_free_nodes
+    sa = int(na[:nfn].max()) if nfn and m else 0
+    sb = int(nb[:nfn].max()) if nfn and m else 0
+    stride = max(32, 32 * ((nfn + 31) // 32))
+    ell_other = np.full((sa + sb, stride), -1, dtype=np.int32)
+    ell_elem = np.zeros((sa + sb, stride), dtype=np.int32)
+    free = snode < nfn
+    slot = np.where(srole == 0, rank, sa + rank)[free]
+    ell_other[slot, snode[free]] = other[order][free]
+    ell_elem[slot, snode[free]] = elem[order][free]
+    sizes = PlanView(plan).leaf_size
+    max_own = int(max(((z // 8) + (1 if z % 8 else 0)) if z >= 8 else 1 for z in sizes)) if len(sizes) else 1
     return Topology(n_nodes=n, n_free_nodes=n_free_nodes, inc_node=inc_node, inc=inc,
                     elem_ab=np.stack([ia, ib], axis=1).astype(np.int32), plan=plan,
-                    n_leaves=int(plan[0]))
+                    n_leaves=int(plan[0]), max_own=max_own, ell_other=ell_other,
+                    ell_elem=ell_elem, ell_slots_a=sa, ell_slots_b=sb)
 
 
 _TOPO_CACHE: dict[bytes, Topology] = {}
@@ -181,7 +206,7 @@ def build_problem(network: FiberNetwork, bc: AffineBC, check_mass: bool = True) 
 def cta_smem_bytes(n_nodes: int, n_free_nodes: int, n_leaves: int) -> int:
     """Mirror of frb_cta_smem_bytes (include/frb200.h)."""
     slots = 2 * n_leaves - 1 if n_leaves > 0 else 1
-    return 8 * (3 * n_nodes + 6 * n_free_nodes + 3 * slots)
+    return 8 * (4 * 3 * n_free_nodes + 3 * slots)
 
 
 # ------------------------------------------------------------------ batch
@@ -199,6 +224,7 @@ class Batch:
     node_base: np.ndarray              # (P+1,) int64 node offsets
     max_leaves: int
     smem_bytes: int
+    max_nf: int
     _packed_state: dict | None = field(default=None, repr=False)
     pinned: dict | None = field(default=None, repr=False)
 
@@ -239,56 +265,68 @@ def _pack(networks, bcs, probs) -> Batch:
     P = len(probs)
     desc = np.zeros(P, dtype=nat.PROBLEM_DTYPE)
     node_base = np.zeros(P + 1, dtype=np.int64)
-    topo_slot: dict[bytes, tuple[int, int, int]] = {}
+    topo_slot: dict[bytes, tuple[int, int]] = {}
     plan_slot: dict[int, int] = {}
-    inc_node, inc, elem_ab, plans = [], [], [], []
-    n_inc = n_elem_shared = n_plan = 0
-    elem_base = 0
-    X, mass, EL, EA = [], [], [], []
-    max_leaves, smem = 0, 0
+    inc, plans, ell_other = [], [], []
+    n_inc = n_plan = n_ell = 0
+    elem_base = ellv_base = 0
+    X, mass, EL, EA, inc_node, elem_ab, ell_L, ell_EA = [], [], [], [], [], [], [], []
+    any_nonuniform = False
+    max_leaves = smem = max_nf = 0
     for i, p in enumerate(probs):
         t = p.topo
         if p.topo_key not in topo_slot:
-            topo_slot[p.topo_key] = (n_inc, n_elem_shared, len(inc_node))
-            inc_node.append(t.inc_node)
+            topo_slot[p.topo_key] = (n_inc, n_ell)
             inc.append(t.inc)
-            elem_ab.append(t.elem_ab)
+            ell_other.append(t.ell_other.reshape(-1))
             n_inc += len(t.inc)
-            n_elem_shared += len(t.elem_ab)
-        inc_b, ab_b, _ = topo_slot[p.topo_key]
+            n_ell += t.ell_other.size
+        inc_b, ell_b = topo_slot[p.topo_key]
         nf = 3 * t.n_free_nodes
         if nf not in plan_slot:
             plan_slot[nf] = n_plan
             plans.append(t.plan)
             n_plan += len(t.plan)
         emod, area, _ = p.network.material_columns()
+        ea = emod * area
+        L = p.network.reference_lengths()
+        uniform = bool(ea.size == 0 or np.all(ea == ea[0]))
         d = desc[i]
         d["node_base"] = node_base[i]
         d["elem_base"] = elem_base
         d["inc_base"] = inc_b
         d["plan_base"] = plan_slot[nf]
+        d["ell_base"] = ell_b
+        d["ellv_base"] = ellv_base
         d["n_nodes"] = p.n_nodes
         d["n_free_nodes"] = t.n_free_nodes
         d["n_elems"] = p.network.n_elements
         d["cluster"] = 1
+        d["ell_stride"] = t.ell_other.shape[1]
+        d["ell_slots_a"] = t.ell_slots_a
+        d["ell_slots_b"] = t.ell_slots_b
+        d["flags"] = nat.PF_EA_UNIFORM if uniform else 0
         d["volume"] = p.network.volume
+        d["ea"] = ea[0] if ea.size else 0.0
         d["F"] = p.F.reshape(9)
         node_base[i + 1] = node_base[i] + p.n_nodes
         X.append(p.X.reshape(-1))
         mass.append(p.node_mass)
-        EL.append(p.network.reference_lengths())
-        EA.append(emod * area)
+        EL.append(L)
+        EA.append(ea)
+        inc_node.append(t.inc_node)
+        elem_ab.append(t.elem_ab)
+        valid = t.ell_other.reshape(-1) >= 0
+        eidx = t.ell_elem.reshape(-1)
+        ell_L.append(np.where(valid, L[eidx] if L.size else 1.0, 1.0))
+        if not uniform:
+            any_nonuniform = True
+        ell_EA.append(np.where(valid, ea[eidx] if ea.size else 0.0, 0.0))
+        ellv_base += t.ell_other.size
         elem_base += p.network.n_elements
         max_leaves = max(max_leaves, t.n_leaves)
+        max_nf = max(max_nf, 3 * t.n_free_nodes)
         smem = max(smem, cta_smem_bytes(p.n_nodes, t.n_free_nodes, t.n_leaves))
-    # incidence and element endpoint arrays are shared per topology but the
-    # kernel indexes inc_node per node and elem_ab per element, so expand the
-    # per-node / per-element ones to the problem's own offsets
-    inc_node_full = []
-    ab_full = []
-    for p in probs:
-        inc_node_full.append(p.topo.inc_node)
-        ab_full.append(p.topo.elem_ab)
 
     def cat(parts, dtype, width=None):
         if not parts:
@@ -297,14 +335,17 @@ def _pack(networks, bcs, probs) -> Batch:
 
     arrays = dict(
         X=cat(X, np.float64), node_mass=cat(mass, np.float64),
-        inc_node=cat(inc_node_full, np.int32, 2), inc=cat(inc, np.int32, 2),
-        elem_ab=cat(ab_full, np.int32, 2), elem_L=cat(EL, np.float64),
+        inc_node=cat(inc_node, np.int32, 2), inc=cat(inc, np.int32, 2),
+        elem_ab=cat(elem_ab, np.int32, 2), elem_L=cat(EL, np.float64),
         elem_EA=cat(EA, np.float64), plans=cat(plans, np.int32),
+        ell_other=cat(ell_other, np.int32), ell_L=cat(ell_L, np.float64),
     )
+    if any_nonuniform:
+        arrays["ell_EA"] = cat(ell_EA, np.float64)
     # order: longest first (nodes as the work proxy) for the dynamic queue
     arrays["order"] = np.argsort(-node_base[1:] + node_base[:-1], kind="stable").astype(np.int32)
     return Batch(networks=networks, bcs=bcs, problems=probs, desc=desc, arrays=arrays,
-                 node_base=node_base, max_leaves=max_leaves, smem_bytes=smem)
+                 node_base=node_base, max_leaves=max_leaves, smem_bytes=smem, max_nf=max_nf)
 
 
 # ------------------------------------------------------------------ device
@@ -357,16 +398,36 @@ class DeviceBatch:
         raw = torch.from_numpy(desc.view(np.uint8).copy())
         return raw.to(self.device, non_blocking=True)
 
+    def default_threads(self) -> int:
+        """Smallest CTA (multiple of 32, >= 64) that covers the pairwise
+        chains and keeps <= MAX_DOFS_PER_THREAD DOFs per thread; large
+        problems get 1024 threads for latency hiding."""
+        h = self.host
+        need = max(64, 8 * h.max_leaves, math.ceil(h.max_nf / MAX_DOFS_PER_THREAD))
+        if h.max_nf > 2048:
+            need = max(need, 1024)
+        return min(MAX_CTA_THREADS, 32 * math.ceil(need / 32))
+
+    @property
+    def work(self):
+        if getattr(self, "_work", None) is None:
+            self._work = _torch().empty(3 * int(self.host.node_base[-1]) + 1, dtype=_torch().float64,
+                                        device=self.device)
+        return self._work
+
     def frb_batch(self, desc_t, u, f, results, queue) -> nat.FrbBatch:
         t = self.t
         b = nat.FrbBatch()
         b.n_problems = self.host.n_problems
         b.smem_bytes = self.host.smem_bytes
+        b.max_nf = self.host.max_nf
         b.problems = desc_t.data_ptr()
         b.order = t["order"].data_ptr()
-        for k in ("X", "node_mass", "inc_node", "inc", "elem_ab", "elem_L", "elem_EA", "plans"):
-            setattr(b, k, t[k].data_ptr() if t[k].numel() else None)
+        for k in ("X", "node_mass", "inc_node", "inc", "elem_ab", "elem_L", "elem_EA", "plans",
+                  "ell_other", "ell_L", "ell_EA"):
+            setattr(b, k, t[k].data_ptr() if k in t and t[k].numel() else None)
         b.u, b.f = u.data_ptr(), f.data_ptr()
+        b.work = self.work.data_ptr()
         b.results = results.data_ptr()
         b.queue = queue.data_ptr()
         return b
@@ -378,7 +439,7 @@ class DeviceBatch:
         strategy = strategy or TeamBatched()
         if isinstance(strategy, NaiveLoop):
             raise NotImplementedError("NaiveLoop per-operation dispatch is not provided on the B200 path")
-        threads = max(64, 32 * math.ceil(8 * self.host.max_leaves / 32))
+        threads = self.default_threads()
         grid = 0
         if isinstance(strategy, TeamBatched):
             if strategy.team_size is not None:
@@ -386,10 +447,12 @@ class DeviceBatch:
             grid = strategy.teams or 0
         elif isinstance(strategy, SerialReference):
             grid = 1
-        if threads < 8 * self.host.max_leaves or threads > MAX_CTA_THREADS:
+        h = self.host
+        if (threads < 8 * h.max_leaves or threads > MAX_CTA_THREADS
+                or h.max_nf > MAX_DOFS_PER_THREAD * threads):
             raise nat.NativeError(nat.FRB_E_TOO_LARGE,
-                                  f"team_size {threads} cannot hold {self.host.max_leaves} "
-                                  "pairwise leaves (cluster path needed)")
+                                  f"team_size {threads} cannot hold {h.max_leaves} pairwise leaves / "
+                                  f"{h.max_nf} free DOFs (cluster path needed)")
         n = int(self.host.node_base[-1])
         dev = self.device
         u = torch.empty(3 * n, dtype=torch.float64, device=dev)

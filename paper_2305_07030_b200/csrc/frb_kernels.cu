@@ -1,4 +1,4 @@
-// frb_kernels.cu -- persistent dynamic-relaxation kernel for sm_100a.
+// frb_kernels.cu -- persistent dynamic-relaxation kernel for sm_100a (K1).
 //
 // One CTA owns one fiber network at a time, pulled from a device work queue
 // (the spec's TeamBatched strategy; the paper's "one team per
@@ -7,27 +7,39 @@
 // the kernel; finalize_result (:549-564) runs in its epilogue.
 //
 // Bit-exactness contract.  Every FP64 operation is an
-// explicit __d{add,sub,mul,div,sqrt}_rn intrinsic, so no FMA contraction or
-// reassociation can occur; the evaluation order of each reference line is
-// reproduced literally:
+// explicit round-to-nearest operation (intrinsics, or the branch-free
+// fast paths of frb_arith.cuh that are bit-identical to them), so no FMA
+// contraction or reassociation can occur; each reference line keeps its
+// evaluation order:
 //   * fiber length sqrt((dx*dx + dz*dz) + dy*dy)        (einsum, :206)
 //   * coef = (EA*(l-L)) / (L*l), nd = d*coef           (:210-211)
 //   * per node f = A + B, A = 0 - nd_e1 - nd_e2 ... over role-a elements in
 //     ascending id, B = 0 + nd... over role b          (bincount, :214-218)
-//   * the three reductions follow NumPy's pairwise tree (plan.py): each
-//     thread accumulates one stride-8 chain of one leaf in order, the
-//     8 chains of a leaf sit in 8 consecutive lanes and fold with xor
-//     shuffles 1,2,4 (= ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7))), tails are
-//     added in order, then leaves combine level by level in SMEM.
+//   * the three reductions follow NumPy's pairwise tree (plan.py): thread
+//     8*leaf + j sums the stride-8 chain j of its leaf in order, the 8
+//     chains of a leaf sit in 8 consecutive lanes and fold with xor shuffles
+//     1, 2, 4 (= ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7))), tails are added in
+//     order, then leaves combine level by level in SMEM.
 //
-// Memory layout per CTA (dynamic SMEM, FP64):
-//   pos  [3N]   current positions X+u of every node (the gather source)
-//   fbuf [2][nf] internal force on free DOFs, ping-pong (current / previous)
-//   slot [3][2L-1] pairwise-tree slots for the three reductions
-// Thread-private registers hold u and v for the <= 17 DOFs a thread owns
-// (its pairwise chain plus at most one tail element), so the state of the
-// relaxation never round-trips through HBM.  Read-only network data
-// (X, mass, incidence lists, L, EA) is streamed through L1/L2.
+// Work split per iteration (one CTA, T threads, DOF d owned by thread d % T):
+//   F  force    thread per free node: gather over its incidence slots -> f
+//   A  per DOF  k_hat, sq = (u k_hat) u, sq2 = (u m) u, ff = f f
+//   C  chains   thread per (leaf, chain): ordered sums of sq, sq2, ff
+//   T  tree     warp 0: pairwise combine, c, residual, convergence
+//   U  per DOF  a = -f/m - c v, two half kicks, drift, new positions
+// Only C is sequential, and only over <= 16 additions per thread; all
+// divisions / square roots run DOF- or node-parallel.
+//
+// Memory layout per CTA (dynamic SMEM, FP64, nf = 3 * free nodes):
+//   pos  [3][NF]  free-node positions X+u (SoA; conflict-free gathers).
+//                 Between F and U it is dead and holds sq (flat, by DOF).
+//   fcur [nf]     f from F; after A it holds ff
+//   fprv [nf]     f of the previous iteration; after A the current f
+//   sq2  [nf]
+//   slot [2L-1][3] pairwise-tree slots
+// u and v of a thread's <= 8 DOFs live in registers.  Fixed-node positions
+// (constant unless the BC ramps) sit in global scratch and are read through
+// L1, as are masses, X and the slot-major incidence table.
 
 #include <cuda_runtime.h>
 #include <math.h>
@@ -36,11 +48,11 @@
 #include <string.h>
 
 #include "frb200.h"
+#include "frb_arith.cuh"
 
 namespace {
 
-constexpr int kMaxThreads = 512;
-constexpr int kMaxOwn = 17;          // 16 chain elements + 1 tail element
+constexpr int kMaxThreads = 1024;
 constexpr int kMaxWarps = kMaxThreads / 32;
 constexpr double kCollapse = 1e-12;  // microsolver.py:30
 
@@ -49,40 +61,22 @@ __device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a,
 __device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ double ddiv(double a, double b) { return __ddiv_rn(a, b); }
 __device__ __forceinline__ double dsqrt(double a) { return __dsqrt_rn(a); }
+__device__ __forceinline__ double qnan() { return __longlong_as_double(0x7ff8000000000000ULL); }
 
 // sqrt(einsum("ij,ij->i", d, d)) for 3 columns == sqrt((x*x + z*z) + y*y)
-__device__ __forceinline__ double seg_len(double dx, double dy, double dz) {
-  return dsqrt(dadd(dadd(dmul(dx, dx), dmul(dz, dz)), dmul(dy, dy)));
+__device__ __forceinline__ double len2(double dx, double dy, double dz) {
+  return dadd(dadd(dmul(dx, dx), dmul(dz, dz)), dmul(dy, dy));
 }
+__device__ __forceinline__ double seg_len(double dx, double dy, double dz) { return dsqrt(len2(dx, dy, dz)); }
 
-struct Plan {
-  int n_leaves, n_levels, root;
-  const int* leaf_start;
-  const int* leaf_size;
-  const int* level_off;
-  const int* op_dst;
-  const int* op_left;
-  const int* op_right;
-};
-
-__device__ __forceinline__ Plan load_plan(const int* flat) {
-  Plan p;
-  p.n_leaves = flat[0];
-  p.n_levels = flat[1];
-  p.root = flat[2];
-  const int L = p.n_leaves, H = p.n_levels, K = L > 0 ? L - 1 : 0;
-  p.leaf_start = flat + 4;
-  p.leaf_size = p.leaf_start + L;
-  p.level_off = p.leaf_size + L;
-  p.op_dst = p.level_off + H + 1;
-  p.op_left = p.op_dst + K;
-  p.op_right = p.op_left + K;
-  return p;
-}
+// ------------------------------------------------------------------ problem view
 
 struct Net {
   int N, NF, nf, M;
-  double dt, hdt, volume;
+  int S, SA, SB, ea_uniform;
+  int L;  // pairwise leaves
+  int n_levels, root;
+  double dt, hdt, volume, ea;
   double g[9];  // F - I
   const double* X;
   const double* mass;
@@ -91,22 +85,36 @@ struct Net {
   const int2* eab;
   const double* EL;
   const double* EA;
-  Plan plan;
+  const int* ell_o;
+  const double* ell_L;
+  const double* ell_EA;
+  const int* leaf_start;
+  const int* leaf_size;
+  const int* level_off;
+  const int* op_dst;
+  const int* op_left;
+  const int* op_right;
+  double* pfix;  // fixed-node positions, AoS [N-NF][3] (global scratch)
+  int64_t node_base;
 };
 
-__device__ __forceinline__ Net load_net(const frb_batch& b, int p) {
+__device__ void load_net(Net& n, const frb_batch& b, int p) {
   const frb_problem& P = b.problems[p];
-  Net n;
   n.N = P.n_nodes;
   n.NF = P.n_free_nodes;
   n.nf = 3 * P.n_free_nodes;
   n.M = P.n_elems;
+  n.S = P.ell_stride;
+  n.SA = P.ell_slots_a;
+  n.SB = P.ell_slots_b;
+  n.ea_uniform = P.flags & FRB_PF_EA_UNIFORM;
   n.dt = P.dt;
   n.hdt = dmul(0.5, P.dt);
   n.volume = P.volume;
+  n.ea = P.ea;
   for (int r = 0; r < 3; ++r)
-    for (int c = 0; c < 3; ++c)
-      n.g[3 * r + c] = dsub(P.F[3 * r + c], r == c ? 1.0 : 0.0);
+    for (int c = 0; c < 3; ++c) n.g[3 * r + c] = dsub(P.F[3 * r + c], r == c ? 1.0 : 0.0);
+  n.node_base = P.node_base;
   n.X = b.X + 3 * P.node_base;
   n.mass = b.node_mass + P.node_base;
   n.incn = reinterpret_cast<const int2*>(b.inc_node) + P.node_base;
@@ -114,8 +122,21 @@ __device__ __forceinline__ Net load_net(const frb_batch& b, int p) {
   n.eab = reinterpret_cast<const int2*>(b.elem_ab) + P.elem_base;
   n.EL = b.elem_L + P.elem_base;
   n.EA = b.elem_EA + P.elem_base;
-  n.plan = load_plan(b.plans + P.plan_base);
-  return n;
+  n.ell_o = b.ell_other + P.ell_base;
+  n.ell_L = b.ell_L + P.ellv_base;
+  n.ell_EA = b.ell_EA ? b.ell_EA + P.ellv_base : nullptr;
+  n.pfix = b.work ? b.work + 3 * P.node_base : nullptr;
+  const int* flat = b.plans + P.plan_base;
+  n.L = flat[0];
+  n.n_levels = flat[1];
+  n.root = flat[2];
+  const int K = n.L > 0 ? n.L - 1 : 0;
+  n.leaf_start = flat + 4;
+  n.leaf_size = n.leaf_start + n.L;
+  n.level_off = n.leaf_size + n.L;
+  n.op_dst = n.level_off + n.n_levels + 1;
+  n.op_left = n.op_dst + K;
+  n.op_right = n.op_left + K;
 }
 
 // u_presc[i][j] = x @ (F-I)^T as OpenBLAS evaluates it (microsolver.py:320-322):
@@ -135,12 +156,19 @@ __device__ __forceinline__ double fixed_u(const Net& n, int node, int j, double 
   return dmul(alpha, presc(n, node, j));
 }
 
-// Position sources: the solver's SMEM array, or X + u recomputed from global
-// memory (one-shot internal_forces).  Both yield the same rounded X + u.
-struct PosSmem {
-  const double* p;
-  __device__ __forceinline__ double operator()(int node, int axis) const { return p[3 * node + axis]; }
+// ------------------------------------------------------------------ positions
+
+// Solver positions: free nodes from SMEM (SoA), fixed nodes from the global
+// scratch (AoS).
+struct PosSolver {
+  const double* p;     // [3][NF]
+  const double* pfix;  // [N-NF][3]
+  int NF;
+  __device__ __forceinline__ double operator()(int node, int axis) const {
+    return node < NF ? p[axis * NF + node] : pfix[3 * (node - NF) + axis];
+  }
 };
+// X + u recomputed from global memory (one-shot internal_forces).
 struct PosGlobal {
   const double* X;
   const double* u;
@@ -149,11 +177,25 @@ struct PosGlobal {
   }
 };
 
-// Internal force at node i (gather over its incidence lists, element order
-// per role).  Returns true if an incident element collapsed (l < 1e-12 L).
+// ------------------------------------------------------------------ gathers
+
+// One element's end-force vector nd = d*coef with d = P[b] - P[a] (exact
+// intrinsics; used off the hot path).  Returns true when it collapsed.
+__device__ __forceinline__ bool element_force(double dx, double dy, double dz, double L, double EA,
+                                              double& nx, double& ny, double& nz) {
+  const double l = seg_len(dx, dy, dz);
+  const double coef = ddiv(dmul(EA, dsub(l, L)), dmul(L, l));
+  nx = dmul(dx, coef);
+  ny = dmul(dy, coef);
+  nz = dmul(dz, coef);
+  return l < dmul(kCollapse, L);
+}
+
+// Internal force at node i from the CSR incidence lists (all nodes; used by
+// the epilogue, the singular path and internal_forces).
 template <class Pos>
-__device__ __forceinline__ bool node_force(const Net& n, const Pos& pos, int i, double& fx,
-                                           double& fy, double& fz) {
+__device__ __forceinline__ bool node_force_csr(const Net& n, const Pos& pos, int i, double& fx,
+                                               double& fy, double& fz) {
   const int2 meta = n.incn[i];
   const int first = meta.x;
   const int na = meta.y & 0xffff;
@@ -164,25 +206,17 @@ __device__ __forceinline__ bool node_force(const Net& n, const Pos& pos, int i, 
   for (int k = 0; k < na + nb; ++k) {
     const int2 e = n.inc[first + k];
     const double ox = pos(e.x, 0), oy = pos(e.x, 1), oz = pos(e.x, 2);
-    const bool role_a = k < na;
-    // d = P[b] - P[a]
-    const double dx = role_a ? dsub(ox, px) : dsub(px, ox);
-    const double dy = role_a ? dsub(oy, py) : dsub(py, oy);
-    const double dz = role_a ? dsub(oz, pz) : dsub(pz, oz);
-    const double L = __ldg(n.EL + e.y);
-    const double EA = __ldg(n.EA + e.y);
-    const double l = seg_len(dx, dy, dz);
-    bad |= l < dmul(kCollapse, L);
-    const double coef = ddiv(dmul(EA, dsub(l, L)), dmul(L, l));
-    const double ndx = dmul(dx, coef), ndy = dmul(dy, coef), ndz = dmul(dz, coef);
-    if (role_a) {  // bincount(ia, -nd): A = 0 + (-nd) + ...
-      ax = dsub(ax, ndx);
-      ay = dsub(ay, ndy);
-      az = dsub(az, ndz);
-    } else {       // bincount(ib, nd)
-      bx = dadd(bx, ndx);
-      by = dadd(by, ndy);
-      bz = dadd(bz, ndz);
+    double nx, ny, nz;
+    if (k < na) {
+      bad |= element_force(dsub(ox, px), dsub(oy, py), dsub(oz, pz), n.EL[e.y], n.EA[e.y], nx, ny, nz);
+      ax = dsub(ax, nx);  // bincount(ia, -nd): 0 + (-nd) + ...
+      ay = dsub(ay, ny);
+      az = dsub(az, nz);
+    } else {
+      bad |= element_force(dsub(px, ox), dsub(py, oy), dsub(pz, oz), n.EL[e.y], n.EA[e.y], nx, ny, nz);
+      bx = dadd(bx, nx);  // bincount(ib, nd)
+      by = dadd(by, ny);
+      bz = dadd(bz, nz);
     }
   }
   fx = dadd(ax, bx);
@@ -191,13 +225,69 @@ __device__ __forceinline__ bool node_force(const Net& n, const Pos& pos, int i, 
   return bad;
 }
 
-// numpy argmin over (l - eps) with NaN-first semantics: a precedes b?
-__device__ __forceinline__ bool argmin_before(double va, int ia, double vb, int ib) {
-  const bool na = isnan(va), nb = isnan(vb);
-  if (na != nb) return na;
-  if (!na && va != vb) return va < vb;
-  return ia < ib;
+// Exact (intrinsic) fallbacks, kept out of line so the rare path does not
+// inflate the register allocation of the hot loops.
+__device__ __noinline__ void exact_len_coef(double dx, double dy, double dz, double L, double EA, double& l,
+                                            double& coef) {
+  l = seg_len(dx, dy, dz);
+  coef = ddiv(dmul(EA, dsub(l, L)), dmul(L, l));
 }
+__device__ __noinline__ double exact_div(double a, double b) { return ddiv(a, b); }
+
+// a / b through the branch-free fast path, exact fallback out of line.
+__device__ __forceinline__ double div_rn(double a, double b) {
+  bool ok;
+  const double q = frb_arith::div_fast(a, b, ok);
+  return ok ? q : exact_div(a, b);
+}
+
+// Internal force at free node i from the slot-major table, one slot at a
+// time (the fast square root / division are branch-free; the rare exact
+// fallback is an out-of-line call).  The per-role sums accumulate strictly in
+// slot (= element) order.  Padding slots (other < 0) contribute an exact
+// +0.0: subtracting +0.0 is the identity, and adding it is too because a
+// role sum that starts at +0.0 never becomes -0.0.
+__device__ __forceinline__ bool node_force_ell(const Net& n, const PosSolver& pos, int i, double& fx,
+                                               double& fy, double& fz) {
+  const int S = n.S, SA = n.SA, ns = n.SA + n.SB;
+  const double px = pos(i, 0), py = pos(i, 1), pz = pos(i, 2);
+  double ax = 0.0, ay = 0.0, az = 0.0, bx = 0.0, by = 0.0, bz = 0.0;
+  bool bad = false;
+#pragma unroll 2
+  for (int k = 0; k < ns; ++k) {
+    const int o = __ldg(n.ell_o + k * S + i);
+    if (o < 0) continue;  // padding
+    const double L = __ldg(n.ell_L + k * S + i);
+    const double EA = n.ea_uniform ? n.ea : __ldg(n.ell_EA + k * S + i);
+    const double ox = pos(o, 0), oy = pos(o, 1), oz = pos(o, 2);
+    const bool role_a = k < SA;
+    // d = P[b] - P[a]
+    const double dx = role_a ? dsub(ox, px) : dsub(px, ox);
+    const double dy = role_a ? dsub(oy, py) : dsub(py, oy);
+    const double dz = role_a ? dsub(oz, pz) : dsub(pz, oz);
+    bool ok1, ok2;
+    double l = frb_arith::sqrt_fast(len2(dx, dy, dz), ok1);
+    double coef = frb_arith::div_fast(dmul(EA, dsub(l, L)), dmul(L, l), ok2);
+    if (!(ok1 && ok2)) exact_len_coef(dx, dy, dz, L, EA, l, coef);
+    bad |= l < dmul(kCollapse, L);
+    const double nx = dmul(dx, coef), ny = dmul(dy, coef), nz = dmul(dz, coef);
+    if (role_a) {  // bincount(ia, -nd): 0 + (-nd) + ...
+      ax = dsub(ax, nx);
+      ay = dsub(ay, ny);
+      az = dsub(az, nz);
+    } else {  // bincount(ib, nd)
+      bx = dadd(bx, nx);
+      by = dadd(by, ny);
+      bz = dadd(bz, nz);
+    }
+  }
+  fx = dadd(ax, bx);
+  fy = dadd(ay, by);
+  fz = dadd(az, bz);
+  return bad;
+}
+
+// ------------------------------------------------------------------ block helpers
 
 struct Scalars {
   double c, residual, r_ref, threshold;
@@ -205,6 +295,14 @@ struct Scalars {
   int ired[kMaxWarps];
   int problem, done, converged, singular;
 };
+
+// numpy argmin over (l - eps) with NaN-first semantics: does (va, ia) come first?
+__device__ __forceinline__ bool argmin_before(double va, int ia, double vb, int ib) {
+  const bool na = isnan(va), nb = isnan(vb);
+  if (na != nb) return na;
+  if (!na && va != vb) return va < vb;
+  return ia < ib;
+}
 
 // Block-wide deterministic sum of 9 per-thread values (fixed shuffle tree,
 // then warps in order).  Result valid in thread 0.
@@ -227,20 +325,20 @@ __device__ void block_sum9(double v[9], Scalars& sc) {
   __syncthreads();
 }
 
-// Singular-element path: reference raises SingularElementError naming
+// Singular-element path: the reference raises SingularElementError naming
 // argmin(length - eps_len) over all elements (microsolver.py:207-209).
 template <class Pos>
 __device__ int singular_argmin(const Net& n, const Pos& pos, Scalars& sc) {
+  constexpr int kNone = 0x7fffffff;
   double best = 0.0;
-  int besti = 0x7fffffff;
+  int besti = kNone;
   for (int e = threadIdx.x; e < n.M; e += blockDim.x) {
     const int2 ab = n.eab[e];
     const double dx = dsub(pos(ab.y, 0), pos(ab.x, 0));
     const double dy = dsub(pos(ab.y, 1), pos(ab.x, 1));
     const double dz = dsub(pos(ab.y, 2), pos(ab.x, 2));
-    const double L = n.EL[e];
-    const double v = dsub(seg_len(dx, dy, dz), dmul(kCollapse, L));
-    if (besti == 0x7fffffff || argmin_before(v, e, best, besti)) {
+    const double v = dsub(seg_len(dx, dy, dz), dmul(kCollapse, n.EL[e]));
+    if (besti == kNone || argmin_before(v, e, best, besti)) {
       best = v;
       besti = e;
     }
@@ -249,7 +347,7 @@ __device__ int singular_argmin(const Net& n, const Pos& pos, Scalars& sc) {
   for (int o = 16; o > 0; o >>= 1) {
     const double ov = __shfl_down_sync(0xffffffffu, best, o);
     const int oi = __shfl_down_sync(0xffffffffu, besti, o);
-    if (oi != 0x7fffffff && (besti == 0x7fffffff || argmin_before(ov, oi, best, besti))) {
+    if (oi != kNone && (besti == kNone || argmin_before(ov, oi, best, besti))) {
       best = ov;
       besti = oi;
     }
@@ -266,7 +364,7 @@ __device__ int singular_argmin(const Net& n, const Pos& pos, Scalars& sc) {
     int bi = sc.ired[0];
     for (int w = 1; w < nw; ++w) {
       const int oi = sc.ired[w];
-      if (oi != 0x7fffffff && (bi == 0x7fffffff || argmin_before(sc.red[w], oi, b, bi))) {
+      if (oi != kNone && (bi == kNone || argmin_before(sc.red[w], oi, b, bi))) {
         b = sc.red[w];
         bi = oi;
       }
@@ -277,24 +375,23 @@ __device__ int singular_argmin(const Net& n, const Pos& pos, Scalars& sc) {
   return result;
 }
 
-// Check every element's current length (init and ramp iterations, when
-// fixed-fixed elements move).  Sets sc.singular.
-__device__ void check_all_elements(const Net& n, const double* pos, Scalars& sc) {
+// Length check of every element (init and ramp iterations, when elements
+// between fixed nodes move).  Sets sc.singular.
+__device__ void check_all_elements(const Net& n, const PosSolver& pos, Scalars& sc) {
   bool bad = false;
   for (int e = threadIdx.x; e < n.M; e += blockDim.x) {
     const int2 ab = n.eab[e];
-    const double dx = dsub(pos[3 * ab.y], pos[3 * ab.x]);
-    const double dy = dsub(pos[3 * ab.y + 1], pos[3 * ab.x + 1]);
-    const double dz = dsub(pos[3 * ab.y + 2], pos[3 * ab.x + 2]);
+    const double dx = dsub(pos(ab.y, 0), pos(ab.x, 0));
+    const double dy = dsub(pos(ab.y, 1), pos(ab.x, 1));
+    const double dz = dsub(pos(ab.y, 2), pos(ab.x, 2));
     bad |= seg_len(dx, dy, dz) < dmul(kCollapse, n.EL[e]);
   }
   if (bad) sc.singular = 1;
 }
 
-__device__ __forceinline__ void set_fixed_positions(const Net& n, double* pos, double alpha,
-                                                    bool ramp) {
+__device__ __forceinline__ void set_fixed_positions(const Net& n, double alpha, bool ramp) {
   for (int i = n.NF + threadIdx.x; i < n.N; i += blockDim.x)
-    for (int j = 0; j < 3; ++j) pos[3 * i + j] = dadd(n.X[3 * i + j], fixed_u(n, i, j, alpha, ramp));
+    for (int j = 0; j < 3; ++j) n.pfix[3 * (i - n.NF) + j] = dadd(n.X[3 * i + j], fixed_u(n, i, j, alpha, ramp));
 }
 
 __device__ __forceinline__ double ramp_alpha(int it_plus_1, int ramp) {
@@ -303,15 +400,46 @@ __device__ __forceinline__ double ramp_alpha(int it_plus_1, int ramp) {
   return x < 1.0 ? x : 1.0;
 }
 
-__device__ void solve_one(const frb_batch& b, const frb_config& cfg, int p, double* smem,
-                          Scalars& sc) {
-  const Net n = load_net(b, p);
+__device__ void write_singular(const frb_batch& b, int p, int bad, int iters) {
+  if (threadIdx.x == 0) {
+    frb_result& r = b.results[p];
+    r.status = FRB_STATUS_SINGULAR;
+    r.bad_element = bad;
+    r.iters = iters;
+    r.converged = 0;
+    r.final_residual = qnan();
+    r.r_ref = qnan();
+    r.energy_residual = qnan();
+  }
+}
+
+// Quotients num(k)/den(k) for the DOFs k < MAXK a thread owns (has(k)); use
+// (k, q) consumes them in DOF order.  den(k) == 0 yields q = 0 (the caller
+// decides what a zero denominator means).
+template <int MAXK, class Has, class Num, class Den, class Use>
+__device__ __forceinline__ void batched_div(Has has, Num num, Den den, Use use) {
+#pragma unroll
+  for (int k = 0; k < MAXK; ++k) {
+    if (has(k)) {
+      const double dk = den(k);
+      use(k, dk == 0.0 ? 0.0 : div_rn(num(k), dk));
+    }
+  }
+}
+
+// ------------------------------------------------------------------ the solve
+
+template <int MAXK>
+__device__ void solve_one(const frb_batch& b, const frb_config& cfg, int p, double* smem, Scalars& sc,
+                          const Net& n) {
   const int T = blockDim.x, t = threadIdx.x, lane = t & 31;
-  const int L = n.plan.n_leaves;
-  double* pos = smem;
-  double* fb0 = pos + 3 * n.N;
-  double* fb1 = fb0 + n.nf;
-  double* slot = fb1 + n.nf;
+  const int NF = n.NF, nf = n.nf, L = n.L;
+  double* pos = smem;        // [3][NF]; sq between phases F and U
+  double* fcur = pos + nf;   // [nf]
+  double* fprv = fcur + nf;  // [nf]
+  double* sq2 = fprv + nf;   // [nf]
+  double* slot = sq2 + nf;   // [2L-1][3]
+  const PosSolver P{pos, n.pfix, NF};
 
   const bool adaptive = cfg.damping == FRB_DAMPING_ADAPTIVE;
   const int ramp_n = cfg.bc_ramp_iters;
@@ -320,146 +448,131 @@ __device__ void solve_one(const frb_batch& b, const frb_config& cfg, int p, doub
   const double dt = n.dt, hdt = n.hdt;
   double alpha = ramp ? -1.0 : 1.0;  // -1: fixed nodes still at their zero init
 
-  // ---- DOF ownership: thread t <-> chain (leaf t/8, lane j = t%8) --------
+  // thread t owns DOFs d = t + k*T (k < MAXK)
+  auto has = [&](int k) { return t + k * T < nf; };
+  double u[MAXK], v[MAXK];
+#pragma unroll
+  for (int k = 0; k < MAXK; ++k) u[k] = v[k] = 0.0;
+
+  // pairwise-chain role: thread t < 8L sums chain j of leaf t/8
   const bool chain = t < 8 * L;
   const int leaf = t >> 3, j = t & 7;
-  int lstart = 0, q = 0, body = 0, nt = 0;
+  int lstart = 0, q = 0, nt = 0;
   if (chain) {
-    lstart = n.plan.leaf_start[leaf];
-    const int lsize = n.plan.leaf_size[leaf];
+    lstart = n.leaf_start[leaf];
+    const int lsize = n.leaf_size[leaf];
     q = lsize >= 8 ? (lsize >> 3) : 0;
-    body = 8 * q;
-    nt = lsize - body;
+    nt = lsize - 8 * q;
   }
-  const int nown = chain ? q + (j < nt ? 1 : 0) : 0;
-  double u[kMaxOwn], v[kMaxOwn];
 
-  if (t == 0) {
-    sc.singular = 0;
-    sc.done = 0;
-    sc.converged = 0;
-    sc.threshold = __longlong_as_double(0x7ff0000000000000ULL);  // +inf until set
-  }
   // ---- prologue: BCs, initial positions (microsolver.py:400-411) ---------
-  for (int k = t; k < 3 * n.NF; k += T) pos[k] = dadd(n.X[k], 0.0);
-  set_fixed_positions(n, pos, alpha, ramp);
+  for (int i = t; i < NF; i += T)
+    for (int a = 0; a < 3; ++a) pos[a * NF + i] = dadd(n.X[3 * i + a], 0.0);
+  set_fixed_positions(n, alpha, ramp);
   __syncthreads();
-  check_all_elements(n, pos, sc);
+  check_all_elements(n, P, sc);
   __syncthreads();
   if (sc.singular) {
-    const int bad = singular_argmin(n, PosSmem{pos}, sc);
-    if (t == 0) {
-      frb_result& r = b.results[p];
-      r.status = FRB_STATUS_SINGULAR;
-      r.bad_element = bad;
-      r.iters = 0;
-      r.converged = 0;
-    }
+    write_singular(b, p, singular_argmin(n, P, sc), 0);
     __syncthreads();
     return;
   }
-  // initial internal forces on free nodes (:413-420)
-  for (int i = t; i < n.NF; i += T) {
+  // initial internal forces on free nodes (:413-420), kept as f_prev
+  for (int i = t; i < NF; i += T) {
     double fx, fy, fz;
-    node_force(n, PosSmem{pos}, i, fx, fy, fz);
-    fb0[3 * i] = fx;
-    fb0[3 * i + 1] = fy;
-    fb0[3 * i + 2] = fz;
+    node_force_ell(n, P, i, fx, fy, fz);
+    fprv[3 * i] = fx;
+    fprv[3 * i + 1] = fy;
+    fprv[3 * i + 2] = fz;
   }
   __syncthreads();
   // a = -f/m (:428-430), then iteration 0's kick + drift (:443-448)
-#pragma unroll
-  for (int k = 0; k < kMaxOwn; ++k) {
-    if (k < nown) {
-      const int d = k < q ? lstart + j + 8 * k : lstart + body + j;
-      const double a = ddiv(-fb0[d], n.mass[d / 3]);
-      v[k] = dadd(0.0, dmul(hdt, a));
-      u[k] = dadd(0.0, dmul(dt, v[k]));
-      pos[d] = dadd(n.X[d], u[k]);
-    }
-  }
+  batched_div<MAXK>(
+      has, [&](int k) { return -fprv[t + k * T]; }, [&](int k) { return __ldg(n.mass + (t + k * T) / 3); },
+      [&](int k, double a) {
+        const int d = t + k * T;
+        v[k] = dadd(0.0, dmul(hdt, a));
+        u[k] = dadd(0.0, dmul(dt, v[k]));
+        const int node = d / 3;
+        pos[(d - 3 * node) * NF + node] = dadd(__ldg(n.X + d), u[k]);
+      });
   if (ramp) {  // iteration 0's ramp step (:449-453)
     alpha = ramp_alpha(1, ramp_n);
-    set_fixed_positions(n, pos, alpha, ramp);
+    set_fixed_positions(n, alpha, ramp);
   }
   __syncthreads();
 
   // ---- relaxation loop (microsolver.py:434-530) ---------------------------
-  int cur = 1;
   int it = 0;
   for (;; ++it) {
-    double* fcur = cur ? fb1 : fb0;
-    const double* fprev = cur ? fb0 : fb1;
-
-    // internal forces at the drifted positions (:456-465)
+    // F: internal forces at the drifted positions (:456-465)
     bool bad = false;
-    for (int i = t; i < n.NF; i += T) {
+    for (int i = t; i < NF; i += T) {
       double fx, fy, fz;
-      bad |= node_force(n, PosSmem{pos}, i, fx, fy, fz);
+      bad |= node_force_ell(n, P, i, fx, fy, fz);
       fcur[3 * i] = fx;
       fcur[3 * i + 1] = fy;
       fcur[3 * i + 2] = fz;
     }
     if (bad) sc.singular = 1;
-    if (ramp && it < ramp_n) check_all_elements(n, pos, sc);
+    if (ramp && it < ramp_n) check_all_elements(n, P, sc);
     __syncthreads();
     if (sc.singular) {
-      const int badi = singular_argmin(n, PosSmem{pos}, sc);
-      if (t == 0) {
-        frb_result& r = b.results[p];
-        r.status = FRB_STATUS_SINGULAR;
-        r.bad_element = badi;
-        r.iters = it;
-        r.converged = 0;
-      }
+      write_singular(b, p, singular_argmin(n, P, sc), it);
       __syncthreads();
       return;
     }
 
-    // per-DOF damping / residual terms + pairwise chains (:467-499)
-    if ((t & ~31) < 8 * L) {  // warp holds at least one chain
-      double r0 = 0.0, r1 = 0.0, r2 = 0.0;     // chains: u k u, u m u, f f
-      double t0 = 0.0, t1 = 0.0, t2 = 0.0;     // this lane's tail element
-#pragma unroll
-      for (int k = 0; k < kMaxOwn; ++k) {
-        if (k < nown) {
-          const int d = k < q ? lstart + j + 8 * k : lstart + body + j;
+    // A: k_hat = (f - f_prev)/(dt v) where dt v != 0 else 0, clamped with
+    // np.maximum(k_hat, 0) (:468-476); sq = (u k_hat) u, sq2 = (u m) u,
+    // ff = f f (:489).  Outputs: sq -> pos (flat), sq2, ff -> fcur, f -> fprv.
+    batched_div<MAXK>(
+        has, [&](int k) { return dsub(fcur[t + k * T], fprv[t + k * T]); },
+        [&](int k) { return adaptive ? dmul(dt, v[k]) : 0.0; },
+        [&](int k, double kh) {
+          const int d = t + k * T;
           const double f = fcur[d];
-          const double ff = dmul(f, f);
-          double sq = 0.0, sq2 = 0.0;
           if (adaptive) {
-            const double den = dmul(dt, v[k]);
-            const double num = dsub(f, fprev[d]);
-            double kh = den != 0.0 ? ddiv(num, den) : 0.0;
-            kh = (kh > 0.0 || isnan(kh)) ? kh : 0.0;  // np.maximum(kh, 0.0)
-            sq = dmul(dmul(u[k], kh), u[k]);
-            sq2 = dmul(dmul(u[k], n.mass[d / 3]), u[k]);
+            kh = (kh > 0.0 || isnan(kh)) ? kh : 0.0;
+            pos[d] = dmul(dmul(u[k], kh), u[k]);
+            sq2[d] = dmul(dmul(u[k], __ldg(n.mass + d / 3)), u[k]);
           }
-          if (k < q) {
-            if (k == 0) {
-              r0 = sq;
-              r1 = sq2;
-              r2 = ff;
-            } else {
-              r0 = dadd(r0, sq);
-              r1 = dadd(r1, sq2);
-              r2 = dadd(r2, ff);
-            }
-          } else {
-            t0 = sq;
-            t1 = sq2;
-            t2 = ff;
+          fcur[d] = dmul(f, f);
+          fprv[d] = f;
+        });
+    __syncthreads();
+
+    // C: ordered chain sums of one leaf chain + fold + tails -> leaf slots
+    if ((t & ~31) < 8 * L) {  // warp holds at least one chain
+      double r0 = 0.0, r1 = 0.0, r2 = 0.0;
+      double t0 = 0.0, t1 = 0.0, t2 = 0.0;
+      if (chain) {
+        int d = lstart + j;
+        if (q > 0) {
+          r0 = pos[d];
+          r1 = sq2[d];
+          r2 = fcur[d];
+          for (int k = 1; k < q; ++k) {
+            d += 8;
+            r0 = dadd(r0, pos[d]);
+            r1 = dadd(r1, sq2[d]);
+            r2 = dadd(r2, fcur[d]);
           }
         }
+        if (j < nt) {
+          const int dtail = lstart + 8 * q + j;
+          t0 = pos[dtail];
+          t1 = sq2[dtail];
+          t2 = fcur[dtail];
+        }
+        if (!adaptive) r0 = r1 = t0 = t1 = 0.0;
       }
-      // fold the 8 chains of the leaf: xor 1, 2, 4
 #pragma unroll
       for (int o = 1; o < 8; o <<= 1) {
         r0 = dadd(r0, __shfl_xor_sync(0xffffffffu, r0, o));
         r1 = dadd(r1, __shfl_xor_sync(0xffffffffu, r1, o));
         r2 = dadd(r2, __shfl_xor_sync(0xffffffffu, r2, o));
       }
-      // tails in order (tail i lives on lane i of the group)
       const int base = lane & ~7;
       const int my_nt = chain ? nt : 0;
 #pragma unroll
@@ -481,12 +594,12 @@ __device__ void solve_one(const frb_batch& b, const frb_config& cfg, int p, doub
     }
     __syncthreads();
 
-    // tree combine + scalar bookkeeping (warp 0)
+    // T: tree combine + scalar bookkeeping (warp 0)
     if (t < 32) {
-      const Plan& pl = n.plan;
-      for (int lev = 0; lev < pl.n_levels; ++lev) {
-        for (int k = pl.level_off[lev] + lane; k < pl.level_off[lev + 1]; k += 32) {
-          const int dd = pl.op_dst[k], la = pl.op_left[k], rb = pl.op_right[k];
+      for (int lev = 0; lev < n.n_levels; ++lev) {
+        const int k1 = n.level_off[lev + 1];
+        for (int k = n.level_off[lev] + lane; k < k1; k += 32) {
+          const int dd = n.op_dst[k], la = n.op_left[k], rb = n.op_right[k];
           slot[3 * dd] = dadd(slot[3 * la], slot[3 * rb]);
           slot[3 * dd + 1] = dadd(slot[3 * la + 1], slot[3 * rb + 1]);
           slot[3 * dd + 2] = dadd(slot[3 * la + 2], slot[3 * rb + 2]);
@@ -496,9 +609,9 @@ __device__ void solve_one(const frb_batch& b, const frb_config& cfg, int p, doub
       if (t == 0) {
         double s_sq = 0.0, s_m = 0.0, s_f = 0.0;
         if (L > 0) {
-          s_sq = slot[3 * pl.root];
-          s_m = slot[3 * pl.root + 1];
-          s_f = slot[3 * pl.root + 2];
+          s_sq = slot[3 * n.root];
+          s_m = slot[3 * n.root + 1];
+          s_f = slot[3 * n.root + 2];
         }
         // np.sum adds the pairwise result to the identity 0.0
         s_sq = dadd(0.0, s_sq);
@@ -534,108 +647,119 @@ __device__ void solve_one(const frb_batch& b, const frb_config& cfg, int p, doub
     }
     __syncthreads();
 
-    // accelerations, second half-kick (:501-507); then the next iteration's
-    // first half-kick and drift (:443-453) unless finished
+    // U: accelerations and second half-kick (:501-507); then the next
+    // iteration's first half-kick and drift (:443-453) unless finished
     const double c = sc.c;
     const bool done = sc.done != 0;
-#pragma unroll
-    for (int k = 0; k < kMaxOwn; ++k) {
-      if (k < nown) {
-        const int d = k < q ? lstart + j + 8 * k : lstart + body + j;
-        const double a = dsub(ddiv(-fcur[d], n.mass[d / 3]), dmul(c, v[k]));
-        v[k] = dadd(v[k], dmul(hdt, a));
-        if (!done) {
+    batched_div<MAXK>(
+        has, [&](int k) { return -fprv[t + k * T]; }, [&](int k) { return __ldg(n.mass + (t + k * T) / 3); },
+        [&](int k, double fm) {
+          const double a = dsub(fm, dmul(c, v[k]));
           v[k] = dadd(v[k], dmul(hdt, a));
-          u[k] = dadd(u[k], dmul(dt, v[k]));
-          pos[d] = dadd(n.X[d], u[k]);
-        }
-      }
-    }
+          if (!done) {
+            const int d = t + k * T;
+            v[k] = dadd(v[k], dmul(hdt, a));
+            u[k] = dadd(u[k], dmul(dt, v[k]));
+            const int node = d / 3;
+            pos[(d - 3 * node) * NF + node] = dadd(__ldg(n.X + d), u[k]);
+          }
+        });
     if (!done && ramp && alpha < 1.0) {
       alpha = ramp_alpha(it + 2, ramp_n);
-      set_fixed_positions(n, pos, alpha, ramp);
+      set_fixed_positions(n, alpha, ramp);
     }
-    cur ^= 1;
     __syncthreads();
     if (done) break;
   }
 
   // ---- epilogue: outputs in solver order + stress (:549-564, :285-299) ----
-  const double* ffin = cur ? fb0 : fb1;  // toggled after the last iteration
-  double* uo = b.u + 3 * b.problems[p].node_base;
-  double* fo = b.f + 3 * b.problems[p].node_base;
+  double* uo = b.u + 3 * n.node_base;
+  double* fo = b.f + 3 * n.node_base;
 #pragma unroll
-  for (int k = 0; k < kMaxOwn; ++k) {
-    if (k < nown) {
-      const int d = k < q ? lstart + j + 8 * k : lstart + body + j;
+  for (int k = 0; k < MAXK; ++k) {
+    if (has(k)) {
+      const int d = t + k * T;
       uo[d] = u[k];
+      fo[d] = fprv[d];
+      const int node = d / 3;
+      pos[(d - 3 * node) * NF + node] = dadd(__ldg(n.X + d), u[k]);  // pos held sq
     }
   }
-  for (int d = t; d < n.nf; d += T) fo[d] = ffin[d];
+  __syncthreads();
   double s9[9];
 #pragma unroll
   for (int r = 0; r < 9; ++r) s9[r] = 0.0;
-  for (int i = n.NF + t; i < n.N; i += T) {
+  for (int i = NF + t; i < n.N; i += T) {
     double f3[3];
-    node_force(n, PosSmem{pos}, i, f3[0], f3[1], f3[2]);
+    node_force_csr(n, P, i, f3[0], f3[1], f3[2]);
     for (int jj = 0; jj < 3; ++jj) {
       uo[3 * i + jj] = fixed_u(n, i, jj, alpha, ramp);
       fo[3 * i + jj] = f3[jj];
     }
-    // S = r^T x over boundary nodes, x = X + u (= pos)
+    // S = r^T x over boundary nodes (sorted ids == solver order), x = X + u
     for (int a = 0; a < 3; ++a)
-      for (int c3 = 0; c3 < 3; ++c3) s9[3 * a + c3] = dadd(s9[3 * a + c3], dmul(f3[a], pos[3 * i + c3]));
+      for (int c3 = 0; c3 < 3; ++c3) s9[3 * a + c3] = dadd(s9[3 * a + c3], dmul(f3[a], P(i, c3)));
   }
   block_sum9(s9, sc);
   if (t == 0) {
     frb_result& r = b.results[p];
     const double two_v = dmul(2.0, n.volume);
     for (int a = 0; a < 3; ++a)
-      for (int c3 = 0; c3 < 3; ++c3)
-        r.avg_stress[3 * a + c3] = ddiv(dadd(s9[3 * a + c3], s9[3 * c3 + a]), two_v);
+      for (int c3 = 0; c3 < 3; ++c3) r.avg_stress[3 * a + c3] = ddiv(dadd(s9[3 * a + c3], s9[3 * c3 + a]), two_v);
     r.status = sc.converged ? FRB_STATUS_CONVERGED : FRB_STATUS_MAX_ITERS;
     r.converged = sc.converged;
     r.iters = it + 1;
     r.bad_element = -1;
     r.final_residual = sc.residual;
-    r.r_ref = (full_bc_iter <= it) ? sc.r_ref : __longlong_as_double(0x7ff8000000000000ULL);
-    r.energy_residual = __longlong_as_double(0x7ff8000000000000ULL);
+    r.r_ref = (full_bc_iter <= it) ? sc.r_ref : qnan();
+    r.energy_residual = qnan();
     for (int e = 0; e < 4; ++e) r.energy[e] = 0.0;
   }
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(kMaxThreads, 1)
-    frb_relax_cta_kernel(frb_batch b, frb_config cfg) {
+template <int MAXK, int MAXT>
+__global__ void __launch_bounds__(MAXT, 1) frb_relax_cta_kernel(frb_batch b, frb_config cfg) {
   extern __shared__ __align__(16) double smem[];
   __shared__ Scalars sc;
+  __shared__ Net net;
   for (;;) {
-    if (threadIdx.x == 0) sc.problem = atomicAdd(b.queue, 1);
+    if (threadIdx.x == 0) {
+      const int idx = atomicAdd(b.queue, 1);
+      sc.problem = idx;
+      if (idx < b.n_problems) {
+        load_net(net, b, b.order ? b.order[idx] : idx);
+        sc.singular = 0;
+        sc.done = 0;
+        sc.converged = 0;
+        sc.threshold = __longlong_as_double(0x7ff0000000000000ULL);  // +inf until set
+      }
+    }
     __syncthreads();
     const int idx = sc.problem;
-    __syncthreads();
     if (idx >= b.n_problems) break;
-    const int p = b.order ? b.order[idx] : idx;
-    solve_one(b, cfg, p, smem, sc);
+    solve_one<MAXK>(b, cfg, b.order ? b.order[idx] : idx, smem, sc, net);
   }
 }
 
 // One-shot forces for every node of problem blockIdx.x (reference
 // internal_forces, microsolver.py:221-238), same gather code as the solver.
-__global__ void __launch_bounds__(kMaxThreads)
-    frb_forces_kernel(frb_batch b, const double* __restrict__ u, double* __restrict__ f) {
+__global__ void __launch_bounds__(256) frb_forces_kernel(frb_batch b, const double* __restrict__ u,
+                                                          double* __restrict__ f) {
   __shared__ Scalars sc;
+  __shared__ Net n;
   const int p = blockIdx.x;
-  const frb_problem& P = b.problems[p];
-  const Net n = load_net(b, p);
-  const PosGlobal pos{n.X, u + 3 * P.node_base};
-  double* fp = f + 3 * P.node_base;
-  if (threadIdx.x == 0) sc.singular = 0;
+  if (threadIdx.x == 0) {
+    load_net(n, b, p);
+    sc.singular = 0;
+  }
   __syncthreads();
+  const PosGlobal pos{n.X, u + 3 * n.node_base};
+  double* fp = f + 3 * n.node_base;
   bool bad = false;
   for (int i = threadIdx.x; i < n.N; i += blockDim.x) {
     double fx, fy, fz;
-    bad |= node_force(n, pos, i, fx, fy, fz);
+    bad |= node_force_csr(n, pos, i, fx, fy, fz);
     fp[3 * i] = fx;
     fp[3 * i + 1] = fy;
     fp[3 * i + 2] = fz;
@@ -650,10 +774,23 @@ __global__ void __launch_bounds__(kMaxThreads)
   }
 }
 
+// out[6*i + ...]: div_fast, div ok flag, __ddiv_rn, sqrt_fast, sqrt ok flag, __dsqrt_rn
+__global__ void arith_selftest_kernel(const double* a, const double* b, int n, double* out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  bool ok;
+  out[6 * i] = frb_arith::div_fast(a[i], b[i], ok);
+  out[6 * i + 1] = ok ? 1.0 : 0.0;
+  out[6 * i + 2] = __ddiv_rn(a[i], b[i]);
+  out[6 * i + 3] = frb_arith::sqrt_fast(a[i], ok);
+  out[6 * i + 4] = ok ? 1.0 : 0.0;
+  out[6 * i + 5] = __dsqrt_rn(a[i]);
+}
+
 thread_local char g_err[512] = "";
 
-int set_err(int code, const char* fmt, const char* what) {
-  snprintf(g_err, sizeof g_err, fmt, what);
+int set_err(int code, const char* msg) {
+  snprintf(g_err, sizeof g_err, "%s", msg);
   return code;
 }
 
@@ -661,6 +798,41 @@ int cuda_check(cudaError_t e, const char* where) {
   if (e == cudaSuccess) return FRB_OK;
   snprintf(g_err, sizeof g_err, "%s: %s", where, cudaGetErrorString(e));
   return FRB_E_CUDA;
+}
+
+template <int MAXK, int MAXT>
+int launch_cta(const frb_batch* batch, const frb_config* cfg, int threads, int grid, cudaStream_t s) {
+  const int smem = batch->smem_bytes;
+  auto kern = frb_relax_cta_kernel<MAXK, MAXT>;
+  int rc = cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
+                      "cudaFuncSetAttribute");
+  if (rc) return rc;
+  if (grid <= 0) {
+    int dev = 0, nsm = 0, per_sm = 0;
+    rc = cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+    if (rc) return rc;
+    rc = cuda_check(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev), "cudaDeviceGetAttribute");
+    if (rc) return rc;
+    rc = cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem),
+                    "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
+    if (rc) return rc;
+    if (per_sm < 1) return set_err(FRB_E_TOO_LARGE, "kernel does not fit on an SM");
+    grid = per_sm * nsm;
+  }
+  if (grid > batch->n_problems) grid = batch->n_problems;
+  rc = cuda_check(cudaMemsetAsync(batch->queue, 0, sizeof(int32_t), s), "cudaMemsetAsync");
+  if (rc) return rc;
+  kern<<<grid, threads, smem, s>>>(*batch, *cfg);
+  return cuda_check(cudaGetLastError(), "frb_relax_cta_kernel launch");
+}
+
+template <int MAXT>
+int dispatch_k(const frb_batch* batch, const frb_config* cfg, int threads, int grid, cudaStream_t s, int k) {
+  if (k <= 1) return launch_cta<1, MAXT>(batch, cfg, threads, grid, s);
+  if (k <= 2) return launch_cta<2, MAXT>(batch, cfg, threads, grid, s);
+  if (k <= 4) return launch_cta<4, MAXT>(batch, cfg, threads, grid, s);
+  if (k <= 6) return launch_cta<6, MAXT>(batch, cfg, threads, grid, s);
+  return launch_cta<FRB_MAX_DOFS_PER_THREAD, MAXT>(batch, cfg, threads, grid, s);
 }
 
 }  // namespace
@@ -683,51 +855,55 @@ int frb_device_info(int device, int* n_sm, int* smem_optin, int* cc_major, int* 
 }
 
 int64_t frb_cta_smem_bytes(int32_t n_nodes, int32_t n_free_nodes, int32_t n_leaves) {
+  (void)n_nodes;
   const int64_t slots = n_leaves > 0 ? 2 * static_cast<int64_t>(n_leaves) - 1 : 1;
-  return 8 * (3 * static_cast<int64_t>(n_nodes) + 6 * static_cast<int64_t>(n_free_nodes) + 3 * slots);
+  return 8 * (12 * static_cast<int64_t>(n_free_nodes) + 3 * slots);
 }
 
 int frb_solve_batch(const frb_batch* batch, const frb_config* cfg, int block_threads, int grid_ctas,
                     void* stream) {
-  if (!batch || !cfg) return set_err(FRB_E_INVALID, "%s", "null batch or config");
-  if (batch->n_problems < 0) return set_err(FRB_E_INVALID, "%s", "negative problem count");
+  if (!batch || !cfg) return set_err(FRB_E_INVALID, "null batch or config");
+  if (batch->n_problems < 0) return set_err(FRB_E_INVALID, "negative problem count");
   if (batch->n_problems == 0) return FRB_OK;
   if (block_threads < 32 || block_threads > kMaxThreads || block_threads % 32)
-    return set_err(FRB_E_INVALID, "%s", "block_threads must be a multiple of 32 in [32, 512]");
-  if (cfg->energy_check_interval > 0)
-    return set_err(FRB_E_UNSUPPORTED, "%s", "energy ledger not in this build");
-  if (cfg->max_iters <= 0) return set_err(FRB_E_INVALID, "%s", "max_iters must be > 0");
-  const int smem = batch->smem_bytes;
-  int dev = 0;
+    return set_err(FRB_E_INVALID, "block_threads must be a multiple of 32 in [32, 1024]");
+  if (!batch->work) return set_err(FRB_E_INVALID, "work buffer missing");
+  if (cfg->energy_check_interval > 0) return set_err(FRB_E_UNSUPPORTED, "energy ledger not in this build");
+  if (cfg->max_iters <= 0) return set_err(FRB_E_INVALID, "max_iters must be > 0");
+  int dev = 0, optin = 0;
   int rc = cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
   if (rc) return rc;
-  int optin = 0, nsm = 0;
-  rc = frb_device_info(dev, &nsm, &optin, nullptr, nullptr);
+  rc = cuda_check(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev),
+                  "cudaDeviceGetAttribute");
   if (rc) return rc;
-  if (smem > optin) return set_err(FRB_E_TOO_LARGE, "%s", "problem exceeds shared memory per CTA");
-  rc = cuda_check(cudaFuncSetAttribute(frb_relax_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
-                  "cudaFuncSetAttribute");
-  if (rc) return rc;
+  if (batch->smem_bytes > optin) return set_err(FRB_E_TOO_LARGE, "problem exceeds shared memory per CTA");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (grid_ctas <= 0) {
-    int per_sm = 0;
-    rc = cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, frb_relax_cta_kernel, block_threads, smem),
-                    "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
-    if (rc) return rc;
-    if (per_sm < 1) return set_err(FRB_E_TOO_LARGE, "%s", "kernel does not fit on an SM");
-    grid_ctas = per_sm * nsm;
-  }
-  if (grid_ctas > batch->n_problems) grid_ctas = batch->n_problems;
-  rc = cuda_check(cudaMemsetAsync(batch->queue, 0, sizeof(int32_t), s), "cudaMemsetAsync");
-  if (rc) return rc;
-  frb_relax_cta_kernel<<<grid_ctas, block_threads, smem, s>>>(*batch, *cfg);
-  return cuda_check(cudaGetLastError(), "frb_relax_cta_kernel launch");
+  // u, v register arrays sized for the DOFs per thread of the largest problem;
+  // the launch bound (and with it the register budget) follows the CTA size
+  const int per_thread = (batch->max_nf + block_threads - 1) / block_threads;
+  if (per_thread > FRB_MAX_DOFS_PER_THREAD)
+    return set_err(FRB_E_TOO_LARGE, "more than FRB_MAX_DOFS_PER_THREAD free DOFs per thread");
+  if (block_threads <= 256) return dispatch_k<256>(batch, cfg, block_threads, grid_ctas, s, per_thread);
+  if (block_threads <= 512) return dispatch_k<512>(batch, cfg, block_threads, grid_ctas, s, per_thread);
+  if (block_threads <= 768) return dispatch_k<768>(batch, cfg, block_threads, grid_ctas, s, per_thread);
+  return dispatch_k<1024>(batch, cfg, block_threads, grid_ctas, s, per_thread);
+}
+
+int frb_selftest_arith(const double* a, const double* b, int n, double* out, void* stream) {
+  if (n <= 0) return FRB_OK;
+  if (!a || !b || !out) return set_err(FRB_E_INVALID, "null argument");
+  arith_selftest_kernel<<<(n + 255) / 256, 256, 0, static_cast<cudaStream_t>(stream)>>>(a, b, n, out);
+  return cuda_check(cudaGetLastError(), "arith_selftest_kernel launch");
 }
 
 int frb_internal_forces(const frb_batch* batch, const double* u, double* f, void* stream) {
-  if (!batch || !u || !f) return set_err(FRB_E_INVALID, "%s", "null argument");
+  if (!batch || !u || !f) return set_err(FRB_E_INVALID, "null argument");
   if (batch->n_problems <= 0) return FRB_OK;
-  frb_forces_kernel<<<batch->n_problems, 256, 0, static_cast<cudaStream_t>(stream)>>>(*batch, u, f);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  int rc = cuda_check(cudaMemsetAsync(batch->results, 0, sizeof(frb_result) * batch->n_problems, s),
+                      "cudaMemsetAsync");
+  if (rc) return rc;
+  frb_forces_kernel<<<batch->n_problems, 256, 0, s>>>(*batch, u, f);
   return cuda_check(cudaGetLastError(), "frb_forces_kernel launch");
 }
 

@@ -1,0 +1,44 @@
+"""The C-ABI library loads without a GPU and exports every symbol that
+include/frb200.h declares; the ctypes struct mirrors match the header."""
+
+import ctypes as C
+import os
+import re
+
+from paper_2305_07030_b200 import _native as nat
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_functions():
+    text = open(os.path.join(ROOT, "include", "frb200.h")).read()
+    return sorted(set(re.findall(r"^\s*(?:int|int64_t|const char\*)\s+(frb_\w+)\s*\(", text, re.M)))
+
+
+def test_library_exports_every_declared_symbol():
+    lib = nat.lib()
+    names = declared_functions()
+    assert set(names) == set(nat.EXPORTS)
+    for name in names:
+        assert hasattr(lib, name), name
+    assert lib.frb_abi_version() == 1
+
+
+def test_struct_layouts():
+    assert C.sizeof(nat.FrbConfig) == 48
+    assert C.sizeof(nat.FrbBatch) == 16 + 18 * 8
+    assert nat.PROBLEM_DTYPE.itemsize == 176
+    assert nat.RESULT_DTYPE.itemsize == 144
+
+
+def test_cta_smem_bytes_matches_host_mirror():
+    from paper_2305_07030_b200.batch import cta_smem_bytes
+    for n, nf, L in [(3375, 2197, 64), (392, 150, 4), (8, 0, 0), (27, 1, 1)]:  # noqa
+        assert nat.lib().frb_cta_smem_bytes(n, nf, L) == cta_smem_bytes(n, nf, L)
+
+
+def test_invalid_arguments_fail_loudly():
+    lib = nat.lib()
+    rc = lib.frb_solve_batch(None, None, 128, 0, None)
+    assert rc == nat.FRB_E_INVALID
+    assert b"null" in lib.frb_last_error()
