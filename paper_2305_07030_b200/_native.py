@@ -36,7 +36,8 @@ class FrbBatch(C.Structure):
                 ("node_mass", C.c_void_p), ("inc_node", C.c_void_p), ("inc", C.c_void_p),
                 ("elem_ab", C.c_void_p), ("elem_L", C.c_void_p), ("elem_EA", C.c_void_p),
                 ("plans", C.c_void_p), ("ell_other", C.c_void_p), ("ell_L", C.c_void_p),
-                ("ell_EA", C.c_void_p), ("u", C.c_void_p), ("f", C.c_void_p), ("work", C.c_void_p),
+                ("ell_EA", C.c_void_p), ("ell_c", C.c_void_p), ("ff_ab", C.c_void_p),
+                ("ff_L", C.c_void_p), ("ff_EA", C.c_void_p), ("u", C.c_void_p), ("f", C.c_void_p), ("work", C.c_void_p),
                 ("results", C.c_void_p), ("queue", C.c_void_p)]
 
 
@@ -44,9 +45,10 @@ class FrbBatch(C.Structure):
 # / downloaded as raw bytes)
 PROBLEM_DTYPE = np.dtype([
     ("node_base", "<i8"), ("elem_base", "<i8"), ("inc_base", "<i8"), ("plan_base", "<i8"),
-    ("ell_base", "<i8"), ("ellv_base", "<i8"),
+    ("ell_base", "<i8"), ("ellv_base", "<i8"), ("ff_base", "<i8"), ("ffv_base", "<i8"),
     ("n_nodes", "<i4"), ("n_free_nodes", "<i4"), ("n_elems", "<i4"), ("cluster", "<i4"),
     ("ell_stride", "<i4"), ("ell_slots_a", "<i4"), ("ell_slots_b", "<i4"), ("flags", "<i4"),
+    ("n_ff", "<i4"), ("pad1", "<i4"),
     ("dt", "<f8"), ("volume", "<f8"), ("ea", "<f8"), ("F", "<f8", (9,)),
 ])
 PF_EA_UNIFORM = 1
@@ -55,7 +57,7 @@ RESULT_DTYPE = np.dtype([
     ("final_residual", "<f8"), ("r_ref", "<f8"), ("energy_residual", "<f8"),
     ("avg_stress", "<f8", (9,)), ("energy", "<f8", (4,)),
 ])
-assert PROBLEM_DTYPE.itemsize == 176 and RESULT_DTYPE.itemsize == 144
+assert PROBLEM_DTYPE.itemsize == 200 and RESULT_DTYPE.itemsize == 144
 
 
 class NativeError(RuntimeError):

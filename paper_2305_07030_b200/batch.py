@@ -121,6 +121,9 @@ class Topology:
     ell_elem: np.ndarray         # (SA+SB, S) int32 element per slot (0 on padding)
     ell_slots_a: int
     ell_slots_b: int
+    ell_c: np.ndarray            # (SA+SB, S) int32 index into ff list, -1 fixed/padding
+    ff_ab: np.ndarray            # (n_ff, 2) int32 endpoints of free-free elements
+    ff_elem: np.ndarray          # (n_ff,) element ids
 
 
 def _topology(network: FiberNetwork, node_rank: np.ndarray, n_free_nodes: int) -> Topology:
@@ -160,10 +163,20 @@ def _topology(network: FiberNetwork, node_rank: np.ndarray, n_free_nodes: int) -
     ell_elem[slot, snode[free]] = elem[order][free]
     sizes = PlanView(plan).leaf_size
     max_own = int(max(((z // 8) + (1 if z % 8 else 0)) if z >= 8 else 1 for z in sizes)) if len(sizes) else 1
+    # elements between two free nodes: their coefficient is computed once per
+    # iteration (fiber-parallel) and looked up by both endpoints' slots
+    ff_mask = (ia < nfn) & (ib < nfn)
+    ff_elem = np.flatnonzero(ff_mask)
+    ff_index = np.full(m, -1, dtype=np.int64)
+    ff_index[ff_elem] = np.arange(ff_elem.size)
+    ell_c = np.where(ell_other >= 0, ff_index[ell_elem], -1)
+    ell_c = np.where((ell_other >= 0) & (ell_other < nfn), ell_c, -1).astype(np.int32)
     return Topology(n_nodes=n, n_free_nodes=n_free_nodes, inc_node=inc_node, inc=inc,
                     elem_ab=np.stack([ia, ib], axis=1).astype(np.int32), plan=plan,
                     n_leaves=int(plan[0]), max_own=max_own, ell_other=ell_other,
-                    ell_elem=ell_elem, ell_slots_a=sa, ell_slots_b=sb)
+                    ell_elem=ell_elem, ell_slots_a=sa, ell_slots_b=sb, ell_c=ell_c,
+                    ff_ab=np.stack([ia[ff_elem], ib[ff_elem]], axis=1).astype(np.int32),
+                    ff_elem=ff_elem.astype(np.int64))
 
 
 _TOPO_CACHE: dict[bytes, Topology] = {}
@@ -203,10 +216,17 @@ def build_problem(network: FiberNetwork, bc: AffineBC, check_mass: bool = True) 
                        node_mass=node_mass, dt_base=dt_base, topo_key=key, topo=topo)
 
 
-def cta_smem_bytes(n_nodes: int, n_free_nodes: int, n_leaves: int) -> int:
-    """Mirror of frb_cta_smem_bytes (include/frb200.h)."""
-    slots = 2 * n_leaves - 1 if n_leaves > 0 else 1
-    return 8 * (4 * 3 * n_free_nodes + 3 * slots)
+def cta_smem_bytes(n_free_nodes: int, n_ff: int, n_leaves: int) -> int:
+    """Mirror of frb_cta_smem_bytes (include/frb200.h): positions / sq, f,
+    f_prev (8 B per free DOF each), sq2 / free-free coefficients, tree
+    slots, and the tree's combine program (int32, bounded by a height of
+    bit_length(L-1) + 1 levels)."""
+    nf = 3 * n_free_nodes
+    L = n_leaves
+    slots = 2 * L - 1 if L > 0 else 1
+    levels = (L - 1).bit_length() + 1 if L > 1 else 0
+    prog = (levels + 1) + 3 * (L - 1 if L > 0 else 0)
+    return 8 * (3 * nf + max(nf, n_ff) + 3 * slots) + 4 * ((prog + 1) & ~1)
 
 
 # ------------------------------------------------------------------ batch
@@ -267,21 +287,25 @@ def _pack(networks, bcs, probs) -> Batch:
     node_base = np.zeros(P + 1, dtype=np.int64)
     topo_slot: dict[bytes, tuple[int, int]] = {}
     plan_slot: dict[int, int] = {}
-    inc, plans, ell_other = [], [], []
-    n_inc = n_plan = n_ell = 0
-    elem_base = ellv_base = 0
+    inc, plans, ell_other, ell_c, ff_ab = [], [], [], [], []
+    n_inc = n_plan = n_ell = n_ffs = 0
+    elem_base = ellv_base = ffv_base = 0
+    ff_L, ff_EA = [], []
     X, mass, EL, EA, inc_node, elem_ab, ell_L, ell_EA = [], [], [], [], [], [], [], []
     any_nonuniform = False
     max_leaves = smem = max_nf = 0
     for i, p in enumerate(probs):
         t = p.topo
         if p.topo_key not in topo_slot:
-            topo_slot[p.topo_key] = (n_inc, n_ell)
+            topo_slot[p.topo_key] = (n_inc, n_ell, n_ffs)
             inc.append(t.inc)
             ell_other.append(t.ell_other.reshape(-1))
+            ell_c.append(t.ell_c.reshape(-1))
+            ff_ab.append(t.ff_ab)
             n_inc += len(t.inc)
             n_ell += t.ell_other.size
-        inc_b, ell_b = topo_slot[p.topo_key]
+            n_ffs += len(t.ff_ab)
+        inc_b, ell_b, ff_b = topo_slot[p.topo_key]
         nf = 3 * t.n_free_nodes
         if nf not in plan_slot:
             plan_slot[nf] = n_plan
@@ -298,6 +322,9 @@ def _pack(networks, bcs, probs) -> Batch:
         d["plan_base"] = plan_slot[nf]
         d["ell_base"] = ell_b
         d["ellv_base"] = ellv_base
+        d["ff_base"] = ff_b
+        d["ffv_base"] = ffv_base
+        d["n_ff"] = len(t.ff_elem)
         d["n_nodes"] = p.n_nodes
         d["n_free_nodes"] = t.n_free_nodes
         d["n_elems"] = p.network.n_elements
@@ -323,10 +350,13 @@ def _pack(networks, bcs, probs) -> Batch:
             any_nonuniform = True
         ell_EA.append(np.where(valid, ea[eidx] if ea.size else 0.0, 0.0))
         ellv_base += t.ell_other.size
+        ff_L.append(L[t.ff_elem])
+        ff_EA.append(ea[t.ff_elem])
+        ffv_base += len(t.ff_elem)
         elem_base += p.network.n_elements
         max_leaves = max(max_leaves, t.n_leaves)
         max_nf = max(max_nf, 3 * t.n_free_nodes)
-        smem = max(smem, cta_smem_bytes(p.n_nodes, t.n_free_nodes, t.n_leaves))
+        smem = max(smem, cta_smem_bytes(t.n_free_nodes, len(t.ff_elem), t.n_leaves))
 
     def cat(parts, dtype, width=None):
         if not parts:
@@ -339,9 +369,11 @@ def _pack(networks, bcs, probs) -> Batch:
         elem_ab=cat(elem_ab, np.int32, 2), elem_L=cat(EL, np.float64),
         elem_EA=cat(EA, np.float64), plans=cat(plans, np.int32),
         ell_other=cat(ell_other, np.int32), ell_L=cat(ell_L, np.float64),
+        ell_c=cat(ell_c, np.int32), ff_ab=cat(ff_ab, np.int32, 2), ff_L=cat(ff_L, np.float64),
     )
     if any_nonuniform:
         arrays["ell_EA"] = cat(ell_EA, np.float64)
+        arrays["ff_EA"] = cat(ff_EA, np.float64)
     # order: longest first (nodes as the work proxy) for the dynamic queue
     arrays["order"] = np.argsort(-node_base[1:] + node_base[:-1], kind="stable").astype(np.int32)
     return Batch(networks=networks, bcs=bcs, problems=probs, desc=desc, arrays=arrays,
@@ -424,7 +456,7 @@ class DeviceBatch:
         b.problems = desc_t.data_ptr()
         b.order = t["order"].data_ptr()
         for k in ("X", "node_mass", "inc_node", "inc", "elem_ab", "elem_L", "elem_EA", "plans",
-                  "ell_other", "ell_L", "ell_EA"):
+                  "ell_other", "ell_L", "ell_EA", "ell_c", "ff_ab", "ff_L", "ff_EA"):
             setattr(b, k, t[k].data_ptr() if k in t and t[k].numel() else None)
         b.u, b.f = u.data_ptr(), f.data_ptr()
         b.work = self.work.data_ptr()

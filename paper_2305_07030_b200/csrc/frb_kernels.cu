@@ -88,6 +88,11 @@ struct Net {
   const int* ell_o;
   const double* ell_L;
   const double* ell_EA;
+  const int* ell_c;
+  const int2* ff_ab;
+  const double* ff_L;
+  const double* ff_EA;
+  int n_ff;
   const int* leaf_start;
   const int* leaf_size;
   const int* level_off;
@@ -125,6 +130,11 @@ __device__ void load_net(Net& n, const frb_batch& b, int p) {
   n.ell_o = b.ell_other + P.ell_base;
   n.ell_L = b.ell_L + P.ellv_base;
   n.ell_EA = b.ell_EA ? b.ell_EA + P.ellv_base : nullptr;
+  n.ell_c = b.ell_c + P.ell_base;
+  n.ff_ab = reinterpret_cast<const int2*>(b.ff_ab) + P.ff_base;
+  n.ff_L = b.ff_L + P.ffv_base;
+  n.ff_EA = b.ff_EA ? b.ff_EA + P.ffv_base : nullptr;
+  n.n_ff = P.n_ff;
   n.pfix = b.work ? b.work + 3 * P.node_base : nullptr;
   const int* flat = b.plans + P.plan_base;
   n.L = flat[0];
@@ -226,11 +236,16 @@ __device__ __forceinline__ bool node_force_csr(const Net& n, const Pos& pos, int
 }
 
 // Exact (intrinsic) fallbacks, kept out of line so the rare path does not
-// inflate the register allocation of the hot loops.
-__device__ __noinline__ void exact_len_coef(double dx, double dy, double dz, double L, double EA, double& l,
-                                            double& coef) {
-  l = seg_len(dx, dy, dz);
-  coef = ddiv(dmul(EA, dsub(l, L)), dmul(L, l));
+// inflate the register allocation of the hot loops.  Results come back by
+// value (references would force the caller's values through local memory).
+struct LenCoef {
+  double l, coef;
+};
+__device__ __noinline__ LenCoef exact_len_coef(double dx, double dy, double dz, double L, double EA) {
+  LenCoef r;
+  r.l = seg_len(dx, dy, dz);
+  r.coef = ddiv(dmul(EA, dsub(r.l, L)), dmul(L, r.l));
+  return r;
 }
 __device__ __noinline__ double exact_div(double a, double b) { return ddiv(a, b); }
 
@@ -241,49 +256,98 @@ __device__ __forceinline__ double div_rn(double a, double b) {
   return ok ? q : exact_div(a, b);
 }
 
-// Internal force at free node i from the slot-major table, one slot at a
-// time (the fast square root / division are branch-free; the rare exact
-// fallback is an out-of-line call).  The per-role sums accumulate strictly in
-// slot (= element) order.  Padding slots (other < 0) contribute an exact
-// +0.0: subtracting +0.0 is the identity, and adding it is too because a
-// role sum that starts at +0.0 never becomes -0.0.
-__device__ __forceinline__ bool node_force_ell(const Net& n, const PosSolver& pos, int i, double& fx,
-                                               double& fy, double& fz) {
-  const int S = n.S, SA = n.SA, ns = n.SA + n.SB;
+// Length and force coefficient of one element through the fast paths.
+__device__ __forceinline__ LenCoef len_coef(double dx, double dy, double dz, double L, double EA) {
+  bool ok1, ok2;
+  LenCoef r;
+  r.l = frb_arith::sqrt_fast(len2(dx, dy, dz), ok1);
+  r.coef = frb_arith::div_fast(dmul(EA, dsub(r.l, L)), dmul(L, r.l), ok2);
+  if (!(ok1 && ok2)) r = exact_len_coef(dx, dy, dz, L, EA);
+  return r;
+}
+
+// Slot-major incidence view of the free nodes (see frb200.h: ell_*).
+struct Ell {
+  const int* __restrict__ o;      // other endpoint, -1 = padding
+  const int* __restrict__ c;      // free-free element index, -1 = other is fixed
+  const double* __restrict__ L;   // reference length (used when c < 0)
+  const double* __restrict__ EA;  // E*A per slot, nullptr when uniform
+  double ea;
+  int SA, SB, S;
+};
+
+// Sum over one role's slots of free node i, in slot (= element) order:
+// role a accumulates 0 - nd - nd ..., role b 0 + nd + nd ...  Elements to a
+// free neighbour take the coefficient computed once in phase F1 (coef[c])
+// and recompute d = P[b] - P[a] from the same operands, so nd is bitwise the
+// value the reference's per-element pass produces; elements to a fixed
+// neighbour are evaluated here.  Padding slots are skipped (exact: the
+// reference adds nothing there).
+template <bool ROLE_A>
+__device__ __forceinline__ void ell_role(const Ell& E, const double* __restrict__ coef, int k0, int k1, int i,
+                                         const PosSolver& pos, double px, double py, double pz, double& sx,
+                                         double& sy, double& sz, bool& bad) {
+  for (int k = k0; k < k1; ++k) {
+    const int o = __ldg(E.o + k * E.S + i);
+    if (o < 0) continue;
+    const int c = __ldg(E.c + k * E.S + i);
+    const double ox = pos(o, 0), oy = pos(o, 1), oz = pos(o, 2);
+    const double dx = ROLE_A ? dsub(ox, px) : dsub(px, ox);
+    const double dy = ROLE_A ? dsub(oy, py) : dsub(py, oy);
+    const double dz = ROLE_A ? dsub(oz, pz) : dsub(pz, oz);
+    double cf;
+    if (c >= 0) {
+      cf = coef[c];
+    } else {
+      const double L = __ldg(E.L + k * E.S + i);
+      const double EA = E.EA ? __ldg(E.EA + k * E.S + i) : E.ea;
+      const LenCoef lc = len_coef(dx, dy, dz, L, EA);
+      bad |= lc.l < dmul(kCollapse, L);
+      cf = lc.coef;
+    }
+    if (ROLE_A) {  // bincount(ia, -nd): 0 + (-nd) + ...
+      sx = dsub(sx, dmul(dx, cf));
+      sy = dsub(sy, dmul(dy, cf));
+      sz = dsub(sz, dmul(dz, cf));
+    } else {  // bincount(ib, nd)
+      sx = dadd(sx, dmul(dx, cf));
+      sy = dadd(sy, dmul(dy, cf));
+      sz = dadd(sz, dmul(dz, cf));
+    }
+  }
+}
+
+// Internal force at free node i (phase F2).
+__device__ __forceinline__ bool node_force_ell(const Ell& E, const double* __restrict__ coef,
+                                               const PosSolver& pos, int i, double& fx, double& fy,
+                                               double& fz) {
   const double px = pos(i, 0), py = pos(i, 1), pz = pos(i, 2);
   double ax = 0.0, ay = 0.0, az = 0.0, bx = 0.0, by = 0.0, bz = 0.0;
   bool bad = false;
-#pragma unroll 2
-  for (int k = 0; k < ns; ++k) {
-    const int o = __ldg(n.ell_o + k * S + i);
-    if (o < 0) continue;  // padding
-    const double L = __ldg(n.ell_L + k * S + i);
-    const double EA = n.ea_uniform ? n.ea : __ldg(n.ell_EA + k * S + i);
-    const double ox = pos(o, 0), oy = pos(o, 1), oz = pos(o, 2);
-    const bool role_a = k < SA;
-    // d = P[b] - P[a]
-    const double dx = role_a ? dsub(ox, px) : dsub(px, ox);
-    const double dy = role_a ? dsub(oy, py) : dsub(py, oy);
-    const double dz = role_a ? dsub(oz, pz) : dsub(pz, oz);
-    bool ok1, ok2;
-    double l = frb_arith::sqrt_fast(len2(dx, dy, dz), ok1);
-    double coef = frb_arith::div_fast(dmul(EA, dsub(l, L)), dmul(L, l), ok2);
-    if (!(ok1 && ok2)) exact_len_coef(dx, dy, dz, L, EA, l, coef);
-    bad |= l < dmul(kCollapse, L);
-    const double nx = dmul(dx, coef), ny = dmul(dy, coef), nz = dmul(dz, coef);
-    if (role_a) {  // bincount(ia, -nd): 0 + (-nd) + ...
-      ax = dsub(ax, nx);
-      ay = dsub(ay, ny);
-      az = dsub(az, nz);
-    } else {  // bincount(ib, nd)
-      bx = dadd(bx, nx);
-      by = dadd(by, ny);
-      bz = dadd(bz, nz);
-    }
-  }
+  ell_role<true>(E, coef, 0, E.SA, i, pos, px, py, pz, ax, ay, az, bad);
+  ell_role<false>(E, coef, E.SA, E.SA + E.SB, i, pos, px, py, pz, bx, by, bz, bad);
   fx = dadd(ax, bx);
   fy = dadd(ay, by);
   fz = dadd(az, bz);
+  return bad;
+}
+
+// Phase F1: coefficient EA (l - L) / (L l) of every free-free element, once
+// per iteration, fiber-parallel (microsolver.py:196-211).
+__device__ __forceinline__ bool free_free_coefs(const Net& n, const double* __restrict__ pos, int NF,
+                                                double* __restrict__ coef) {
+  bool bad = false;
+  for (int e = threadIdx.x; e < n.n_ff; e += blockDim.x) {
+    const int2 ab = __ldg(n.ff_ab + e);
+    const double L = __ldg(n.ff_L + e);
+    const double EA = n.ff_EA ? __ldg(n.ff_EA + e) : n.ea;
+    const double dx = dsub(pos[ab.y], pos[ab.x]);
+    const double dy = dsub(pos[NF + ab.y], pos[NF + ab.x]);
+    const double dz = dsub(pos[2 * NF + ab.y], pos[2 * NF + ab.x]);
+    const LenCoef lc = len_coef(dx, dy, dz, L, EA);
+    bad |= lc.l < dmul(kCollapse, L);
+    coef[e] = lc.coef;
+  }
   return bad;
 }
 
@@ -437,9 +501,22 @@ __device__ void solve_one(const frb_batch& b, const frb_config& cfg, int p, doub
   double* pos = smem;        // [3][NF]; sq between phases F and U
   double* fcur = pos + nf;   // [nf]
   double* fprv = fcur + nf;  // [nf]
-  double* sq2 = fprv + nf;   // [nf]
-  double* slot = sq2 + nf;   // [2L-1][3]
+  double* sq2 = fprv + nf;   // [max(nf, n_ff)]: F1 coefficients, then sq2
+  double* slot = sq2 + (nf > n.n_ff ? nf : n.n_ff);  // [2L-1][3]
   const PosSolver P{pos, n.pfix, NF};
+  // the tree's combine program lives in SMEM (warp 0 walks it every iteration)
+  const int n_ops = L > 0 ? L - 1 : 0;
+  int* prog = reinterpret_cast<int*>(slot + 3 * (L > 0 ? 2 * L - 1 : 1));  // [levels+1][3*ops]
+  int* lvl_s = prog;
+  int* dst_s = lvl_s + n.n_levels + 1;
+  int* lft_s = dst_s + n_ops;
+  int* rgt_s = lft_s + n_ops;
+  for (int k = t; k <= n.n_levels; k += T) lvl_s[k] = n.level_off[k];
+  for (int k = t; k < n_ops; k += T) {
+    dst_s[k] = n.op_dst[k];
+    lft_s[k] = n.op_left[k];
+    rgt_s[k] = n.op_right[k];
+  }
 
   const bool adaptive = cfg.damping == FRB_DAMPING_ADAPTIVE;
   const int ramp_n = cfg.bc_ramp_iters;
@@ -477,10 +554,16 @@ __device__ void solve_one(const frb_batch& b, const frb_config& cfg, int p, doub
     __syncthreads();
     return;
   }
+  // hot loop-invariant views of the incidence table
+  const Ell E{n.ell_o, n.ell_c, n.ell_L, n.ea_uniform ? nullptr : n.ell_EA, n.ea, n.SA, n.SB, n.S};
+  const double* __restrict__ Xg = n.X;
+  const double* __restrict__ mass = n.mass;
   // initial internal forces on free nodes (:413-420), kept as f_prev
+  free_free_coefs(n, pos, NF, sq2);
+  __syncthreads();
   for (int i = t; i < NF; i += T) {
     double fx, fy, fz;
-    node_force_ell(n, P, i, fx, fy, fz);
+    node_force_ell(E, sq2, P, i, fx, fy, fz);
     fprv[3 * i] = fx;
     fprv[3 * i + 1] = fy;
     fprv[3 * i + 2] = fz;
@@ -488,13 +571,13 @@ __device__ void solve_one(const frb_batch& b, const frb_config& cfg, int p, doub
   __syncthreads();
   // a = -f/m (:428-430), then iteration 0's kick + drift (:443-448)
   batched_div<MAXK>(
-      has, [&](int k) { return -fprv[t + k * T]; }, [&](int k) { return __ldg(n.mass + (t + k * T) / 3); },
+      has, [&](int k) { return -fprv[t + k * T]; }, [&](int k) { return __ldg(mass + (t + k * T) / 3); },
       [&](int k, double a) {
         const int d = t + k * T;
         v[k] = dadd(0.0, dmul(hdt, a));
         u[k] = dadd(0.0, dmul(dt, v[k]));
         const int node = d / 3;
-        pos[(d - 3 * node) * NF + node] = dadd(__ldg(n.X + d), u[k]);
+        pos[(d - 3 * node) * NF + node] = dadd(__ldg(Xg + d), u[k]);
       });
   if (ramp) {  // iteration 0's ramp step (:449-453)
     alpha = ramp_alpha(1, ramp_n);
@@ -505,11 +588,13 @@ __device__ void solve_one(const frb_batch& b, const frb_config& cfg, int p, doub
   // ---- relaxation loop (microsolver.py:434-530) ---------------------------
   int it = 0;
   for (;; ++it) {
-    // F: internal forces at the drifted positions (:456-465)
-    bool bad = false;
+    // F: internal forces at the drifted positions (:456-465): F1 element
+    // coefficients into the sq2 buffer, then F2 per-node gathers
+    bool bad = free_free_coefs(n, pos, NF, sq2);
+    __syncthreads();
     for (int i = t; i < NF; i += T) {
       double fx, fy, fz;
-      bad |= node_force_ell(n, P, i, fx, fy, fz);
+      bad |= node_force_ell(E, sq2, P, i, fx, fy, fz);
       fcur[3 * i] = fx;
       fcur[3 * i + 1] = fy;
       fcur[3 * i + 2] = fz;
@@ -535,7 +620,7 @@ __device__ void solve_one(const frb_batch& b, const frb_config& cfg, int p, doub
           if (adaptive) {
             kh = (kh > 0.0 || isnan(kh)) ? kh : 0.0;
             pos[d] = dmul(dmul(u[k], kh), u[k]);
-            sq2[d] = dmul(dmul(u[k], __ldg(n.mass + d / 3)), u[k]);
+            sq2[d] = dmul(dmul(u[k], __ldg(mass + d / 3)), u[k]);
           }
           fcur[d] = dmul(f, f);
           fprv[d] = f;
@@ -597,9 +682,9 @@ __device__ void solve_one(const frb_batch& b, const frb_config& cfg, int p, doub
     // T: tree combine + scalar bookkeeping (warp 0)
     if (t < 32) {
       for (int lev = 0; lev < n.n_levels; ++lev) {
-        const int k1 = n.level_off[lev + 1];
-        for (int k = n.level_off[lev] + lane; k < k1; k += 32) {
-          const int dd = n.op_dst[k], la = n.op_left[k], rb = n.op_right[k];
+        const int k1 = lvl_s[lev + 1];
+        for (int k = lvl_s[lev] + lane; k < k1; k += 32) {
+          const int dd = dst_s[k], la = lft_s[k], rb = rgt_s[k];
           slot[3 * dd] = dadd(slot[3 * la], slot[3 * rb]);
           slot[3 * dd + 1] = dadd(slot[3 * la + 1], slot[3 * rb + 1]);
           slot[3 * dd + 2] = dadd(slot[3 * la + 2], slot[3 * rb + 2]);
@@ -652,7 +737,7 @@ __device__ void solve_one(const frb_batch& b, const frb_config& cfg, int p, doub
     const double c = sc.c;
     const bool done = sc.done != 0;
     batched_div<MAXK>(
-        has, [&](int k) { return -fprv[t + k * T]; }, [&](int k) { return __ldg(n.mass + (t + k * T) / 3); },
+        has, [&](int k) { return -fprv[t + k * T]; }, [&](int k) { return __ldg(mass + (t + k * T) / 3); },
         [&](int k, double fm) {
           const double a = dsub(fm, dmul(c, v[k]));
           v[k] = dadd(v[k], dmul(hdt, a));
@@ -661,7 +746,7 @@ __device__ void solve_one(const frb_batch& b, const frb_config& cfg, int p, doub
             v[k] = dadd(v[k], dmul(hdt, a));
             u[k] = dadd(u[k], dmul(dt, v[k]));
             const int node = d / 3;
-            pos[(d - 3 * node) * NF + node] = dadd(__ldg(n.X + d), u[k]);
+            pos[(d - 3 * node) * NF + node] = dadd(__ldg(Xg + d), u[k]);
           }
         });
     if (!done && ramp && alpha < 1.0) {
@@ -682,7 +767,7 @@ __device__ void solve_one(const frb_batch& b, const frb_config& cfg, int p, doub
       uo[d] = u[k];
       fo[d] = fprv[d];
       const int node = d / 3;
-      pos[(d - 3 * node) * NF + node] = dadd(__ldg(n.X + d), u[k]);  // pos held sq
+      pos[(d - 3 * node) * NF + node] = dadd(__ldg(Xg + d), u[k]);  // pos held sq
     }
   }
   __syncthreads();
@@ -854,10 +939,13 @@ int frb_device_info(int device, int* n_sm, int* smem_optin, int* cc_major, int* 
   return FRB_OK;
 }
 
-int64_t frb_cta_smem_bytes(int32_t n_nodes, int32_t n_free_nodes, int32_t n_leaves) {
-  (void)n_nodes;
-  const int64_t slots = n_leaves > 0 ? 2 * static_cast<int64_t>(n_leaves) - 1 : 1;
-  return 8 * (12 * static_cast<int64_t>(n_free_nodes) + 3 * slots);
+int64_t frb_cta_smem_bytes(int32_t n_free_nodes, int32_t n_ff, int32_t n_leaves) {
+  const int64_t nf = 3 * static_cast<int64_t>(n_free_nodes);
+  const int64_t L = n_leaves;
+  const int64_t slots = L > 0 ? 2 * L - 1 : 1;
+  const int64_t levels = L > 1 ? 64 - __builtin_clzll(static_cast<uint64_t>(L - 1)) + 1 : 0;  // >= tree height
+  const int64_t prog_ints = (levels + 1) + 3 * (L > 0 ? L - 1 : 0);
+  return 8 * (3 * nf + (nf > n_ff ? nf : n_ff) + 3 * slots) + 4 * ((prog_ints + 1) & ~1LL);
 }
 
 int frb_solve_batch(const frb_batch* batch, const frb_config* cfg, int block_threads, int grid_ctas,

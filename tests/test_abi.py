@@ -26,15 +26,15 @@ def test_library_exports_every_declared_symbol():
 
 def test_struct_layouts():
     assert C.sizeof(nat.FrbConfig) == 48
-    assert C.sizeof(nat.FrbBatch) == 16 + 18 * 8
-    assert nat.PROBLEM_DTYPE.itemsize == 176
+    assert C.sizeof(nat.FrbBatch) == 16 + 22 * 8
+    assert nat.PROBLEM_DTYPE.itemsize == 200
     assert nat.RESULT_DTYPE.itemsize == 144
 
 
 def test_cta_smem_bytes_matches_host_mirror():
     from paper_2305_07030_b200.batch import cta_smem_bytes
-    for n, nf, L in [(3375, 2197, 64), (392, 150, 4), (8, 0, 0), (27, 1, 1)]:  # noqa
-        assert nat.lib().frb_cta_smem_bytes(n, nf, L) == cta_smem_bytes(n, nf, L)
+    for nfn, nff, L in [(2197, 6084, 64), (150, 360, 4), (0, 0, 0), (1, 0, 1), (63, 400, 2)]:
+        assert nat.lib().frb_cta_smem_bytes(nfn, nff, L) == cta_smem_bytes(nfn, nff, L)
 
 
 def test_invalid_arguments_fail_loudly():

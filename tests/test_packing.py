@@ -56,10 +56,11 @@ def test_pack_offsets_and_dedup():
     # equal topologies share one incidence table
     assert len({int(d["inc_base"]) for d in b.desc[:4]}) == 1
     assert b.arrays["inc"].shape[0] == 2 * (540 + 300)
-    assert b.smem_bytes == max(fb.cta_smem_bytes(p.n_nodes, p.n_free_nodes, p.topo.n_leaves) for p in b.problems)
+    assert b.smem_bytes == max(fb.cta_smem_bytes(p.n_free_nodes, len(p.topo.ff_elem), p.topo.n_leaves)
+                               for p in b.problems)
     assert "ell_EA" not in b.arrays        # uniform EA -> scalar per problem
     assert all(d["flags"] & nat.PF_EA_UNIFORM for d in b.desc)
-    assert b.desc.dtype.itemsize == 176
+    assert b.desc.dtype.itemsize == 200
 
 
 def test_mixed_materials_carry_slot_ea():
@@ -84,3 +85,19 @@ def test_isolated_node_is_mass_error():
                            [frb.Material(1, 1, 1)], frozenset({0}))
     with pytest.raises(frb.NetworkMassError):
         frb.pack_batch([net], [frb.AffineBC(np.eye(3))])
+
+
+@pytest.mark.parametrize("net", list(_nets()))
+def test_free_free_coefficient_slots(net):
+    p = fb.build_problem(net, frb.AffineBC(np.eye(3)))
+    t = p.topo
+    nfn = t.n_free_nodes
+    for k in range(t.ell_slots_a + t.ell_slots_b):
+        for i in range(nfn):
+            o, c = t.ell_other[k, i], t.ell_c[k, i]
+            if o < 0 or o >= nfn:
+                assert c == -1
+            else:
+                a, b = t.ff_ab[c]
+                assert {int(a), int(b)} == {i, int(o)}
+                assert t.ff_elem[c] == t.ell_elem[k, i]
