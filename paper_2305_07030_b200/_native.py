@@ -15,12 +15,16 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "lib", "libfrb200.so")
 
+ABI_VERSION = 2
+MAX_CLUSTER = 16
 FRB_OK, FRB_E_INVALID, FRB_E_TOO_LARGE, FRB_E_CUDA, FRB_E_UNSUPPORTED = 0, -1, -2, -3, -4
 STATUS_CONVERGED, STATUS_MAX_ITERS, STATUS_SINGULAR = 0, 1, 2
 DAMPING_ADAPTIVE, DAMPING_FIXED = 0, 1
+PF_EA_UNIFORM = 1
 
-EXPORTS = ("frb_abi_version", "frb_last_error", "frb_device_info", "frb_cta_smem_bytes",
-           "frb_solve_batch", "frb_internal_forces", "frb_selftest_arith")
+EXPORTS = ("frb_abi_version", "frb_last_error", "frb_device_info", "frb_rank_smem_bytes",
+           "frb_max_dofs_per_thread", "frb_solve_batch", "frb_internal_forces",
+           "frb_selftest_arith")
 
 
 class FrbConfig(C.Structure):
@@ -29,35 +33,43 @@ class FrbConfig(C.Structure):
                 ("energy_check_interval", C.c_int32), ("bc_ramp_iters", C.c_int32)]
 
 
+BATCH_POINTERS = ("groups", "problems", "parts", "order", "X", "node_mass", "inc_node", "inc",
+                  "elem_ab", "elem_L", "elem_EA", "plans", "ell_o", "ell_c", "act_ab", "act_L",
+                  "act_EA", "halo_g", "send", "u", "f", "work", "results", "queue",
+                  "phase_cycles")
+
+
 class FrbBatch(C.Structure):
-    _fields_ = [("n_problems", C.c_int32), ("smem_bytes", C.c_int32), ("max_nf", C.c_int32),
-                ("pad0", C.c_int32),
-                ("problems", C.c_void_p), ("order", C.c_void_p), ("X", C.c_void_p),
-                ("node_mass", C.c_void_p), ("inc_node", C.c_void_p), ("inc", C.c_void_p),
-                ("elem_ab", C.c_void_p), ("elem_L", C.c_void_p), ("elem_EA", C.c_void_p),
-                ("plans", C.c_void_p), ("ell_other", C.c_void_p), ("ell_L", C.c_void_p),
-                ("ell_EA", C.c_void_p), ("ell_c", C.c_void_p), ("ff_ab", C.c_void_p),
-                ("ff_L", C.c_void_p), ("ff_EA", C.c_void_p), ("u", C.c_void_p), ("f", C.c_void_p), ("work", C.c_void_p),
-                ("results", C.c_void_p), ("queue", C.c_void_p)]
+    _fields_ = [("n_problems", C.c_int32), ("n_groups", C.c_int32)] + \
+               [(name, C.c_void_p) for name in BATCH_POINTERS]
 
 
-# frb_problem / frb_result as numpy record types (arrays of them are uploaded
-# / downloaded as raw bytes)
+# frb_problem / frb_part / frb_group / frb_result as numpy record types
 PROBLEM_DTYPE = np.dtype([
     ("node_base", "<i8"), ("elem_base", "<i8"), ("inc_base", "<i8"), ("plan_base", "<i8"),
-    ("ell_base", "<i8"), ("ellv_base", "<i8"), ("ff_base", "<i8"), ("ffv_base", "<i8"),
+    ("part_base", "<i8"), ("actv_base", "<i8"),
     ("n_nodes", "<i4"), ("n_free_nodes", "<i4"), ("n_elems", "<i4"), ("cluster", "<i4"),
-    ("ell_stride", "<i4"), ("ell_slots_a", "<i4"), ("ell_slots_b", "<i4"), ("flags", "<i4"),
-    ("n_ff", "<i4"), ("pad1", "<i4"),
+    ("flags", "<i4"), ("pad", "<i4"),
     ("dt", "<f8"), ("volume", "<f8"), ("ea", "<f8"), ("F", "<f8", (9,)),
 ])
-PF_EA_UNIFORM = 1
+PART_DTYPE = np.dtype([
+    ("ell_base", "<i8"), ("act_base", "<i8"), ("actv_off", "<i8"), ("halo_base", "<i8"),
+    ("send_base", "<i8"),
+    ("node0", "<i4"), ("n_own", "<i4"), ("n_local", "<i4"), ("n_act", "<i4"),
+    ("ell_stride", "<i4"), ("slots_a", "<i4"), ("slots_b", "<i4"), ("leaf0", "<i4"),
+    ("n_leaves", "<i4"), ("pad", "<i4"),
+])
+GROUP_DTYPE = np.dtype([
+    ("cluster", "<i4"), ("first", "<i4"), ("count", "<i4"), ("block_threads", "<i4"),
+    ("smem_bytes", "<i4"), ("max_own_dofs", "<i4"), ("grid_clusters", "<i4"), ("pad", "<i4"),
+])
 RESULT_DTYPE = np.dtype([
     ("status", "<i4"), ("iters", "<i4"), ("bad_element", "<i4"), ("converged", "<i4"),
     ("final_residual", "<f8"), ("r_ref", "<f8"), ("energy_residual", "<f8"),
     ("avg_stress", "<f8", (9,)), ("energy", "<f8", (4,)),
 ])
-assert PROBLEM_DTYPE.itemsize == 200 and RESULT_DTYPE.itemsize == 144
+assert PROBLEM_DTYPE.itemsize == 168 and PART_DTYPE.itemsize == 80
+assert GROUP_DTYPE.itemsize == 32 and RESULT_DTYPE.itemsize == 144
 
 
 class NativeError(RuntimeError):
@@ -81,13 +93,14 @@ def lib() -> C.CDLL:
     h.frb_abi_version.restype = C.c_int
     h.frb_last_error.restype = C.c_char_p
     h.frb_device_info.argtypes = [C.c_int] + [C.POINTER(C.c_int)] * 4
-    h.frb_cta_smem_bytes.restype = C.c_int64
-    h.frb_cta_smem_bytes.argtypes = [C.c_int32, C.c_int32, C.c_int32]
-    h.frb_solve_batch.argtypes = [C.POINTER(FrbBatch), C.POINTER(FrbConfig), C.c_int, C.c_int, C.c_void_p]
+    h.frb_rank_smem_bytes.restype = C.c_int64
+    h.frb_rank_smem_bytes.argtypes = [C.c_int32] * 4
+    h.frb_max_dofs_per_thread.argtypes = [C.c_int]
+    h.frb_solve_batch.argtypes = [C.POINTER(FrbBatch), C.POINTER(FrbConfig), C.c_void_p]
     h.frb_internal_forces.argtypes = [C.POINTER(FrbBatch), C.c_void_p, C.c_void_p, C.c_void_p]
     h.frb_selftest_arith.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]
-    if h.frb_abi_version() != 1:
-        raise ImportError("libfrb200.so ABI version mismatch")
+    if h.frb_abi_version() != ABI_VERSION:
+        raise ImportError("libfrb200.so ABI version mismatch (rebuild)")
     _lib = h
     return h
 

@@ -1,26 +1,26 @@
-"""Batch submit: pack many networks into one device batch and solve them in a
-single persistent-kernel launch.
+"""Batch submit: pack many networks into one device batch and solve them with
+persistent cluster-kernel launches.
 
 Implements the spec'd ``batch`` module (reference ``SPEC.md:338-394``; there
 is no batch code in the reference package itself):
 
 * ``pack_batch(networks, bcs) -> Batch``
 * ``solve_batch(batch, strategy, config) -> list[SolveResult]``
-* strategies ``TeamBatched`` (the default: a device work queue, one CTA per
-  network) and ``SerialReference`` (one team, problems in order,
-  SPEC.md:359).
+* strategies ``TeamBatched`` (the default: a device work queue, one team =
+  one CTA cluster per network) and ``SerialReference`` (one team,
+  problems in order).
 
 Host setup per network restates ``build_problem`` (reference
-``microsolver.py:302-335``) in vectorised form and adds what the kernel
-needs on top: the per-node incidence lists (role a then role b, ascending
-element id -- the exact summation order of ``np.bincount`` in
-``_scatter_forces``, :214-218) and the pairwise-sum plan for the free-DOF
-count (plan.py).  Networks that share topology and materials share their
-incidence / element arrays on the device.
+``microsolver.py:302-335``) in vectorised form and adds what the kernel needs:
+the per-node incidence lists (role a then role b, ascending element id -- the
+summation order of ``np.bincount`` in ``_scatter_forces``, :214-218), the
+pairwise-sum plan of the free-DOF count (plan.py), and the cluster partition
+(partition.py).  Tables that depend only on topology are shared by every
+network of that topology.
 
-Layout is a PackedStorage in spirit (reference ``packed.py``): flat SoA
-arrays with per-problem offsets, host space "a" (numpy) mirrored to device
-space "b" (torch CUDA tensors) with explicit upload/download.
+Layout is a PackedStorage in spirit (reference ``packed.py``): flat SoA arrays
+with per-problem offsets, host space "a" (numpy) mirrored to device space "b"
+(torch CUDA tensors) with explicit upload/download.
 """
 
 from __future__ import annotations
@@ -28,6 +28,7 @@ from __future__ import annotations
 import ctypes as C
 import hashlib
 import math
+import os
 from dataclasses import dataclass, field
 from typing import Sequence
 
@@ -41,20 +42,31 @@ from .microsolver import (
 )
 from .network import AffineBC, FiberNetwork
 from .packed import PackedStorage
-from .plan import PlanView, reduction_plan
+from .partition import MAX_SEND, Partition, partition, rank_smem_bytes
+from .plan import reduction_plan
 
 __all__ = ["Batch", "DeviceBatch", "ExecutionStrategy", "NaiveLoop", "SerialReference",
            "TeamBatched", "pack_batch", "solve_batch", "build_problem", "DeviceResults"]
 
 MAX_CTA_THREADS = 1024
-MAX_DOFS_PER_THREAD = 8     # FRB_MAX_DOFS_PER_THREAD
+CLUSTER_SIZES = (1, 2, 4, 8, 16)
+# per-CTA dynamic SMEM budget (227 KB opt-in minus the kernel's static SMEM)
+SMEM_BUDGET = 227 * 1024 - 4 * 1024
+# target free DOFs per cluster rank: keeps u, v register-resident and leaves
+# L1 room for the read-only tables (C2's 10k-DOF networks -> 2 ranks)
+DOFS_PER_RANK = int(os.environ.get("FRB_DOFS_PER_RANK", "3400"))
+
+
+def dofs_per_thread_cap(threads: int) -> int:
+    """Register-resident DOFs per thread the kernel instantiates (frb200.h)."""
+    return 8 if threads > 768 else 12 if threads > 512 else 16
 
 
 # ------------------------------------------------------------------ strategies
 
 @dataclass(frozen=True)
 class SerialReference:
-    """Problems one after another on a single team (one CTA)."""
+    """Problems one after another on a single team."""
 
 
 @dataclass(frozen=True)
@@ -66,17 +78,18 @@ class NaiveLoop:
 
 @dataclass(frozen=True)
 class TeamBatched:
-    """Shared work queue; each team runs whole solves.
-    teams=None sizes the persistent grid by occupancy; team_size=None picks
-    the smallest CTA that covers the pairwise-sum chains."""
+    """Shared work queue; each team (a CTA cluster) runs whole solves
+    (SPEC.md:361).  teams=None sizes the persistent grid by occupancy;
+    team_size overrides the threads per CTA."""
     teams: int | None = None
     team_size: int | None = None
 
     def __post_init__(self):
         if self.teams is not None and self.teams < 1:
             raise ValueError("teams must be >= 1")
-        if self.team_size is not None and (self.team_size < 32 or self.team_size % 32):
-            raise ValueError("team_size must be a positive multiple of 32")
+        if self.team_size is not None and (self.team_size < 32 or self.team_size % 32
+                                           or self.team_size > MAX_CTA_THREADS):
+            raise ValueError("team_size must be a multiple of 32 in [32, 1024]")
 
 
 ExecutionStrategy = SerialReference | NaiveLoop | TeamBatched
@@ -85,30 +98,9 @@ ExecutionStrategy = SerialReference | NaiveLoop | TeamBatched
 # ------------------------------------------------------------------ host setup
 
 @dataclass
-class HostProblem:
-    """Solver-order setup of one network (ProblemSetup, microsolver.py:138-163)."""
-    network: FiberNetwork
-    F: np.ndarray
-    node_order: np.ndarray       # solver position -> original node
-    X: np.ndarray                # (N, 3)
-    node_mass: np.ndarray        # (N,)
-    dt_base: float               # min_e L sqrt(rho/E); dt = dt_safety * dt_base
-    topo_key: bytes
-    topo: "Topology"
-
-    @property
-    def n_nodes(self) -> int:
-        return len(self.X)
-
-    @property
-    def n_free_nodes(self) -> int:
-        return self.topo.n_free_nodes
-
-
-@dataclass
 class Topology:
-    """Arrays that depend only on (elements, boundary, materials) -- shared
-    by every network of the same topology."""
+    """Arrays that depend only on (elements, boundary) -- shared by every
+    network of the same topology."""
     n_nodes: int
     n_free_nodes: int
     inc_node: np.ndarray         # (N, 2) int32: first entry, n_a | n_b << 16
@@ -116,14 +108,32 @@ class Topology:
     elem_ab: np.ndarray          # (M, 2) int32 solver node ids
     plan: np.ndarray             # int32 flat pairwise plan for nf
     n_leaves: int
-    max_own: int                 # most DOFs one chain thread owns
-    ell_other: np.ndarray        # (SA+SB, S) int32 slot-major, -1 padding
-    ell_elem: np.ndarray         # (SA+SB, S) int32 element per slot (0 on padding)
-    ell_slots_a: int
-    ell_slots_b: int
-    ell_c: np.ndarray            # (SA+SB, S) int32 index into ff list, -1 fixed/padding
-    ff_ab: np.ndarray            # (n_ff, 2) int32 endpoints of free-free elements
-    ff_elem: np.ndarray          # (n_ff,) element ids
+    ell_other: np.ndarray        # (SA+SB, NF) int32 slot-major, -1 padding (solver ids)
+    ell_elem: np.ndarray         # (SA+SB, NF) int32 element per slot (0 on padding)
+    slots_a: int
+    slots_b: int
+    parts: dict = field(default_factory=dict)   # cluster size -> Partition
+
+    def partition(self, C: int) -> Partition:
+        if C not in self.parts:
+            self.parts[C] = partition(self.n_nodes, self.n_free_nodes, self.elem_ab[:, 0].astype(np.int64),
+                                      self.elem_ab[:, 1].astype(np.int64), self.ell_other, self.ell_elem,
+                                      self.slots_a, self.slots_b, self.plan, C)
+        return self.parts[C]
+
+    def choose_cluster(self) -> Partition:
+        """Smallest cluster with at most DOFS_PER_RANK free DOFs per rank whose
+        ranks fit the SMEM budget (more ranks if SMEM demands it)."""
+        nf = 3 * self.n_free_nodes
+        want = max(1, math.ceil(nf / DOFS_PER_RANK))
+        for C in CLUSTER_SIZES:
+            if C < want and C != CLUSTER_SIZES[-1]:
+                continue
+            part = self.partition(C)
+            if max(rank_smem_bytes(r, self.n_leaves) for r in part.ranks) <= SMEM_BUDGET:
+                return part
+        raise nat.NativeError(nat.FRB_E_TOO_LARGE,
+                              f"network with {nf} free DOFs does not fit a {CLUSTER_SIZES[-1]}-CTA cluster")
 
 
 def _topology(network: FiberNetwork, node_rank: np.ndarray, n_free_nodes: int) -> Topology:
@@ -145,41 +155,49 @@ def _topology(network: FiberNetwork, node_rank: np.ndarray, n_free_nodes: int) -
     np.cumsum((na + nb)[:-1], out=first[1:])
     inc_node = np.stack([first, na | (nb << 16)], axis=1).astype(np.int32)
     plan = reduction_plan(3 * n_free_nodes)
-    # slot-major table for free nodes: slot k < SA is the k-th role-a
+    # slot-major table of the free nodes: slot k < SA is the k-th role-a
     # incidence (ascending element), slot SA + k the k-th role-b incidence
     snode, srole = node[order], role[order]
     grp = snode.astype(np.int64) * 2 + srole
-    starts = np.flatnonzero(np.r_[True, grp[1:] != grp[:-1]])
+    starts = np.flatnonzero(np.r_[True, grp[1:] != grp[:-1]]) if len(grp) else np.zeros(0, np.int64)
     rank = np.arange(len(grp)) - np.repeat(starts, np.diff(np.r_[starts, len(grp)]))
     nfn = n_free_nodes
     sa = int(na[:nfn].max()) if nfn and m else 0
     sb = int(nb[:nfn].max()) if nfn and m else 0
-    stride = max(32, 32 * ((nfn + 31) // 32))
-    ell_other = np.full((sa + sb, stride), -1, dtype=np.int32)
-    ell_elem = np.zeros((sa + sb, stride), dtype=np.int32)
+    ell_other = np.full((sa + sb, nfn), -1, dtype=np.int32)
+    ell_elem = np.zeros((sa + sb, nfn), dtype=np.int32)
     free = snode < nfn
     slot = np.where(srole == 0, rank, sa + rank)[free]
     ell_other[slot, snode[free]] = other[order][free]
     ell_elem[slot, snode[free]] = elem[order][free]
-    sizes = PlanView(plan).leaf_size
-    max_own = int(max(((z // 8) + (1 if z % 8 else 0)) if z >= 8 else 1 for z in sizes)) if len(sizes) else 1
-    # elements between two free nodes: their coefficient is computed once per
-    # iteration (fiber-parallel) and looked up by both endpoints' slots
-    ff_mask = (ia < nfn) & (ib < nfn)
-    ff_elem = np.flatnonzero(ff_mask)
-    ff_index = np.full(m, -1, dtype=np.int64)
-    ff_index[ff_elem] = np.arange(ff_elem.size)
-    ell_c = np.where(ell_other >= 0, ff_index[ell_elem], -1)
-    ell_c = np.where((ell_other >= 0) & (ell_other < nfn), ell_c, -1).astype(np.int32)
     return Topology(n_nodes=n, n_free_nodes=n_free_nodes, inc_node=inc_node, inc=inc,
                     elem_ab=np.stack([ia, ib], axis=1).astype(np.int32), plan=plan,
-                    n_leaves=int(plan[0]), max_own=max_own, ell_other=ell_other,
-                    ell_elem=ell_elem, ell_slots_a=sa, ell_slots_b=sb, ell_c=ell_c,
-                    ff_ab=np.stack([ia[ff_elem], ib[ff_elem]], axis=1).astype(np.int32),
-                    ff_elem=ff_elem.astype(np.int64))
+                    n_leaves=int(plan[0]), ell_other=ell_other, ell_elem=ell_elem,
+                    slots_a=sa, slots_b=sb)
 
 
 _TOPO_CACHE: dict[bytes, Topology] = {}
+
+
+@dataclass
+class HostProblem:
+    """Solver-order setup of one network (ProblemSetup, microsolver.py:138-163)."""
+    network: FiberNetwork
+    F: np.ndarray
+    node_order: np.ndarray       # solver position -> original node
+    X: np.ndarray                # (N, 3)
+    node_mass: np.ndarray        # (N,)
+    dt_base: float               # min_e L sqrt(rho/E); dt = dt_safety * dt_base
+    topo_key: bytes
+    topo: Topology
+
+    @property
+    def n_nodes(self) -> int:
+        return len(self.X)
+
+    @property
+    def n_free_nodes(self) -> int:
+        return self.topo.n_free_nodes
 
 
 def build_problem(network: FiberNetwork, bc: AffineBC, check_mass: bool = True) -> HostProblem:
@@ -193,16 +211,13 @@ def build_problem(network: FiberNetwork, bc: AffineBC, check_mass: bool = True) 
     rank = np.empty(n, dtype=np.int64)
     rank[order] = np.arange(n)
     nfn = dm.n_free // 3
-    if check_mass:
-        node_mass = _lumped_node_mass(network)[order]
-    else:
-        node_mass = np.ones(n)
-    emod, area, rho = network.material_columns()
+    node_mass = _lumped_node_mass(network)[order] if check_mass else np.ones(n)
+    emod, _, rho = network.material_columns()
     L = network.reference_lengths()
     dt_base = float(np.min(L * np.sqrt(rho / emod))) if L.size else math.nan
     h = hashlib.blake2b(digest_size=16)
     h.update(np.int64([n, network.n_elements]).tobytes())
-    h.update(network.elements.tobytes())
+    h.update(network.elements[:, :2].tobytes())
     h.update(np.asarray(sorted(network.boundary_nodes), dtype=np.int64).tobytes())
     key = h.digest()
     topo = _TOPO_CACHE.get(key)
@@ -216,19 +231,6 @@ def build_problem(network: FiberNetwork, bc: AffineBC, check_mass: bool = True) 
                        node_mass=node_mass, dt_base=dt_base, topo_key=key, topo=topo)
 
 
-def cta_smem_bytes(n_free_nodes: int, n_ff: int, n_leaves: int) -> int:
-    """Mirror of frb_cta_smem_bytes (include/frb200.h): positions / sq, f,
-    f_prev (8 B per free DOF each), sq2 / free-free coefficients, tree
-    slots, and the tree's combine program (int32, bounded by a height of
-    bit_length(L-1) + 1 levels)."""
-    nf = 3 * n_free_nodes
-    L = n_leaves
-    slots = 2 * L - 1 if L > 0 else 1
-    levels = (L - 1).bit_length() + 1 if L > 1 else 0
-    prog = (levels + 1) + 3 * (L - 1 if L > 0 else 0)
-    return 8 * (3 * nf + max(nf, n_ff) + 3 * slots) + 4 * ((prog + 1) & ~1)
-
-
 # ------------------------------------------------------------------ batch
 
 @dataclass
@@ -240,13 +242,16 @@ class Batch:
     bcs: list
     problems: list                     # HostProblem per network
     desc: np.ndarray                   # PROBLEM_DTYPE records (dt filled per solve)
-    arrays: dict                       # flat host arrays
+    parts: np.ndarray                  # PART_DTYPE records
+    groups: np.ndarray                 # GROUP_DTYPE records (host)
+    arrays: dict                       # flat host arrays uploaded to the device
     node_base: np.ndarray              # (P+1,) int64 node offsets
-    max_leaves: int
-    smem_bytes: int
-    max_nf: int
     _packed_state: dict | None = field(default=None, repr=False)
     pinned: dict | None = field(default=None, repr=False)
+
+    @property
+    def n_problems(self) -> int:
+        return len(self.problems)
 
     def pin(self) -> "Batch":
         """Page-lock the packed arrays once so uploads are pure DMA."""
@@ -254,10 +259,6 @@ class Batch:
         self.pinned = {k: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
                        for k, a in self.arrays.items()}
         return self
-
-    @property
-    def n_problems(self) -> int:
-        return len(self.problems)
 
     @property
     def packed_state(self) -> dict:
@@ -281,31 +282,63 @@ def pack_batch(networks: Sequence[FiberNetwork], bcs: Sequence[AffineBC]) -> Bat
     return _pack(list(networks), list(bcs), probs)
 
 
-def _pack(networks, bcs, probs) -> Batch:
+def _cat(parts, dtype, width=None):
+    if not parts:
+        return np.zeros((0,) if width is None else (0, width), dtype=dtype)
+    return np.ascontiguousarray(np.concatenate(parts).astype(dtype, copy=False))
+
+
+def _group_threads(max_own_dofs: int, max_rank_leaves: int, n_problems: int, cluster: int) -> int:
+    """Threads per CTA for a group: 8 per pairwise leaf at least, few enough
+    DOFs per thread for the register budget; more threads when there are too
+    few problems to fill the GPU (latency), fewer when many small problems
+    can share an SM."""
+    need = max(64, 8 * max_rank_leaves, math.ceil(max_own_dofs / 16))
+    if max_own_dofs > 1024 or n_problems * cluster < 148:
+        need = max(need, min(512, 32 * math.ceil(max_own_dofs / 32)))
+    threads = min(MAX_CTA_THREADS, 32 * math.ceil(need / 32))
+    while max_own_dofs > dofs_per_thread_cap(threads) * threads and threads < MAX_CTA_THREADS:
+        threads += 32
+    return threads
+
+
+def _pack(networks, bcs, probs, cluster: int | None = None) -> Batch:
     P = len(probs)
     desc = np.zeros(P, dtype=nat.PROBLEM_DTYPE)
     node_base = np.zeros(P + 1, dtype=np.int64)
-    topo_slot: dict[bytes, tuple[int, int]] = {}
     plan_slot: dict[int, int] = {}
-    inc, plans, ell_other, ell_c, ff_ab = [], [], [], [], []
-    n_inc = n_plan = n_ell = n_ffs = 0
-    elem_base = ellv_base = ffv_base = 0
-    ff_L, ff_EA = [], []
-    X, mass, EL, EA, inc_node, elem_ab, ell_L, ell_EA = [], [], [], [], [], [], [], []
+    shared_slot: dict[tuple, list] = {}       # (topo, C) -> per-rank base offsets
+    topo_slot: dict[bytes, int] = {}
+    inc, plans, ell_o, ell_c, act_ab, halo_g, send = [], [], [], [], [], [], []
+    n_inc = n_plan = n_ell = n_act = n_halo = n_send = 0
+    X, mass, EL, EA, inc_node, elem_ab, act_L, act_EA = [], [], [], [], [], [], [], []
+    parts_rows = []
+    elem_base = actv_base = 0
     any_nonuniform = False
-    max_leaves = smem = max_nf = 0
+    part_of = []
     for i, p in enumerate(probs):
         t = p.topo
+        part = t.partition(cluster) if cluster else t.choose_cluster()
+        part_of.append(part)
         if p.topo_key not in topo_slot:
-            topo_slot[p.topo_key] = (n_inc, n_ell, n_ffs)
+            topo_slot[p.topo_key] = n_inc
             inc.append(t.inc)
-            ell_other.append(t.ell_other.reshape(-1))
-            ell_c.append(t.ell_c.reshape(-1))
-            ff_ab.append(t.ff_ab)
             n_inc += len(t.inc)
-            n_ell += t.ell_other.size
-            n_ffs += len(t.ff_ab)
-        inc_b, ell_b, ff_b = topo_slot[p.topo_key]
+        key = (p.topo_key, part.C)
+        if key not in shared_slot:
+            bases = []
+            for rt in part.ranks:
+                bases.append((n_ell, n_act, n_halo, n_send))
+                ell_o.append(rt.ell_o.reshape(-1))
+                ell_c.append(rt.ell_c.reshape(-1))
+                act_ab.append(rt.act_ab)
+                halo_g.append(rt.halo_g)
+                send.append(rt.send)
+                n_ell += rt.ell_o.size
+                n_act += len(rt.act_ab)
+                n_halo += len(rt.halo_g)
+                n_send += len(rt.send)
+            shared_slot[key] = bases
         nf = 3 * t.n_free_nodes
         if nf not in plan_slot:
             plan_slot[nf] = n_plan
@@ -315,27 +348,35 @@ def _pack(networks, bcs, probs) -> Batch:
         ea = emod * area
         L = p.network.reference_lengths()
         uniform = bool(ea.size == 0 or np.all(ea == ea[0]))
+        any_nonuniform |= not uniform
         d = desc[i]
         d["node_base"] = node_base[i]
         d["elem_base"] = elem_base
-        d["inc_base"] = inc_b
+        d["inc_base"] = topo_slot[p.topo_key]
         d["plan_base"] = plan_slot[nf]
-        d["ell_base"] = ell_b
-        d["ellv_base"] = ellv_base
-        d["ff_base"] = ff_b
-        d["ffv_base"] = ffv_base
-        d["n_ff"] = len(t.ff_elem)
+        d["part_base"] = len(parts_rows)
+        d["actv_base"] = actv_base
         d["n_nodes"] = p.n_nodes
         d["n_free_nodes"] = t.n_free_nodes
         d["n_elems"] = p.network.n_elements
-        d["cluster"] = 1
-        d["ell_stride"] = t.ell_other.shape[1]
-        d["ell_slots_a"] = t.ell_slots_a
-        d["ell_slots_b"] = t.ell_slots_b
+        d["cluster"] = part.C
         d["flags"] = nat.PF_EA_UNIFORM if uniform else 0
         d["volume"] = p.network.volume
         d["ea"] = ea[0] if ea.size else 0.0
         d["F"] = p.F.reshape(9)
+        off = 0
+        for rt, (b_ell, b_act, b_halo, b_send) in zip(part.ranks, shared_slot[key]):
+            row = np.zeros((), dtype=nat.PART_DTYPE)
+            row["ell_base"], row["act_base"], row["actv_off"] = b_ell, b_act, off
+            row["halo_base"], row["send_base"] = b_halo, b_send
+            row["node0"], row["n_own"], row["n_local"], row["n_act"] = rt.node0, rt.n_own, rt.n_local, rt.n_act
+            row["ell_stride"], row["slots_a"], row["slots_b"] = rt.stride, part.slots_a, part.slots_b
+            row["leaf0"], row["n_leaves"] = rt.leaf0, rt.n_leaves
+            parts_rows.append(row)
+            act_L.append(L[rt.act_elem])
+            act_EA.append(ea[rt.act_elem])
+            off += rt.n_act
+        actv_base += off
         node_base[i + 1] = node_base[i] + p.n_nodes
         X.append(p.X.reshape(-1))
         mass.append(p.node_mass)
@@ -343,41 +384,38 @@ def _pack(networks, bcs, probs) -> Batch:
         EA.append(ea)
         inc_node.append(t.inc_node)
         elem_ab.append(t.elem_ab)
-        valid = t.ell_other.reshape(-1) >= 0
-        eidx = t.ell_elem.reshape(-1)
-        ell_L.append(np.where(valid, L[eidx] if L.size else 1.0, 1.0))
-        if not uniform:
-            any_nonuniform = True
-        ell_EA.append(np.where(valid, ea[eidx] if ea.size else 0.0, 0.0))
-        ellv_base += t.ell_other.size
-        ff_L.append(L[t.ff_elem])
-        ff_EA.append(ea[t.ff_elem])
-        ffv_base += len(t.ff_elem)
         elem_base += p.network.n_elements
-        max_leaves = max(max_leaves, t.n_leaves)
-        max_nf = max(max_nf, 3 * t.n_free_nodes)
-        smem = max(smem, cta_smem_bytes(t.n_free_nodes, len(t.ff_elem), t.n_leaves))
 
-    def cat(parts, dtype, width=None):
-        if not parts:
-            return np.zeros((0,) if width is None else (0, width), dtype=dtype)
-        return np.ascontiguousarray(np.concatenate(parts).astype(dtype, copy=False))
-
+    parts = np.array(parts_rows, dtype=nat.PART_DTYPE) if parts_rows else np.zeros(0, nat.PART_DTYPE)
+    # launch groups by cluster size, longest problems first inside a group
+    order, groups = [], []
+    for C in sorted({pt.C for pt in part_of}):
+        ids = [i for i in range(P) if part_of[i].C == C]
+        ids.sort(key=lambda i: -probs[i].n_nodes)
+        smem = max(rank_smem_bytes(rt, probs[i].topo.n_leaves) for i in ids for rt in part_of[i].ranks)
+        own = max(3 * rt.n_own for i in ids for rt in part_of[i].ranks)
+        leaves = max(rt.n_leaves for i in ids for rt in part_of[i].ranks)
+        g = np.zeros((), dtype=nat.GROUP_DTYPE)
+        g["cluster"], g["first"], g["count"] = C, len(order), len(ids)
+        g["block_threads"] = _group_threads(own, leaves, len(ids), C)
+        g["smem_bytes"], g["max_own_dofs"] = smem, own
+        groups.append(g)
+        order.extend(ids)
     arrays = dict(
-        X=cat(X, np.float64), node_mass=cat(mass, np.float64),
-        inc_node=cat(inc_node, np.int32, 2), inc=cat(inc, np.int32, 2),
-        elem_ab=cat(elem_ab, np.int32, 2), elem_L=cat(EL, np.float64),
-        elem_EA=cat(EA, np.float64), plans=cat(plans, np.int32),
-        ell_other=cat(ell_other, np.int32), ell_L=cat(ell_L, np.float64),
-        ell_c=cat(ell_c, np.int32), ff_ab=cat(ff_ab, np.int32, 2), ff_L=cat(ff_L, np.float64),
+        X=_cat(X, np.float64), node_mass=_cat(mass, np.float64),
+        inc_node=_cat(inc_node, np.int32, 2), inc=_cat(inc, np.int32, 2),
+        elem_ab=_cat(elem_ab, np.int32, 2), elem_L=_cat(EL, np.float64),
+        elem_EA=_cat(EA, np.float64), plans=_cat(plans, np.int32),
+        ell_o=_cat(ell_o, np.int32), ell_c=_cat(ell_c, np.int32),
+        act_ab=_cat(act_ab, np.int32, 2), act_L=_cat(act_L, np.float64),
+        halo_g=_cat(halo_g, np.int32), send=_cat(send, np.int32, MAX_SEND),
+        order=np.asarray(order, dtype=np.int32),
+        problems=desc.view(np.uint8).copy(), parts=parts.view(np.uint8).copy(),
     )
     if any_nonuniform:
-        arrays["ell_EA"] = cat(ell_EA, np.float64)
-        arrays["ff_EA"] = cat(ff_EA, np.float64)
-    # order: longest first (nodes as the work proxy) for the dynamic queue
-    arrays["order"] = np.argsort(-node_base[1:] + node_base[:-1], kind="stable").astype(np.int32)
-    return Batch(networks=networks, bcs=bcs, problems=probs, desc=desc, arrays=arrays,
-                 node_base=node_base, max_leaves=max_leaves, smem_bytes=smem, max_nf=max_nf)
+        arrays["act_EA"] = _cat(act_EA, np.float64)
+    return Batch(networks=networks, bcs=bcs, problems=probs, desc=desc, parts=parts,
+                 groups=np.array(groups, dtype=nat.GROUP_DTYPE), arrays=arrays, node_base=node_base)
 
 
 # ------------------------------------------------------------------ device
@@ -404,7 +442,6 @@ class DeviceBatch:
     host: Batch
     device: object
     t: dict
-    desc_host: np.ndarray
 
     @classmethod
     def upload(cls, batch: Batch, device=None, pin: bool = True) -> "DeviceBatch":
@@ -421,83 +458,61 @@ class DeviceBatch:
                 if pin:
                     src = src.pin_memory()
             t[k] = src.to(device, non_blocking=True)
-        return cls(host=batch, device=device, t=t, desc_host=batch.desc.copy())
+        return cls(host=batch, device=device, t=t)
 
-    def _desc_tensor(self, cfg: SolverConfig):
-        torch = _torch()
-        desc = self.desc_host
-        desc["dt"] = [cfg.dt_safety * p.dt_base for p in self.host.problems]
-        raw = torch.from_numpy(desc.view(np.uint8).copy())
-        return raw.to(self.device, non_blocking=True)
-
-    def default_threads(self) -> int:
-        """Smallest CTA (multiple of 32, >= 64) that covers the pairwise
-        chains and keeps <= MAX_DOFS_PER_THREAD DOFs per thread; large
-        problems get 1024 threads for latency hiding."""
-        h = self.host
-        need = max(64, 8 * h.max_leaves, math.ceil(h.max_nf / MAX_DOFS_PER_THREAD))
-        if h.max_nf > 2048:
-            need = max(need, 1024)
-        return min(MAX_CTA_THREADS, 32 * math.ceil(need / 32))
-
-    @property
-    def work(self):
-        if getattr(self, "_work", None) is None:
-            self._work = _torch().empty(3 * int(self.host.node_base[-1]) + 1, dtype=_torch().float64,
-                                        device=self.device)
-        return self._work
-
-    def frb_batch(self, desc_t, u, f, results, queue) -> nat.FrbBatch:
-        t = self.t
-        b = nat.FrbBatch()
-        b.n_problems = self.host.n_problems
-        b.smem_bytes = self.host.smem_bytes
-        b.max_nf = self.host.max_nf
-        b.problems = desc_t.data_ptr()
-        b.order = t["order"].data_ptr()
-        for k in ("X", "node_mass", "inc_node", "inc", "elem_ab", "elem_L", "elem_EA", "plans",
-                  "ell_other", "ell_L", "ell_EA", "ell_c", "ff_ab", "ff_L", "ff_EA"):
-            setattr(b, k, t[k].data_ptr() if k in t and t[k].numel() else None)
-        b.u, b.f = u.data_ptr(), f.data_ptr()
-        b.work = self.work.data_ptr()
-        b.results = results.data_ptr()
-        b.queue = queue.data_ptr()
-        return b
-
-    def prepare(self, cfg: SolverConfig, strategy=None) -> "Launch":
+    def prepare(self, cfg: SolverConfig, strategy=None, phase_profile: bool = False) -> "Launch":
         """Allocate outputs and build the launch arguments once; the
         returned Launch can be replayed (bench) or run once (solve)."""
         torch = _torch()
         strategy = strategy or TeamBatched()
         if isinstance(strategy, NaiveLoop):
             raise NotImplementedError("NaiveLoop per-operation dispatch is not provided on the B200 path")
-        threads = self.default_threads()
-        grid = 0
-        if isinstance(strategy, TeamBatched):
-            if strategy.team_size is not None:
-                threads = strategy.team_size
-            grid = strategy.teams or 0
-        elif isinstance(strategy, SerialReference):
-            grid = 1
         h = self.host
-        if (threads < 8 * h.max_leaves or threads > MAX_CTA_THREADS
-                or h.max_nf > MAX_DOFS_PER_THREAD * threads):
-            raise nat.NativeError(nat.FRB_E_TOO_LARGE,
-                                  f"team_size {threads} cannot hold {h.max_leaves} pairwise leaves / "
-                                  f"{h.max_nf} free DOFs (cluster path needed)")
-        n = int(self.host.node_base[-1])
+        groups = h.groups.copy()
+        for g in groups:
+            if isinstance(strategy, TeamBatched):
+                if strategy.team_size is not None:
+                    g["block_threads"] = strategy.team_size
+                if strategy.teams is not None:
+                    g["grid_clusters"] = strategy.teams
+            elif isinstance(strategy, SerialReference):
+                g["grid_clusters"] = 1
+            T = int(g["block_threads"])
+            if int(g["max_own_dofs"]) > dofs_per_thread_cap(T) * T:
+                raise nat.NativeError(nat.FRB_E_TOO_LARGE,
+                                      f"team_size {T} cannot hold {int(g['max_own_dofs'])} own DOFs")
+        n = int(h.node_base[-1])
         dev = self.device
         u = torch.empty(3 * n, dtype=torch.float64, device=dev)
         f = torch.empty(3 * n, dtype=torch.float64, device=dev)
-        res = torch.zeros(self.host.n_problems * nat.RESULT_DTYPE.itemsize, dtype=torch.uint8, device=dev)
-        queue = torch.zeros(1, dtype=torch.int32, device=dev)
-        desc_t = self._desc_tensor(cfg)
-        return Launch(self, self.frb_batch(desc_t, u, f, res, queue), config_struct(cfg), threads, grid,
-                      DeviceResults(u=u, f=f, results=res, node_base=self.host.node_base),
-                      keep=(desc_t, queue))
+        work = torch.empty(3 * n + 1, dtype=torch.float64, device=dev)
+        res = torch.zeros(h.n_problems * nat.RESULT_DTYPE.itemsize, dtype=torch.uint8, device=dev)
+        queue = torch.zeros(max(len(groups), 1), dtype=torch.int32, device=dev)
+        desc = h.desc.copy()
+        desc["dt"] = [cfg.dt_safety * p.dt_base for p in h.problems]
+        desc_t = torch.from_numpy(desc.view(np.uint8).copy()).to(dev)
+        groups_c = np.ascontiguousarray(groups)
+        fb = nat.FrbBatch()
+        fb.n_problems = h.n_problems
+        fb.n_groups = len(groups)
+        fb.groups = groups_c.ctypes.data
+        t = self.t
+        for k in ("parts", "order", "X", "node_mass", "inc_node", "inc", "elem_ab", "elem_L", "elem_EA",
+                  "plans", "ell_o", "ell_c", "act_ab", "act_L", "act_EA", "halo_g", "send"):
+            setattr(fb, k, t[k].data_ptr() if k in t and t[k].numel() else None)
+        fb.problems = desc_t.data_ptr()
+        fb.u, fb.f, fb.work = u.data_ptr(), f.data_ptr(), work.data_ptr()
+        fb.results, fb.queue = res.data_ptr(), queue.data_ptr()
+        phase = None
+        if phase_profile:
+            phase = torch.zeros(8 * 148 * 16, dtype=torch.int64, device=dev)
+            fb.phase_cycles = phase.data_ptr()
+        return Launch(self, fb, config_struct(cfg), groups_c,
+                      DeviceResults(u=u, f=f, results=res, node_base=h.node_base),
+                      keep=(desc_t, queue, work, groups_c), phase=phase)
 
     def solve(self, cfg: SolverConfig, strategy=None, stream=None) -> DeviceResults:
-        """Launch the persistent kernel; returns device-resident results
+        """Launch the persistent kernels; returns device-resident results
         (asynchronous on the current torch stream)."""
         launch = self.prepare(cfg, strategy)
         launch.run(stream)
@@ -509,17 +524,20 @@ class Launch:
     dbatch: DeviceBatch
     fb: nat.FrbBatch
     fc: nat.FrbConfig
-    threads: int
-    grid: int
+    groups: np.ndarray
     out: DeviceResults
     keep: tuple = ()
+    phase: object = None
+
+    @property
+    def threads(self) -> int:
+        return int(self.groups["block_threads"].max()) if len(self.groups) else 0
 
     def run(self, stream=None):
-        """One frb_solve_batch call (one kernel launch) on `stream`."""
+        """One frb_solve_batch call (one kernel launch per group) on `stream`."""
         torch = _torch()
         s = stream if stream is not None else torch.cuda.current_stream(self.dbatch.device)
-        nat.check(nat.lib().frb_solve_batch(C.byref(self.fb), C.byref(self.fc), self.threads,
-                                            self.grid, C.c_void_p(s.cuda_stream)))
+        nat.check(nat.lib().frb_solve_batch(C.byref(self.fb), C.byref(self.fc), C.c_void_p(s.cuda_stream)))
 
 
 def config_struct(cfg: SolverConfig) -> nat.FrbConfig:
@@ -575,8 +593,7 @@ def solve_batch(batch: Batch, strategy=None, config: SolverConfig | None = None)
     cfg = config or SolverConfig()
     if batch.n_problems == 0:
         return []
-    dbatch = batch.to_device()
-    dres = dbatch.solve(cfg, strategy)
+    dres = batch.to_device().solve(cfg, strategy)
     return results_to_solve_results(batch, dres)
 
 
@@ -586,20 +603,17 @@ def internal_forces_device(network: FiberNetwork, u: np.ndarray) -> np.ndarray:
     """f(u) for one network on the GPU, original DOF order."""
     torch = _torch()
     p = build_problem(network, AffineBC(np.eye(3)), check_mass=False)
-    batch = _pack([network], [None], [p])
+    batch = _pack([network], [None], [p], cluster=1)
     dbatch = batch.to_device()
     n = p.n_nodes
+    launch = dbatch.prepare(SolverConfig())
     u_solver = np.asarray(u, dtype=np.float64).reshape(n, 3)[p.node_order].reshape(-1)
     u_t = torch.from_numpy(u_solver).to(dbatch.device)
     f_t = torch.empty_like(u_t)
-    res = torch.zeros(nat.RESULT_DTYPE.itemsize, dtype=torch.uint8, device=dbatch.device)
-    queue = torch.zeros(1, dtype=torch.int32, device=dbatch.device)
-    desc_t = dbatch._desc_tensor(SolverConfig())
-    fb = dbatch.frb_batch(desc_t, u_t, f_t, res, queue)
     s = torch.cuda.current_stream(dbatch.device)
-    nat.check(nat.lib().frb_internal_forces(C.byref(fb), C.c_void_p(u_t.data_ptr()),
+    nat.check(nat.lib().frb_internal_forces(C.byref(launch.fb), C.c_void_p(u_t.data_ptr()),
                                             C.c_void_p(f_t.data_ptr()), C.c_void_p(s.cuda_stream)))
-    rec = res.cpu().numpy().view(nat.RESULT_DTYPE)[0]
+    rec = launch.out.host_results()[0]
     if rec["status"] == nat.STATUS_SINGULAR:
         e = int(rec["bad_element"])
         raise SingularElementError(f"element {e}: current length collapsed", element=e)

@@ -1,14 +1,18 @@
-// frb_kernels.cu -- persistent dynamic-relaxation kernel for sm_100a (K1).
+// frb_kernels.cu -- persistent dynamic-relaxation cluster kernel for sm_100a.
 //
-// One CTA owns one fiber network at a time, pulled from a device work queue
-// (the spec's TeamBatched strategy; the paper's "one team per
-// sub-problem" kernel).  The whole Fig.-1 loop of the
-// reference (_relax, pkg/src/fibrelax/microsolver.py:379-530) runs inside
-// the kernel; finalize_result (:549-564) runs in its epilogue.
+// A thread-block cluster of C CTAs ("ranks") owns one fiber network at a time,
+// pulled from a device work queue (the spec's TeamBatched strategy,
+// SPEC.md:361; the paper's "one team per sub-problem" kernel,
+// PAPER.md:76-82).  C = 1 for networks that fit one SM; larger networks are
+// split over the cluster by node range and exchange halo positions and
+// pairwise-leaf sums through distributed shared memory (DSMEM).  The whole
+// Fig.-1 loop of the reference (_relax, pkg/src/fibrelax/microsolver.py:
+// 379-530) runs inside the kernel; finalize_result (:549-564) runs in its
+// epilogue.
 //
 // Bit-exactness contract.  Every FP64 operation is an
-// explicit round-to-nearest operation (intrinsics, or the branch-free
-// fast paths of frb_arith.cuh that are bit-identical to them), so no FMA
+// explicit round-to-nearest operation (intrinsics, or the branch-free fast
+// paths of frb_arith.cuh that are bit-identical to them), so no FMA
 // contraction or reassociation can occur; each reference line keeps its
 // evaluation order:
 //   * fiber length sqrt((dx*dx + dz*dz) + dy*dy)        (einsum, :206)
@@ -19,28 +23,30 @@
 //     8*leaf + j sums the stride-8 chain j of its leaf in order, the 8
 //     chains of a leaf sit in 8 consecutive lanes and fold with xor shuffles
 //     1, 2, 4 (= ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7))), tails are added in
-//     order, then leaves combine level by level in SMEM.
+//     order; every rank receives every leaf sum and replays the combine tree
+//     identically, so all ranks take the same decisions.
 //
-// Work split per iteration (one CTA, T threads, DOF d owned by thread d % T):
-//   F  force    thread per free node: gather over its incidence slots -> f
-//   A  per DOF  k_hat, sq = (u k_hat) u, sq2 = (u m) u, ff = f f
-//   C  chains   thread per (leaf, chain): ordered sums of sq, sq2, ff
-//   T  tree     warp 0: pairwise combine, c, residual, convergence
-//   U  per DOF  a = -f/m - c v, two half kicks, drift, new positions
-// Only C is sequential, and only over <= 16 additions per thread; all
-// divisions / square roots run DOF- or node-parallel.
+// Work per iteration on each rank (T threads; own DOF d owned by thread d%T):
+//   F1 coefs   per active element (>= 1 own endpoint): EA (l-L)/(L l)
+//   F2 gather  per own node: f = A + B from the coefficients
+//   A  per DOF k_hat, sq = (u k_hat) u, sq2 = (u m) u, ff = f f
+//   C  chains  per (own leaf, chain): ordered sums -> all ranks' tree slots
+//   T  tree    warp 0: pairwise combine, c, residual, convergence
+//   U  per DOF a = -f/m - c v, two half kicks, drift, positions (+ halo push)
+// Cluster barriers follow C (leaf sums) and U (halo positions).
 //
-// Memory layout per CTA (dynamic SMEM, FP64, nf = 3 * free nodes):
-//   pos  [3][NF]  free-node positions X+u (SoA; conflict-free gathers).
-//                 Between F and U it is dead and holds sq (flat, by DOF).
-//   fcur [nf]     f from F; after A it holds ff
-//   fprv [nf]     f of the previous iteration; after A the current f
-//   sq2  [nf]
-//   slot [2L-1][3] pairwise-tree slots
-// u and v of a thread's <= 8 DOFs live in registers.  Fixed-node positions
-// (constant unless the BC ramps) sit in global scratch and are read through
-// L1, as are masses, X and the slot-major incidence table.
+// Shared memory per rank (offsets identical on every rank of a problem so a
+// peer's buffer is addressed by the same offset):
+//   pos  [3][PS]  positions of own + halo nodes (SoA).  An own DOF's slot
+//                 holds its sq between F and U.
+//   fcur [NFO]    f from F2; after A it holds ff
+//   fprv [NFO]    f of the previous iteration; after A the current f
+//   cf   [CF]     F1 element coefficients, then sq2
+//   slot [2L-1][3] pairwise-tree slots;  prog: the tree's combine program
+// u and v of a thread's own DOFs live in registers; fixed-node positions
+// (constant unless the BC ramps) live in global scratch, read through L1.
 
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
@@ -49,6 +55,8 @@
 
 #include "frb200.h"
 #include "frb_arith.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace {
 
@@ -69,13 +77,11 @@ __device__ __forceinline__ double len2(double dx, double dy, double dz) {
 }
 __device__ __forceinline__ double seg_len(double dx, double dy, double dz) { return dsqrt(len2(dx, dy, dz)); }
 
-// ------------------------------------------------------------------ problem view
+// ------------------------------------------------------------------ problem views
 
 struct Net {
-  int N, NF, nf, M;
-  int S, SA, SB, ea_uniform;
-  int L;  // pairwise leaves
-  int n_levels, root;
+  int N, NF, M, C;
+  int L, n_levels, root, ea_uniform;
   double dt, hdt, volume, ea;
   double g[9];  // F - I
   const double* X;
@@ -85,40 +91,37 @@ struct Net {
   const int2* eab;
   const double* EL;
   const double* EA;
-  const int* ell_o;
-  const double* ell_L;
-  const double* ell_EA;
-  const int* ell_c;
-  const int2* ff_ab;
-  const double* ff_L;
-  const double* ff_EA;
-  int n_ff;
-  const int* leaf_start;
-  const int* leaf_size;
-  const int* level_off;
-  const int* op_dst;
-  const int* op_left;
-  const int* op_right;
-  double* pfix;  // fixed-node positions, AoS [N-NF][3] (global scratch)
+  const int* plan;
+  double* posg;  // [N][3] positions scratch (fixed nodes always; free at the end)
   int64_t node_base;
 };
 
-__device__ void load_net(Net& n, const frb_batch& b, int p) {
+struct Rank {
+  int node0, n_own, n_local, n_act;
+  int S, SA, SB, leaf0, n_leaves;
+  int PS, NFO, CF;  // uniform SMEM strides of the problem (max over ranks)
+  const int* ell_o;
+  const int* ell_c;
+  const int2* act_ab;
+  const double* act_L;
+  const double* act_EA;
+  const int* halo_g;
+  const int2* send;
+};
+
+__device__ void load_views(Net& n, Rank& R, const frb_batch& b, int p, int r) {
   const frb_problem& P = b.problems[p];
   n.N = P.n_nodes;
   n.NF = P.n_free_nodes;
-  n.nf = 3 * P.n_free_nodes;
   n.M = P.n_elems;
-  n.S = P.ell_stride;
-  n.SA = P.ell_slots_a;
-  n.SB = P.ell_slots_b;
+  n.C = P.cluster;
   n.ea_uniform = P.flags & FRB_PF_EA_UNIFORM;
   n.dt = P.dt;
   n.hdt = dmul(0.5, P.dt);
   n.volume = P.volume;
   n.ea = P.ea;
-  for (int r = 0; r < 3; ++r)
-    for (int c = 0; c < 3; ++c) n.g[3 * r + c] = dsub(P.F[3 * r + c], r == c ? 1.0 : 0.0);
+  for (int i = 0; i < 3; ++i)
+    for (int c = 0; c < 3; ++c) n.g[3 * i + c] = dsub(P.F[3 * i + c], i == c ? 1.0 : 0.0);
   n.node_base = P.node_base;
   n.X = b.X + 3 * P.node_base;
   n.mass = b.node_mass + P.node_base;
@@ -127,26 +130,37 @@ __device__ void load_net(Net& n, const frb_batch& b, int p) {
   n.eab = reinterpret_cast<const int2*>(b.elem_ab) + P.elem_base;
   n.EL = b.elem_L + P.elem_base;
   n.EA = b.elem_EA + P.elem_base;
-  n.ell_o = b.ell_other + P.ell_base;
-  n.ell_L = b.ell_L + P.ellv_base;
-  n.ell_EA = b.ell_EA ? b.ell_EA + P.ellv_base : nullptr;
-  n.ell_c = b.ell_c + P.ell_base;
-  n.ff_ab = reinterpret_cast<const int2*>(b.ff_ab) + P.ff_base;
-  n.ff_L = b.ff_L + P.ffv_base;
-  n.ff_EA = b.ff_EA ? b.ff_EA + P.ffv_base : nullptr;
-  n.n_ff = P.n_ff;
-  n.pfix = b.work ? b.work + 3 * P.node_base : nullptr;
-  const int* flat = b.plans + P.plan_base;
-  n.L = flat[0];
-  n.n_levels = flat[1];
-  n.root = flat[2];
-  const int K = n.L > 0 ? n.L - 1 : 0;
-  n.leaf_start = flat + 4;
-  n.leaf_size = n.leaf_start + n.L;
-  n.level_off = n.leaf_size + n.L;
-  n.op_dst = n.level_off + n.n_levels + 1;
-  n.op_left = n.op_dst + K;
-  n.op_right = n.op_left + K;
+  n.plan = b.plans + P.plan_base;
+  n.L = n.plan[0];
+  n.n_levels = n.plan[1];
+  n.root = n.plan[2];
+  n.posg = b.work + 3 * P.node_base;
+  const frb_part& Q = b.parts[P.part_base + r];
+  R.node0 = Q.node0;
+  R.n_own = Q.n_own;
+  R.n_local = Q.n_local;
+  R.n_act = Q.n_act;
+  R.S = Q.ell_stride;
+  R.SA = Q.slots_a;
+  R.SB = Q.slots_b;
+  R.leaf0 = Q.leaf0;
+  R.n_leaves = Q.n_leaves;
+  // uniform strides: maxima over the problem's ranks
+  R.PS = R.NFO = R.CF = 0;
+  for (int q = 0; q < n.C; ++q) {
+    const frb_part& Qq = b.parts[P.part_base + q];
+    R.PS = max(R.PS, Qq.n_local);
+    R.NFO = max(R.NFO, 3 * Qq.n_own);
+    R.CF = max(R.CF, Qq.n_act);
+  }
+  R.CF = max(R.CF, R.NFO);
+  R.ell_o = b.ell_o + Q.ell_base;
+  R.ell_c = b.ell_c + Q.ell_base;
+  R.act_ab = reinterpret_cast<const int2*>(b.act_ab) + Q.act_base;
+  R.act_L = b.act_L + P.actv_base + Q.actv_off;
+  R.act_EA = (b.act_EA && !n.ea_uniform) ? b.act_EA + P.actv_base + Q.actv_off : nullptr;
+  R.halo_g = b.halo_g + Q.halo_base;
+  R.send = reinterpret_cast<const int2*>(b.send) + Q.send_base;
 }
 
 // u_presc[i][j] = x @ (F-I)^T as OpenBLAS evaluates it (microsolver.py:320-322):
@@ -168,15 +182,20 @@ __device__ __forceinline__ double fixed_u(const Net& n, int node, int j, double 
 
 // ------------------------------------------------------------------ positions
 
-// Solver positions: free nodes from SMEM (SoA), fixed nodes from the global
-// scratch (AoS).
-struct PosSolver {
-  const double* p;     // [3][NF]
-  const double* pfix;  // [N-NF][3]
-  int NF;
+// Rank-local numbering: own + halo nodes in SMEM (SoA, stride PS), fixed
+// nodes from the global scratch (AoS by solver id).
+struct PosRank {
+  const double* p;
+  const double* posg;
+  int PS, n_local, NF;
   __device__ __forceinline__ double operator()(int node, int axis) const {
-    return node < NF ? p[axis * NF + node] : pfix[3 * (node - NF) + axis];
+    return node < n_local ? p[axis * PS + node] : posg[3 * (NF + node - n_local) + axis];
   }
+};
+// Solver numbering, all positions from global memory.
+struct PosGlobalAll {
+  const double* posg;
+  __device__ __forceinline__ double operator()(int node, int axis) const { return posg[3 * node + axis]; }
 };
 // X + u recomputed from global memory (one-shot internal_forces).
 struct PosGlobal {
@@ -187,53 +206,7 @@ struct PosGlobal {
   }
 };
 
-// ------------------------------------------------------------------ gathers
-
-// One element's end-force vector nd = d*coef with d = P[b] - P[a] (exact
-// intrinsics; used off the hot path).  Returns true when it collapsed.
-__device__ __forceinline__ bool element_force(double dx, double dy, double dz, double L, double EA,
-                                              double& nx, double& ny, double& nz) {
-  const double l = seg_len(dx, dy, dz);
-  const double coef = ddiv(dmul(EA, dsub(l, L)), dmul(L, l));
-  nx = dmul(dx, coef);
-  ny = dmul(dy, coef);
-  nz = dmul(dz, coef);
-  return l < dmul(kCollapse, L);
-}
-
-// Internal force at node i from the CSR incidence lists (all nodes; used by
-// the epilogue, the singular path and internal_forces).
-template <class Pos>
-__device__ __forceinline__ bool node_force_csr(const Net& n, const Pos& pos, int i, double& fx,
-                                               double& fy, double& fz) {
-  const int2 meta = n.incn[i];
-  const int first = meta.x;
-  const int na = meta.y & 0xffff;
-  const int nb = (meta.y >> 16) & 0xffff;
-  const double px = pos(i, 0), py = pos(i, 1), pz = pos(i, 2);
-  double ax = 0.0, ay = 0.0, az = 0.0, bx = 0.0, by = 0.0, bz = 0.0;
-  bool bad = false;
-  for (int k = 0; k < na + nb; ++k) {
-    const int2 e = n.inc[first + k];
-    const double ox = pos(e.x, 0), oy = pos(e.x, 1), oz = pos(e.x, 2);
-    double nx, ny, nz;
-    if (k < na) {
-      bad |= element_force(dsub(ox, px), dsub(oy, py), dsub(oz, pz), n.EL[e.y], n.EA[e.y], nx, ny, nz);
-      ax = dsub(ax, nx);  // bincount(ia, -nd): 0 + (-nd) + ...
-      ay = dsub(ay, ny);
-      az = dsub(az, nz);
-    } else {
-      bad |= element_force(dsub(px, ox), dsub(py, oy), dsub(pz, oz), n.EL[e.y], n.EA[e.y], nx, ny, nz);
-      bx = dadd(bx, nx);  // bincount(ib, nd)
-      by = dadd(by, ny);
-      bz = dadd(bz, nz);
-    }
-  }
-  fx = dadd(ax, bx);
-  fy = dadd(ay, by);
-  fz = dadd(az, bz);
-  return bad;
-}
+// ------------------------------------------------------------------ element math
 
 // Exact (intrinsic) fallbacks, kept out of line so the rare path does not
 // inflate the register allocation of the hot loops.  Results come back by
@@ -266,99 +239,148 @@ __device__ __forceinline__ LenCoef len_coef(double dx, double dy, double dz, dou
   return r;
 }
 
-// Slot-major incidence view of the free nodes (see frb200.h: ell_*).
-struct Ell {
-  const int* __restrict__ o;      // other endpoint, -1 = padding
-  const int* __restrict__ c;      // free-free element index, -1 = other is fixed
-  const double* __restrict__ L;   // reference length (used when c < 0)
-  const double* __restrict__ EA;  // E*A per slot, nullptr when uniform
-  double ea;
-  int SA, SB, S;
-};
-
-// Sum over one role's slots of free node i, in slot (= element) order:
-// role a accumulates 0 - nd - nd ..., role b 0 + nd + nd ...  Elements to a
-// free neighbour take the coefficient computed once in phase F1 (coef[c])
-// and recompute d = P[b] - P[a] from the same operands, so nd is bitwise the
-// value the reference's per-element pass produces; elements to a fixed
-// neighbour are evaluated here.  Padding slots are skipped (exact: the
-// reference adds nothing there).
-template <bool ROLE_A>
-__device__ __forceinline__ void ell_role(const Ell& E, const double* __restrict__ coef, int k0, int k1, int i,
-                                         const PosSolver& pos, double px, double py, double pz, double& sx,
-                                         double& sy, double& sz, bool& bad) {
-  for (int k = k0; k < k1; ++k) {
-    const int o = __ldg(E.o + k * E.S + i);
-    if (o < 0) continue;
-    const int c = __ldg(E.c + k * E.S + i);
-    const double ox = pos(o, 0), oy = pos(o, 1), oz = pos(o, 2);
-    const double dx = ROLE_A ? dsub(ox, px) : dsub(px, ox);
-    const double dy = ROLE_A ? dsub(oy, py) : dsub(py, oy);
-    const double dz = ROLE_A ? dsub(oz, pz) : dsub(pz, oz);
-    double cf;
-    if (c >= 0) {
-      cf = coef[c];
-    } else {
-      const double L = __ldg(E.L + k * E.S + i);
-      const double EA = E.EA ? __ldg(E.EA + k * E.S + i) : E.ea;
-      const LenCoef lc = len_coef(dx, dy, dz, L, EA);
-      bad |= lc.l < dmul(kCollapse, L);
-      cf = lc.coef;
-    }
-    if (ROLE_A) {  // bincount(ia, -nd): 0 + (-nd) + ...
-      sx = dsub(sx, dmul(dx, cf));
-      sy = dsub(sy, dmul(dy, cf));
-      sz = dsub(sz, dmul(dz, cf));
-    } else {  // bincount(ib, nd)
-      sx = dadd(sx, dmul(dx, cf));
-      sy = dadd(sy, dmul(dy, cf));
-      sz = dadd(sz, dmul(dz, cf));
-    }
-  }
+// One element's end-force vector nd = d*coef with d = P[b] - P[a] (exact
+// intrinsics; used off the hot path).  Returns true when it collapsed.
+__device__ __forceinline__ bool element_force(double dx, double dy, double dz, double L, double EA,
+                                              double& nx, double& ny, double& nz) {
+  const double l = seg_len(dx, dy, dz);
+  const double coef = ddiv(dmul(EA, dsub(l, L)), dmul(L, l));
+  nx = dmul(dx, coef);
+  ny = dmul(dy, coef);
+  nz = dmul(dz, coef);
+  return l < dmul(kCollapse, L);
 }
 
-// Internal force at free node i (phase F2).
-__device__ __forceinline__ bool node_force_ell(const Ell& E, const double* __restrict__ coef,
-                                               const PosSolver& pos, int i, double& fx, double& fy,
-                                               double& fz) {
+// Internal force at node i from the CSR incidence lists (all nodes, solver
+// numbering; used by the epilogue, the singular path and internal_forces).
+template <class Pos>
+__device__ __noinline__ bool node_force_csr(const Net& n, const Pos& pos, int i, double& fx,
+                                               double& fy, double& fz) {
+  const int2 meta = n.incn[i];
+  const int first = meta.x;
+  const int na = meta.y & 0xffff;
+  const int nb = (meta.y >> 16) & 0xffff;
   const double px = pos(i, 0), py = pos(i, 1), pz = pos(i, 2);
   double ax = 0.0, ay = 0.0, az = 0.0, bx = 0.0, by = 0.0, bz = 0.0;
   bool bad = false;
-  ell_role<true>(E, coef, 0, E.SA, i, pos, px, py, pz, ax, ay, az, bad);
-  ell_role<false>(E, coef, E.SA, E.SA + E.SB, i, pos, px, py, pz, bx, by, bz, bad);
+  for (int k = 0; k < na + nb; ++k) {
+    const int2 e = n.inc[first + k];
+    const double ox = pos(e.x, 0), oy = pos(e.x, 1), oz = pos(e.x, 2);
+    double nx, ny, nz;
+    if (k < na) {
+      bad |= element_force(dsub(ox, px), dsub(oy, py), dsub(oz, pz), n.EL[e.y], n.EA[e.y], nx, ny, nz);
+      ax = dsub(ax, nx);  // bincount(ia, -nd): 0 + (-nd) + ...
+      ay = dsub(ay, ny);
+      az = dsub(az, nz);
+    } else {
+      bad |= element_force(dsub(px, ox), dsub(py, oy), dsub(pz, oz), n.EL[e.y], n.EA[e.y], nx, ny, nz);
+      bx = dadd(bx, nx);  // bincount(ib, nd)
+      by = dadd(by, ny);
+      bz = dadd(bz, nz);
+    }
+  }
   fx = dadd(ax, bx);
   fy = dadd(ay, by);
   fz = dadd(az, bz);
   return bad;
 }
 
-// Phase F1: coefficient EA (l - L) / (L l) of every free-free element, once
-// per iteration, fiber-parallel (microsolver.py:196-211).
-__device__ __forceinline__ bool free_free_coefs(const Net& n, const double* __restrict__ pos, int NF,
-                                                double* __restrict__ coef) {
+// Phase F1: coefficient EA (l - L) / (L l) of every active element of the
+// rank, once per iteration (microsolver.py:196-211).  Elements cut by a rank
+// boundary are evaluated by both ranks from identical operands.
+__device__ __forceinline__ void act_one(const Rank& R, double ea, const PosRank& P, int e, int2 ab, double L,
+                                        double* __restrict__ cf, bool& bad) {
+  const double EA = R.act_EA ? __ldg(R.act_EA + e) : ea;
+  const double dx = dsub(P(ab.y, 0), P(ab.x, 0));
+  const double dy = dsub(P(ab.y, 1), P(ab.x, 1));
+  const double dz = dsub(P(ab.y, 2), P(ab.x, 2));
+  const LenCoef lc = len_coef(dx, dy, dz, L, EA);
+  bad |= lc.l < dmul(kCollapse, L);
+  cf[e] = lc.coef;
+}
+
+__device__ __forceinline__ bool element_coefs(const Rank& R, double ea, const PosRank& P,
+                                              double* __restrict__ cf) {
   bool bad = false;
-  for (int e = threadIdx.x; e < n.n_ff; e += blockDim.x) {
-    const int2 ab = __ldg(n.ff_ab + e);
-    const double L = __ldg(n.ff_L + e);
-    const double EA = n.ff_EA ? __ldg(n.ff_EA + e) : n.ea;
-    const double dx = dsub(pos[ab.y], pos[ab.x]);
-    const double dy = dsub(pos[NF + ab.y], pos[NF + ab.x]);
-    const double dz = dsub(pos[2 * NF + ab.y], pos[2 * NF + ab.x]);
-    const LenCoef lc = len_coef(dx, dy, dz, L, EA);
-    bad |= lc.l < dmul(kCollapse, L);
-    coef[e] = lc.coef;
+  const int T = blockDim.x;
+  int e = threadIdx.x;
+  for (; e + T < R.n_act; e += 2 * T) {  // two elements per step: their loads overlap
+    const int2 ab0 = __ldg(R.act_ab + e), ab1 = __ldg(R.act_ab + e + T);
+    const double L0 = __ldg(R.act_L + e), L1 = __ldg(R.act_L + e + T);
+    act_one(R, ea, P, e, ab0, L0, cf, bad);
+    act_one(R, ea, P, e + T, ab1, L1, cf, bad);
   }
+  if (e < R.n_act) act_one(R, ea, P, e, __ldg(R.act_ab + e), __ldg(R.act_L + e), cf, bad);
   return bad;
+}
+
+// Phase F2: internal force at own node i, summed over its slots in slot
+// (= element) order: role a accumulates 0 - nd - nd ..., role b
+// 0 + nd + nd ...  nd = d * coef with d = P[b] - P[a] recomputed from the
+// operands F1 used, so it is bitwise the reference's per-element value.
+// Padding slots are skipped (exact: the reference adds nothing there).  The
+// slot table of a chunk is loaded up front so its latencies overlap.
+constexpr int kSlots = 6;
+
+__device__ __forceinline__ void node_force_ell(const Rank& R, const double* __restrict__ cf, const PosRank& P,
+                                               int i, double& fx, double& fy, double& fz) {
+  const double px = P(i, 0), py = P(i, 1), pz = P(i, 2);
+  double ax = 0.0, ay = 0.0, az = 0.0, bx = 0.0, by = 0.0, bz = 0.0;
+  const int ns = R.SA + R.SB;
+  for (int k0 = 0; k0 < ns; k0 += kSlots) {
+    int o[kSlots], c[kSlots];
+#pragma unroll
+    for (int q = 0; q < kSlots; ++q) {
+      const int k = k0 + q;
+      o[q] = k < ns ? __ldg(R.ell_o + k * R.S + i) : -1;
+      c[q] = k < ns ? __ldg(R.ell_c + k * R.S + i) : 0;
+    }
+#pragma unroll
+    for (int q = 0; q < kSlots; ++q) {
+      if (o[q] < 0) continue;
+      const bool role_a = k0 + q < R.SA;
+      const double ox = P(o[q], 0), oy = P(o[q], 1), oz = P(o[q], 2);
+      const double coef = cf[c[q]];
+      const double dx = role_a ? dsub(ox, px) : dsub(px, ox);
+      const double dy = role_a ? dsub(oy, py) : dsub(py, oy);
+      const double dz = role_a ? dsub(oz, pz) : dsub(pz, oz);
+      const double nx = dmul(dx, coef), ny = dmul(dy, coef), nz = dmul(dz, coef);
+      if (role_a) {  // bincount(ia, -nd): 0 + (-nd) + ...
+        ax = dsub(ax, nx);
+        ay = dsub(ay, ny);
+        az = dsub(az, nz);
+      } else {  // bincount(ib, nd)
+        bx = dadd(bx, nx);
+        by = dadd(by, ny);
+        bz = dadd(bz, nz);
+      }
+    }
+  }
+  fx = dadd(ax, bx);
+  fy = dadd(ay, by);
+  fz = dadd(az, bz);
 }
 
 // ------------------------------------------------------------------ block helpers
 
 struct Scalars {
+  long long clk[8];  // per-phase cycle totals (thread 0, when instrumented)
+  long long t_last;
   double c, residual, r_ref, threshold;
   double red[kMaxWarps * 9];
   int ired[kMaxWarps];
   int problem, done, converged, singular;
 };
+
+// Phase timing: thread 0 charges the cycles since the previous mark to
+// phase `ph` (called right after a barrier, so it measures the critical path).
+__device__ __forceinline__ void mark(Scalars& sc, bool on, int ph) {
+  if (on && threadIdx.x == 0) {
+    const long long now = clock64();
+    sc.clk[ph] += now - sc.t_last;
+    sc.t_last = now;
+  }
+}
 
 // numpy argmin over (l - eps) with NaN-first semantics: does (va, ia) come first?
 __device__ __forceinline__ bool argmin_before(double va, int ia, double vb, int ib) {
@@ -392,7 +414,7 @@ __device__ void block_sum9(double v[9], Scalars& sc) {
 // Singular-element path: the reference raises SingularElementError naming
 // argmin(length - eps_len) over all elements (microsolver.py:207-209).
 template <class Pos>
-__device__ int singular_argmin(const Net& n, const Pos& pos, Scalars& sc) {
+__device__ __noinline__ int singular_argmin(const Net& n, const Pos& pos, Scalars& sc) {
   constexpr int kNone = 0x7fffffff;
   double best = 0.0;
   int besti = kNone;
@@ -439,12 +461,15 @@ __device__ int singular_argmin(const Net& n, const Pos& pos, Scalars& sc) {
   return result;
 }
 
-// Length check of every element (init and ramp iterations, when elements
-// between fixed nodes move).  Sets sc.singular.
-__device__ void check_all_elements(const Net& n, const PosSolver& pos, Scalars& sc) {
+// Length check of elements whose endpoints are both fixed (their only motion
+// is the BC ramp; every other element is checked in F1).  With all_elements,
+// every element is checked (init, positions from posg).  Sets sc.singular.
+template <class Pos>
+__device__ __noinline__ void check_elements(const Net& n, const Pos& pos, Scalars& sc, bool all_elements) {
   bool bad = false;
   for (int e = threadIdx.x; e < n.M; e += blockDim.x) {
     const int2 ab = n.eab[e];
+    if (!all_elements && (ab.x < n.NF || ab.y < n.NF)) continue;
     const double dx = dsub(pos(ab.y, 0), pos(ab.x, 0));
     const double dy = dsub(pos(ab.y, 1), pos(ab.x, 1));
     const double dz = dsub(pos(ab.y, 2), pos(ab.x, 2));
@@ -453,28 +478,16 @@ __device__ void check_all_elements(const Net& n, const PosSolver& pos, Scalars& 
   if (bad) sc.singular = 1;
 }
 
-__device__ __forceinline__ void set_fixed_positions(const Net& n, double alpha, bool ramp) {
-  for (int i = n.NF + threadIdx.x; i < n.N; i += blockDim.x)
-    for (int j = 0; j < 3; ++j) n.pfix[3 * (i - n.NF) + j] = dadd(n.X[3 * i + j], fixed_u(n, i, j, alpha, ramp));
+// Fixed-node positions into global scratch, split over the cluster's ranks.
+__device__ __noinline__ void set_fixed_positions(const Net& n, int rank, double alpha, bool ramp) {
+  for (int i = n.NF + rank * blockDim.x + threadIdx.x; i < n.N; i += n.C * blockDim.x)
+    for (int j = 0; j < 3; ++j) n.posg[3 * i + j] = dadd(n.X[3 * i + j], fixed_u(n, i, j, alpha, ramp));
 }
 
 __device__ __forceinline__ double ramp_alpha(int it_plus_1, int ramp) {
   // Python: min(1.0, (it + 1) / ramp)
   const double x = ddiv(static_cast<double>(it_plus_1), static_cast<double>(ramp));
   return x < 1.0 ? x : 1.0;
-}
-
-__device__ void write_singular(const frb_batch& b, int p, int bad, int iters) {
-  if (threadIdx.x == 0) {
-    frb_result& r = b.results[p];
-    r.status = FRB_STATUS_SINGULAR;
-    r.bad_element = bad;
-    r.iters = iters;
-    r.converged = 0;
-    r.final_residual = qnan();
-    r.r_ref = qnan();
-    r.energy_residual = qnan();
-  }
 }
 
 // Quotients num(k)/den(k) for the DOFs k < MAXK a thread owns (has(k)); use
@@ -491,31 +504,116 @@ __device__ __forceinline__ void batched_div(Has has, Num num, Den den, Use use) 
   }
 }
 
+// Cluster-wide barrier with release/acquire semantics (DSMEM and global
+// memory writes before it are visible after it); a CTA barrier when C == 1.
+__device__ __forceinline__ void csync(int C) {
+  if (C > 1) {
+    cg::this_cluster().sync();
+  } else {
+    __syncthreads();
+  }
+}
+
+template <class T>
+__device__ __forceinline__ T* peer(T* p, int q) {
+  return cg::this_cluster().map_shared_rank(p, q);
+}
+
+// Epilogue on rank 0: reactions at the fixed nodes from the final positions
+// (posg), their displacements, sigma = sym(sum r (x) x)/V (microsolver.py:
+// 285-299; deterministic order, tolerance-only vs the reference's BLAS) and
+// the result record.
+__device__ __noinline__ void fixed_forces_and_stress(const frb_batch& b, int p, const Net& n, Scalars& sc,
+                                                     int it, double alpha, bool ramp, int full_bc_iter) {
+  const int T = blockDim.x, t = threadIdx.x;
+  double* uo = b.u + 3 * n.node_base;
+  double* fo = b.f + 3 * n.node_base;
+  double s9[9];
+#pragma unroll
+  for (int r = 0; r < 9; ++r) s9[r] = 0.0;
+  const PosGlobalAll G{n.posg};
+  for (int i = n.NF + t; i < n.N; i += T) {
+    double f3[3];
+    node_force_csr(n, G, i, f3[0], f3[1], f3[2]);
+    for (int jj = 0; jj < 3; ++jj) {
+      uo[3 * i + jj] = fixed_u(n, i, jj, alpha, ramp);
+      fo[3 * i + jj] = f3[jj];
+    }
+    // S = r^T x over boundary nodes (sorted ids == solver order), x = X + u
+    for (int a = 0; a < 3; ++a)
+      for (int c3 = 0; c3 < 3; ++c3) s9[3 * a + c3] = dadd(s9[3 * a + c3], dmul(f3[a], G(i, c3)));
+  }
+  block_sum9(s9, sc);
+  if (t == 0) {
+    frb_result& r = b.results[p];
+    const double two_v = dmul(2.0, n.volume);
+    for (int a = 0; a < 3; ++a)
+      for (int c3 = 0; c3 < 3; ++c3) r.avg_stress[3 * a + c3] = ddiv(dadd(s9[3 * a + c3], s9[3 * c3 + a]), two_v);
+    r.status = sc.converged ? FRB_STATUS_CONVERGED : FRB_STATUS_MAX_ITERS;
+    r.converged = sc.converged;
+    r.iters = it + 1;
+    r.bad_element = -1;
+    r.final_residual = sc.residual;
+    r.r_ref = (full_bc_iter <= it) ? sc.r_ref : qnan();
+    r.energy_residual = qnan();
+    for (int e = 0; e < 4; ++e) r.energy[e] = 0.0;
+  }
+}
+
 // ------------------------------------------------------------------ the solve
 
+struct Smem {
+  double* pos;   // [3][PS]
+  double* fcur;  // [NFO]
+  double* fprv;  // [NFO]
+  double* cf;    // [CF]
+  double* slot;  // [2L-1][3]
+  int* prog;     // [levels+1] level offsets, then dst, left, right
+};
+
+__device__ __forceinline__ Smem carve(double* smem, const Net& n, const Rank& R) {
+  Smem s;
+  s.pos = smem;
+  s.fcur = s.pos + 3 * R.PS;
+  s.fprv = s.fcur + R.NFO;
+  s.cf = s.fprv + R.NFO;
+  s.slot = s.cf + R.CF;
+  s.prog = reinterpret_cast<int*>(s.slot + 3 * (n.L > 0 ? 2 * n.L - 1 : 1));
+  return s;
+}
+
 template <int MAXK>
-__device__ void solve_one(const frb_batch& b, const frb_config& cfg, int p, double* smem, Scalars& sc,
-                          const Net& n) {
+__device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, int rank, double* smem,
+                              Scalars& sc, const Net& n, const Rank& R) {
   const int T = blockDim.x, t = threadIdx.x, lane = t & 31;
-  const int NF = n.NF, nf = n.nf, L = n.L;
-  double* pos = smem;        // [3][NF]; sq between phases F and U
-  double* fcur = pos + nf;   // [nf]
-  double* fprv = fcur + nf;  // [nf]
-  double* sq2 = fprv + nf;   // [max(nf, n_ff)]: F1 coefficients, then sq2
-  double* slot = sq2 + (nf > n.n_ff ? nf : n.n_ff);  // [2L-1][3]
-  const PosSolver P{pos, n.pfix, NF};
+  const int C = n.C, NF = n.NF, L = n.L, n_own = R.n_own, nfo = 3 * n_own;
+  const Smem S = carve(smem, n, R);
+  double* __restrict__ pos = S.pos;
+  double* __restrict__ fcur = S.fcur;
+  double* __restrict__ fprv = S.fprv;
+  double* __restrict__ cf = S.cf;
+  double* __restrict__ slot = S.slot;
+  const int PS = R.PS;
+  const PosRank P{pos, n.posg, PS, R.n_local, NF};
+  const double* __restrict__ Xg = n.X;
+  const double* __restrict__ mass = n.mass;
+  const int dof0 = 3 * R.node0;
+
   // the tree's combine program lives in SMEM (warp 0 walks it every iteration)
   const int n_ops = L > 0 ? L - 1 : 0;
-  int* prog = reinterpret_cast<int*>(slot + 3 * (L > 0 ? 2 * L - 1 : 1));  // [levels+1][3*ops]
-  int* lvl_s = prog;
+  int* lvl_s = S.prog;
   int* dst_s = lvl_s + n.n_levels + 1;
   int* lft_s = dst_s + n_ops;
   int* rgt_s = lft_s + n_ops;
-  for (int k = t; k <= n.n_levels; k += T) lvl_s[k] = n.level_off[k];
-  for (int k = t; k < n_ops; k += T) {
-    dst_s[k] = n.op_dst[k];
-    lft_s[k] = n.op_left[k];
-    rgt_s[k] = n.op_right[k];
+  {
+    const int* level_off = n.plan + 4 + 2 * L;
+    const int* op = level_off + n.n_levels + 1;
+    for (int k = t; k <= n.n_levels; k += T) lvl_s[k] = level_off[k];
+    for (int k = t; k < n_ops; k += T) {
+      dst_s[k] = op[k];
+      lft_s[k] = op[n_ops + k];
+      rgt_s[k] = op[2 * n_ops + k];
+    }
   }
 
   const bool adaptive = cfg.damping == FRB_DAMPING_ADAPTIVE;
@@ -524,131 +622,163 @@ __device__ void solve_one(const frb_batch& b, const frb_config& cfg, int p, doub
   const int full_bc_iter = ramp ? ramp_n - 1 : 0;
   const double dt = n.dt, hdt = n.hdt;
   double alpha = ramp ? -1.0 : 1.0;  // -1: fixed nodes still at their zero init
+  const bool prof = b.phase_cycles != nullptr;
 
-  // thread t owns DOFs d = t + k*T (k < MAXK)
-  auto has = [&](int k) { return t + k * T < nf; };
+  // own DOF dl = t + k*T (local DOF; global DOF dof0 + dl)
+  auto has = [&](int k) { return t + k * T < nfo; };
   double u[MAXK], v[MAXK];
 #pragma unroll
   for (int k = 0; k < MAXK; ++k) u[k] = v[k] = 0.0;
 
-  // pairwise-chain role: thread t < 8L sums chain j of leaf t/8
-  const bool chain = t < 8 * L;
-  const int leaf = t >> 3, j = t & 7;
+  // pairwise-chain role: thread t < 8 * own leaves sums chain j of leaf
+  // leaf0 + t/8; DOF offsets are relative to the rank's first DOF
+  const bool chain = t < 8 * R.n_leaves;
+  const int lloc = t >> 3, j = t & 7;
   int lstart = 0, q = 0, nt = 0;
   if (chain) {
-    lstart = n.leaf_start[leaf];
-    const int lsize = n.leaf_size[leaf];
+    const int* leaf_start = n.plan + 4;
+    const int* leaf_size = leaf_start + L;
+    lstart = leaf_start[R.leaf0 + lloc] - dof0;
+    const int lsize = leaf_size[R.leaf0 + lloc];
     q = lsize >= 8 ? (lsize >> 3) : 0;
     nt = lsize - 8 * q;
   }
 
+  // new position of own DOF dl: local SoA slot + the halo copies of peers
+  auto put_pos = [&](int dl, double x) {
+    const int node = dl / 3, axis = dl - 3 * node;
+    pos[axis * PS + node] = x;
+    if (C > 1) {
+      const int2 tg = __ldg(R.send + node);
+      if (tg.x >= 0) peer(pos, tg.x >> 24)[axis * PS + (tg.x & 0xffffff)] = x;
+      if (tg.y >= 0) peer(pos, tg.y >> 24)[axis * PS + (tg.y & 0xffffff)] = x;
+    }
+  };
+
   // ---- prologue: BCs, initial positions (microsolver.py:400-411) ---------
-  for (int i = t; i < NF; i += T)
-    for (int a = 0; a < 3; ++a) pos[a * NF + i] = dadd(n.X[3 * i + a], 0.0);
-  set_fixed_positions(n, alpha, ramp);
-  __syncthreads();
-  check_all_elements(n, P, sc);
+  for (int l = t; l < R.n_local; l += T) {
+    const int g = l < n_own ? R.node0 + l : R.halo_g[l - n_own];
+    for (int a = 0; a < 3; ++a) pos[a * PS + l] = dadd(Xg[3 * g + a], 0.0);
+  }
+  set_fixed_positions(n, rank, alpha, ramp);
+  // initial free positions to global too (the all-element check reads posg)
+  for (int l = t; l < n_own; l += T)
+    for (int a = 0; a < 3; ++a) n.posg[3 * (R.node0 + l) + a] = dadd(Xg[3 * (R.node0 + l) + a], 0.0);
+  csync(C);
+  check_elements(n, PosGlobalAll{n.posg}, sc, true);
   __syncthreads();
   if (sc.singular) {
-    write_singular(b, p, singular_argmin(n, P, sc), 0);
-    __syncthreads();
+    const int bad = singular_argmin(n, PosGlobalAll{n.posg}, sc);
+    if (rank == 0 && t == 0) {
+      frb_result& r = b.results[p];
+      r.status = FRB_STATUS_SINGULAR;
+      r.bad_element = bad;
+      r.iters = 0;
+      r.converged = 0;
+      r.final_residual = r.r_ref = r.energy_residual = qnan();
+    }
     return;
   }
-  // hot loop-invariant views of the incidence table
-  const Ell E{n.ell_o, n.ell_c, n.ell_L, n.ea_uniform ? nullptr : n.ell_EA, n.ea, n.SA, n.SB, n.S};
-  const double* __restrict__ Xg = n.X;
-  const double* __restrict__ mass = n.mass;
-  // initial internal forces on free nodes (:413-420), kept as f_prev
-  free_free_coefs(n, pos, NF, sq2);
+  // initial internal forces on own nodes (:413-420), kept as f_prev
+  element_coefs(R, n.ea, P, cf);
   __syncthreads();
-  for (int i = t; i < NF; i += T) {
+  for (int i = t; i < n_own; i += T) {
     double fx, fy, fz;
-    node_force_ell(E, sq2, P, i, fx, fy, fz);
+    node_force_ell(R, cf, P, i, fx, fy, fz);
     fprv[3 * i] = fx;
     fprv[3 * i + 1] = fy;
     fprv[3 * i + 2] = fz;
   }
   __syncthreads();
   // a = -f/m (:428-430), then iteration 0's kick + drift (:443-448)
-  batched_div<MAXK>(
-      has, [&](int k) { return -fprv[t + k * T]; }, [&](int k) { return __ldg(mass + (t + k * T) / 3); },
-      [&](int k, double a) {
-        const int d = t + k * T;
-        v[k] = dadd(0.0, dmul(hdt, a));
-        u[k] = dadd(0.0, dmul(dt, v[k]));
-        const int node = d / 3;
-        pos[(d - 3 * node) * NF + node] = dadd(__ldg(Xg + d), u[k]);
-      });
+  {
+    batched_div<MAXK>(
+        has, [&](int k) { return -fprv[t + k * T]; }, [&](int k) { return __ldg(mass + (dof0 + t + k * T) / 3); },
+        [&](int k, double a) {
+          const int dl = t + k * T;
+          v[k] = dadd(0.0, dmul(hdt, a));
+          u[k] = dadd(0.0, dmul(dt, v[k]));
+          put_pos(dl, dadd(__ldg(Xg + dof0 + dl), u[k]));
+        });
+  }
   if (ramp) {  // iteration 0's ramp step (:449-453)
     alpha = ramp_alpha(1, ramp_n);
-    set_fixed_positions(n, alpha, ramp);
+    set_fixed_positions(n, rank, alpha, ramp);
   }
-  __syncthreads();
+  csync(C);
 
   // ---- relaxation loop (microsolver.py:434-530) ---------------------------
+  mark(sc, prof, 7);
   int it = 0;
   for (;; ++it) {
-    // F: internal forces at the drifted positions (:456-465): F1 element
-    // coefficients into the sq2 buffer, then F2 per-node gathers
-    bool bad = free_free_coefs(n, pos, NF, sq2);
+    // F: internal forces at the drifted positions (:456-465)
+    bool bad = element_coefs(R, n.ea, P, cf);
+    if (ramp && it < ramp_n) check_elements(n, PosGlobalAll{n.posg}, sc, false);  // fixed-fixed
     __syncthreads();
-    for (int i = t; i < NF; i += T) {
+    mark(sc, prof, 0);
+    for (int i = t; i < n_own; i += T) {
       double fx, fy, fz;
-      bad |= node_force_ell(E, sq2, P, i, fx, fy, fz);
+      node_force_ell(R, cf, P, i, fx, fy, fz);
       fcur[3 * i] = fx;
       fcur[3 * i + 1] = fy;
       fcur[3 * i + 2] = fz;
     }
     if (bad) sc.singular = 1;
-    if (ramp && it < ramp_n) check_all_elements(n, P, sc);
     __syncthreads();
-    if (sc.singular) {
-      write_singular(b, p, singular_argmin(n, P, sc), it);
-      __syncthreads();
-      return;
-    }
+    mark(sc, prof, 1);
 
     // A: k_hat = (f - f_prev)/(dt v) where dt v != 0 else 0, clamped with
     // np.maximum(k_hat, 0) (:468-476); sq = (u k_hat) u, sq2 = (u m) u,
-    // ff = f f (:489).  Outputs: sq -> pos (flat), sq2, ff -> fcur, f -> fprv.
-    batched_div<MAXK>(
-        has, [&](int k) { return dsub(fcur[t + k * T], fprv[t + k * T]); },
-        [&](int k) { return adaptive ? dmul(dt, v[k]) : 0.0; },
-        [&](int k, double kh) {
-          const int d = t + k * T;
-          const double f = fcur[d];
-          if (adaptive) {
-            kh = (kh > 0.0 || isnan(kh)) ? kh : 0.0;
-            pos[d] = dmul(dmul(u[k], kh), u[k]);
-            sq2[d] = dmul(dmul(u[k], __ldg(mass + d / 3)), u[k]);
-          }
-          fcur[d] = dmul(f, f);
-          fprv[d] = f;
-        });
+    // ff = f f (:489).  Outputs: sq -> own position slot, sq2 -> cf,
+    // ff -> fcur, f -> fprv.
+    {
+      batched_div<MAXK>(
+          has, [&](int k) { return dsub(fcur[t + k * T], fprv[t + k * T]); },
+          [&](int k) { return adaptive ? dmul(dt, v[k]) : 0.0; },
+          [&](int k, double kh) {
+            const int dl = t + k * T;
+            const double f = fcur[dl];
+            if (adaptive) {
+              kh = (kh > 0.0 || isnan(kh)) ? kh : 0.0;
+              const int node = dl / 3;
+              pos[(dl - 3 * node) * PS + node] = dmul(dmul(u[k], kh), u[k]);
+              cf[dl] = dmul(dmul(u[k], __ldg(mass + (dof0 + dl) / 3)), u[k]);
+            }
+            fcur[dl] = dmul(f, f);
+            fprv[dl] = f;
+          });
+    }
     __syncthreads();
+    mark(sc, prof, 2);
 
-    // C: ordered chain sums of one leaf chain + fold + tails -> leaf slots
-    if ((t & ~31) < 8 * L) {  // warp holds at least one chain
+    // C: ordered chain sums of one leaf chain + fold + tails -> every rank's
+    // slots; the singular flag travels with them
+    if ((t & ~31) < 8 * R.n_leaves) {  // warp holds at least one chain
       double r0 = 0.0, r1 = 0.0, r2 = 0.0;
       double t0 = 0.0, t1 = 0.0, t2 = 0.0;
+      auto sqv = [&](int dl) {
+        const int node = dl / 3;
+        return pos[(dl - 3 * node) * PS + node];
+      };
       if (chain) {
-        int d = lstart + j;
+        int dl = lstart + j;
         if (q > 0) {
-          r0 = pos[d];
-          r1 = sq2[d];
-          r2 = fcur[d];
+          r0 = sqv(dl);
+          r1 = cf[dl];
+          r2 = fcur[dl];
+#pragma unroll 4
           for (int k = 1; k < q; ++k) {
-            d += 8;
-            r0 = dadd(r0, pos[d]);
-            r1 = dadd(r1, sq2[d]);
-            r2 = dadd(r2, fcur[d]);
+            dl += 8;
+            r0 = dadd(r0, sqv(dl));
+            r1 = dadd(r1, cf[dl]);
+            r2 = dadd(r2, fcur[dl]);
           }
         }
         if (j < nt) {
-          const int dtail = lstart + 8 * q + j;
-          t0 = pos[dtail];
-          t1 = sq2[dtail];
-          t2 = fcur[dtail];
+          const int dtl = lstart + 8 * q + j;
+          t0 = sqv(dtl);
+          t1 = cf[dtl];
+          t2 = fcur[dtl];
         }
         if (!adaptive) r0 = r1 = t0 = t1 = 0.0;
       }
@@ -672,14 +802,39 @@ __device__ void solve_one(const frb_batch& b, const frb_config& cfg, int p, doub
         }
       }
       if (chain && j == 0) {
-        slot[3 * leaf] = r0;
-        slot[3 * leaf + 1] = r1;
-        slot[3 * leaf + 2] = r2;
+        const int s = 3 * (R.leaf0 + lloc);
+        for (int qr = 0; qr < C; ++qr) {
+          double* ds = C > 1 ? peer(slot, qr) : slot;
+          ds[s] = r0;
+          ds[s + 1] = r1;
+          ds[s + 2] = r2;
+        }
       }
     }
-    __syncthreads();
+    if (C > 1 && t == 0 && sc.singular)
+      for (int qr = 0; qr < C; ++qr) *peer(&sc.singular, qr) = 1;
+    csync(C);
+    mark(sc, prof, 3);
+    if (sc.singular) {
+      // positions of every free node to global memory, then the argmin over
+      // all elements (each rank redundantly; rank 0 reports)
+#pragma unroll
+      for (int k = 0; k < MAXK; ++k)
+        if (has(k)) n.posg[dof0 + t + k * T] = dadd(__ldg(Xg + dof0 + t + k * T), u[k]);
+      csync(C);
+      const int badi = singular_argmin(n, PosGlobalAll{n.posg}, sc);
+      if (rank == 0 && t == 0) {
+        frb_result& r = b.results[p];
+        r.status = FRB_STATUS_SINGULAR;
+        r.bad_element = badi;
+        r.iters = it;
+        r.converged = 0;
+        r.final_residual = r.r_ref = r.energy_residual = qnan();
+      }
+      return;
+    }
 
-    // T: tree combine + scalar bookkeeping (warp 0)
+    // T: tree combine + scalar bookkeeping (warp 0 of every rank)
     if (t < 32) {
       for (int lev = 0; lev < n.n_levels; ++lev) {
         const int k1 = lvl_s[lev + 1];
@@ -731,29 +886,31 @@ __device__ void solve_one(const frb_batch& b, const frb_config& cfg, int p, doub
       }
     }
     __syncthreads();
+    mark(sc, prof, 4);
 
     // U: accelerations and second half-kick (:501-507); then the next
     // iteration's first half-kick and drift (:443-453) unless finished
     const double c = sc.c;
     const bool done = sc.done != 0;
-    batched_div<MAXK>(
-        has, [&](int k) { return -fprv[t + k * T]; }, [&](int k) { return __ldg(mass + (t + k * T) / 3); },
-        [&](int k, double fm) {
-          const double a = dsub(fm, dmul(c, v[k]));
-          v[k] = dadd(v[k], dmul(hdt, a));
-          if (!done) {
-            const int d = t + k * T;
+    {
+      batched_div<MAXK>(
+          has, [&](int k) { return -fprv[t + k * T]; }, [&](int k) { return __ldg(mass + (dof0 + t + k * T) / 3); },
+          [&](int k, double fm) {
+            const double a = dsub(fm, dmul(c, v[k]));
             v[k] = dadd(v[k], dmul(hdt, a));
-            u[k] = dadd(u[k], dmul(dt, v[k]));
-            const int node = d / 3;
-            pos[(d - 3 * node) * NF + node] = dadd(__ldg(Xg + d), u[k]);
-          }
-        });
+            if (!done) {
+              v[k] = dadd(v[k], dmul(hdt, a));
+              u[k] = dadd(u[k], dmul(dt, v[k]));
+              put_pos(t + k * T, dadd(__ldg(Xg + dof0 + t + k * T), u[k]));
+            }
+          });
+    }
     if (!done && ramp && alpha < 1.0) {
       alpha = ramp_alpha(it + 2, ramp_n);
-      set_fixed_positions(n, alpha, ramp);
+      set_fixed_positions(n, rank, alpha, ramp);
     }
-    __syncthreads();
+    csync(C);
+    mark(sc, prof, 5);
     if (done) break;
   }
 
@@ -763,79 +920,66 @@ __device__ void solve_one(const frb_batch& b, const frb_config& cfg, int p, doub
 #pragma unroll
   for (int k = 0; k < MAXK; ++k) {
     if (has(k)) {
-      const int d = t + k * T;
+      const int d = dof0 + t + k * T;
       uo[d] = u[k];
-      fo[d] = fprv[d];
-      const int node = d / 3;
-      pos[(d - 3 * node) * NF + node] = dadd(__ldg(Xg + d), u[k]);  // pos held sq
+      fo[d] = fprv[t + k * T];
+      n.posg[d] = dadd(__ldg(Xg + d), u[k]);  // x = X + u, all free nodes
     }
   }
+  csync(C);
+  if (rank == 0) fixed_forces_and_stress(b, p, n, sc, it, alpha, ramp, full_bc_iter);
   __syncthreads();
-  double s9[9];
-#pragma unroll
-  for (int r = 0; r < 9; ++r) s9[r] = 0.0;
-  for (int i = NF + t; i < n.N; i += T) {
-    double f3[3];
-    node_force_csr(n, P, i, f3[0], f3[1], f3[2]);
-    for (int jj = 0; jj < 3; ++jj) {
-      uo[3 * i + jj] = fixed_u(n, i, jj, alpha, ramp);
-      fo[3 * i + jj] = f3[jj];
-    }
-    // S = r^T x over boundary nodes (sorted ids == solver order), x = X + u
-    for (int a = 0; a < 3; ++a)
-      for (int c3 = 0; c3 < 3; ++c3) s9[3 * a + c3] = dadd(s9[3 * a + c3], dmul(f3[a], P(i, c3)));
-  }
-  block_sum9(s9, sc);
-  if (t == 0) {
-    frb_result& r = b.results[p];
-    const double two_v = dmul(2.0, n.volume);
-    for (int a = 0; a < 3; ++a)
-      for (int c3 = 0; c3 < 3; ++c3) r.avg_stress[3 * a + c3] = ddiv(dadd(s9[3 * a + c3], s9[3 * c3 + a]), two_v);
-    r.status = sc.converged ? FRB_STATUS_CONVERGED : FRB_STATUS_MAX_ITERS;
-    r.converged = sc.converged;
-    r.iters = it + 1;
-    r.bad_element = -1;
-    r.final_residual = sc.residual;
-    r.r_ref = (full_bc_iter <= it) ? sc.r_ref : qnan();
-    r.energy_residual = qnan();
-    for (int e = 0; e < 4; ++e) r.energy[e] = 0.0;
-  }
-  __syncthreads();
+  mark(sc, prof, 6);
 }
 
 template <int MAXK, int MAXT>
-__global__ void __launch_bounds__(MAXT, 1) frb_relax_cta_kernel(frb_batch b, frb_config cfg) {
+__global__ void __launch_bounds__(MAXT, 1)
+    frb_relax_kernel(frb_batch b, frb_config cfg, int first, int count, int32_t* queue) {
   extern __shared__ __align__(16) double smem[];
   __shared__ Scalars sc;
   __shared__ Net net;
+  __shared__ Rank rk;
+  const int C = static_cast<int>(cg::this_cluster().num_blocks());
+  const int rank = C > 1 ? static_cast<int>(cg::this_cluster().block_rank()) : 0;
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < 8; ++k) sc.clk[k] = 0;
+    sc.t_last = clock64();
+  }
   for (;;) {
+    if (rank == 0 && threadIdx.x == 0) {
+      const int idx = atomicAdd(queue, 1);
+      for (int q = 0; q < C; ++q) *(C > 1 ? peer(&sc.problem, q) : &sc.problem) = idx;
+    }
+    csync(C);
+    const int idx = sc.problem;
+    if (idx >= count) break;
+    const int p = b.order[first + idx];
     if (threadIdx.x == 0) {
-      const int idx = atomicAdd(b.queue, 1);
-      sc.problem = idx;
-      if (idx < b.n_problems) {
-        load_net(net, b, b.order ? b.order[idx] : idx);
-        sc.singular = 0;
-        sc.done = 0;
-        sc.converged = 0;
-        sc.threshold = __longlong_as_double(0x7ff0000000000000ULL);  // +inf until set
-      }
+      load_views(net, rk, b, p, rank);
+      sc.singular = 0;
+      sc.done = 0;
+      sc.converged = 0;
+      sc.threshold = __longlong_as_double(0x7ff0000000000000ULL);  // +inf until set
     }
     __syncthreads();
-    const int idx = sc.problem;
-    if (idx >= b.n_problems) break;
-    solve_one<MAXK>(b, cfg, b.order ? b.order[idx] : idx, smem, sc, net);
+    solve_problem<MAXK>(b, cfg, p, rank, smem, sc, net, rk);
+    csync(C);  // no rank reuses its SMEM before every peer is done with it
+  }
+  if (b.phase_cycles && threadIdx.x == 0) {
+    for (int k = 0; k < 8; ++k) b.phase_cycles[8 * blockIdx.x + k] = sc.clk[k];
   }
 }
 
 // One-shot forces for every node of problem blockIdx.x (reference
-// internal_forces, microsolver.py:221-238), same gather code as the solver.
+// internal_forces, microsolver.py:221-238), same element math as the solver.
 __global__ void __launch_bounds__(256) frb_forces_kernel(frb_batch b, const double* __restrict__ u,
                                                           double* __restrict__ f) {
   __shared__ Scalars sc;
   __shared__ Net n;
+  __shared__ Rank rk;
   const int p = blockIdx.x;
   if (threadIdx.x == 0) {
-    load_net(n, b, p);
+    load_views(n, rk, b, p, 0);
     sc.singular = 0;
   }
   __syncthreads();
@@ -885,39 +1029,65 @@ int cuda_check(cudaError_t e, const char* where) {
   return FRB_E_CUDA;
 }
 
+int dofs_cap(int threads) { return threads > 768 ? 8 : threads > 512 ? 12 : 16; }
+
 template <int MAXK, int MAXT>
-int launch_cta(const frb_batch* batch, const frb_config* cfg, int threads, int grid, cudaStream_t s) {
-  const int smem = batch->smem_bytes;
-  auto kern = frb_relax_cta_kernel<MAXK, MAXT>;
-  int rc = cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
-                      "cudaFuncSetAttribute");
+int launch_group(const frb_batch* batch, const frb_config* cfg, const frb_group& g, int32_t* queue,
+                 cudaStream_t s) {
+  auto kern = frb_relax_kernel<MAXK, MAXT>;
+  const int C = g.cluster;
+  int rc = cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, g.smem_bytes),
+                      "cudaFuncSetAttribute(smem)");
   if (rc) return rc;
-  if (grid <= 0) {
-    int dev = 0, nsm = 0, per_sm = 0;
-    rc = cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+  if (C > 8) {
+    rc = cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1),
+                    "cudaFuncSetAttribute(non-portable cluster)");
     if (rc) return rc;
-    rc = cuda_check(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev), "cudaDeviceGetAttribute");
-    if (rc) return rc;
-    rc = cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem),
-                    "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
-    if (rc) return rc;
-    if (per_sm < 1) return set_err(FRB_E_TOO_LARGE, "kernel does not fit on an SM");
-    grid = per_sm * nsm;
   }
-  if (grid > batch->n_problems) grid = batch->n_problems;
-  rc = cuda_check(cudaMemsetAsync(batch->queue, 0, sizeof(int32_t), s), "cudaMemsetAsync");
+  cudaLaunchConfig_t lc = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  lc.blockDim = dim3(g.block_threads);
+  lc.dynamicSmemBytes = g.smem_bytes;
+  lc.stream = s;
+  lc.attrs = attr;
+  lc.numAttrs = 1;
+  int clusters = g.grid_clusters;
+  if (clusters <= 0) {
+    lc.gridDim = dim3(C);
+    rc = cuda_check(cudaOccupancyMaxActiveClusters(&clusters, kern, &lc), "cudaOccupancyMaxActiveClusters");
+    if (rc) return rc;
+    if (clusters < 1) return set_err(FRB_E_TOO_LARGE, "cluster does not fit on the GPU");
+  }
+  if (clusters > g.count) clusters = g.count;
+  lc.gridDim = dim3(clusters * C);
+  rc = cuda_check(cudaMemsetAsync(queue, 0, sizeof(int32_t), s), "cudaMemsetAsync");
   if (rc) return rc;
-  kern<<<grid, threads, smem, s>>>(*batch, *cfg);
-  return cuda_check(cudaGetLastError(), "frb_relax_cta_kernel launch");
+  rc = cuda_check(cudaLaunchKernelEx(&lc, kern, *batch, *cfg, g.first, g.count, queue), "cudaLaunchKernelEx");
+  if (rc) return rc;
+  return cuda_check(cudaGetLastError(), "frb_relax_kernel launch");
 }
 
 template <int MAXT>
-int dispatch_k(const frb_batch* batch, const frb_config* cfg, int threads, int grid, cudaStream_t s, int k) {
-  if (k <= 1) return launch_cta<1, MAXT>(batch, cfg, threads, grid, s);
-  if (k <= 2) return launch_cta<2, MAXT>(batch, cfg, threads, grid, s);
-  if (k <= 4) return launch_cta<4, MAXT>(batch, cfg, threads, grid, s);
-  if (k <= 6) return launch_cta<6, MAXT>(batch, cfg, threads, grid, s);
-  return launch_cta<FRB_MAX_DOFS_PER_THREAD, MAXT>(batch, cfg, threads, grid, s);
+int dispatch_k(const frb_batch* batch, const frb_config* cfg, const frb_group& g, int32_t* queue,
+               cudaStream_t s, int k) {
+  if (k <= 1) return launch_group<1, MAXT>(batch, cfg, g, queue, s);
+  if (k <= 2) return launch_group<2, MAXT>(batch, cfg, g, queue, s);
+  if (k <= 4) return launch_group<4, MAXT>(batch, cfg, g, queue, s);
+  if (k <= 6) return launch_group<6, MAXT>(batch, cfg, g, queue, s);
+  if (k <= 8) return launch_group<8, MAXT>(batch, cfg, g, queue, s);
+  if constexpr (MAXT <= 768) {
+    if (k <= 10) return launch_group<10, MAXT>(batch, cfg, g, queue, s);
+    if (k <= 12) return launch_group<12, MAXT>(batch, cfg, g, queue, s);
+  }
+  if constexpr (MAXT <= 512) {
+    if (k <= 14) return launch_group<14, MAXT>(batch, cfg, g, queue, s);
+    if (k <= 16) return launch_group<16, MAXT>(batch, cfg, g, queue, s);
+  }
+  return set_err(FRB_E_TOO_LARGE, "too many free DOFs per thread for this CTA size");
 }
 
 }  // namespace
@@ -939,23 +1109,23 @@ int frb_device_info(int device, int* n_sm, int* smem_optin, int* cc_major, int* 
   return FRB_OK;
 }
 
-int64_t frb_cta_smem_bytes(int32_t n_free_nodes, int32_t n_ff, int32_t n_leaves) {
-  const int64_t nf = 3 * static_cast<int64_t>(n_free_nodes);
-  const int64_t L = n_leaves;
+int64_t frb_rank_smem_bytes(int32_t n_local, int32_t n_own, int32_t n_act, int32_t n_leaves_total) {
+  const int64_t nf = 3 * static_cast<int64_t>(n_own);
+  const int64_t L = n_leaves_total;
   const int64_t slots = L > 0 ? 2 * L - 1 : 1;
   const int64_t levels = L > 1 ? 64 - __builtin_clzll(static_cast<uint64_t>(L - 1)) + 1 : 0;  // >= tree height
   const int64_t prog_ints = (levels + 1) + 3 * (L > 0 ? L - 1 : 0);
-  return 8 * (3 * nf + (nf > n_ff ? nf : n_ff) + 3 * slots) + 4 * ((prog_ints + 1) & ~1LL);
+  return 8 * (3 * static_cast<int64_t>(n_local) + 2 * nf + (nf > n_act ? nf : n_act) + 3 * slots) +
+         4 * ((prog_ints + 1) & ~1LL);
 }
 
-int frb_solve_batch(const frb_batch* batch, const frb_config* cfg, int block_threads, int grid_ctas,
-                    void* stream) {
+int frb_max_dofs_per_thread(int block_threads) { return dofs_cap(block_threads); }
+
+int frb_solve_batch(const frb_batch* batch, const frb_config* cfg, void* stream) {
   if (!batch || !cfg) return set_err(FRB_E_INVALID, "null batch or config");
-  if (batch->n_problems < 0) return set_err(FRB_E_INVALID, "negative problem count");
+  if (batch->n_problems < 0 || batch->n_groups < 0) return set_err(FRB_E_INVALID, "negative counts");
   if (batch->n_problems == 0) return FRB_OK;
-  if (block_threads < 32 || block_threads > kMaxThreads || block_threads % 32)
-    return set_err(FRB_E_INVALID, "block_threads must be a multiple of 32 in [32, 1024]");
-  if (!batch->work) return set_err(FRB_E_INVALID, "work buffer missing");
+  if (!batch->groups || !batch->queue || !batch->work) return set_err(FRB_E_INVALID, "groups/queue/work missing");
   if (cfg->energy_check_interval > 0) return set_err(FRB_E_UNSUPPORTED, "energy ledger not in this build");
   if (cfg->max_iters <= 0) return set_err(FRB_E_INVALID, "max_iters must be > 0");
   int dev = 0, optin = 0;
@@ -964,17 +1134,23 @@ int frb_solve_batch(const frb_batch* batch, const frb_config* cfg, int block_thr
   rc = cuda_check(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev),
                   "cudaDeviceGetAttribute");
   if (rc) return rc;
-  if (batch->smem_bytes > optin) return set_err(FRB_E_TOO_LARGE, "problem exceeds shared memory per CTA");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  // u, v register arrays sized for the DOFs per thread of the largest problem;
-  // the launch bound (and with it the register budget) follows the CTA size
-  const int per_thread = (batch->max_nf + block_threads - 1) / block_threads;
-  if (per_thread > FRB_MAX_DOFS_PER_THREAD)
-    return set_err(FRB_E_TOO_LARGE, "more than FRB_MAX_DOFS_PER_THREAD free DOFs per thread");
-  if (block_threads <= 256) return dispatch_k<256>(batch, cfg, block_threads, grid_ctas, s, per_thread);
-  if (block_threads <= 512) return dispatch_k<512>(batch, cfg, block_threads, grid_ctas, s, per_thread);
-  if (block_threads <= 768) return dispatch_k<768>(batch, cfg, block_threads, grid_ctas, s, per_thread);
-  return dispatch_k<1024>(batch, cfg, block_threads, grid_ctas, s, per_thread);
+  for (int gi = 0; gi < batch->n_groups; ++gi) {
+    const frb_group& g = batch->groups[gi];
+    if (g.count == 0) continue;
+    if (g.cluster < 1 || g.cluster > FRB_MAX_CLUSTER) return set_err(FRB_E_INVALID, "cluster size out of range");
+    if (g.block_threads < 32 || g.block_threads > kMaxThreads || g.block_threads % 32)
+      return set_err(FRB_E_INVALID, "block_threads must be a multiple of 32 in [32, 1024]");
+    if (g.smem_bytes > optin) return set_err(FRB_E_TOO_LARGE, "a rank exceeds shared memory per CTA");
+    const int k = (g.max_own_dofs + g.block_threads - 1) / g.block_threads;
+    if (k > dofs_cap(g.block_threads)) return set_err(FRB_E_TOO_LARGE, "too many free DOFs per thread");
+    if (g.block_threads <= 256) rc = dispatch_k<256>(batch, cfg, g, batch->queue + gi, s, k);
+    else if (g.block_threads <= 512) rc = dispatch_k<512>(batch, cfg, g, batch->queue + gi, s, k);
+    else if (g.block_threads <= 768) rc = dispatch_k<768>(batch, cfg, g, batch->queue + gi, s, k);
+    else rc = dispatch_k<1024>(batch, cfg, g, batch->queue + gi, s, k);
+    if (rc) return rc;
+  }
+  return FRB_OK;
 }
 
 int frb_selftest_arith(const double* a, const double* b, int n, double* out, void* stream) {

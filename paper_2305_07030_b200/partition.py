@@ -1,0 +1,179 @@
+"""Split one network's free DOFs over the CTAs of a thread-block cluster.
+
+A network that outgrows one SM is solved by a cluster of C CTAs ("ranks")
+exchanging data through distributed shared memory.  The split follows the
+pairwise-sum plan (plan.py): rank r owns a contiguous run of leaves whose DOF
+range [3*node0, 3*(node0 + n_own)) starts at a node boundary, so the
+per-DOF work, the ordered chain sums and the force gather of a node all stay
+on one rank.  Cuts are chosen among leaf starts that are multiples of 3,
+nearest to the even split.
+
+Per rank the kernel works in *local* node numbering:
+    [0, n_own)            own free nodes (global solver ids node0 ...)
+    [n_own, n_local)      halo: free neighbours owned by other ranks
+    n_local + (g - NF)    fixed node g (positions live in global scratch)
+Tables built here (all int32, shared by networks of equal topology):
+    ell_o / ell_c   slot-major incidence of the own nodes (other endpoint in
+                    local numbering, index into the rank's active list)
+    act_ab          active elements (>= 1 own endpoint) in local numbering
+    act_elem        their global element ids (per-network L / EA lookups)
+    halo_g          global solver id of each halo node
+    send            per own node up to two (rank << 24 | local index) targets
+                    that keep it as halo (-1 = none)
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from .plan import PlanView
+
+MAX_SEND = 2
+
+
+@dataclass
+class RankTables:
+    node0: int
+    n_own: int
+    n_local: int
+    leaf0: int
+    n_leaves: int
+    ell_o: np.ndarray        # (SA+SB, stride) int32
+    ell_c: np.ndarray        # (SA+SB, stride) int32
+    act_ab: np.ndarray       # (n_act, 2) int32
+    act_elem: np.ndarray     # (n_act,) int64
+    halo_g: np.ndarray       # (n_local - n_own,) int32
+    send: np.ndarray         # (n_own, MAX_SEND) int32
+
+    @property
+    def stride(self) -> int:
+        return self.ell_o.shape[1]
+
+    @property
+    def n_act(self) -> int:
+        return len(self.act_elem)
+
+
+@dataclass
+class Partition:
+    C: int
+    slots_a: int
+    slots_b: int
+    ranks: list
+
+
+def cut_points(plan: np.ndarray, nf: int, C: int) -> list[int]:
+    """DOF cut offsets (0 = c_0 < ... < c_C = nf) at leaf starts that are
+    multiples of 3; fewer ranks when the plan has too few such starts."""
+    p = PlanView(plan)
+    starts = [int(s) for s in p.leaf_start]
+    cand = sorted({s for s in starts if s % 3 == 0 and 0 < s < nf})
+    cuts = [0]
+    for r in range(1, C):
+        target = nf * r / C
+        best = None
+        for s in cand:
+            if s <= cuts[-1]:
+                continue
+            if best is None or abs(s - target) < abs(best - target):
+                best = s
+        if best is None:
+            break
+        cuts.append(best)
+    cuts.append(nf)
+    return cuts
+
+
+def partition(n_nodes: int, n_free: int, ia: np.ndarray, ib: np.ndarray, ell_other: np.ndarray,
+              ell_elem: np.ndarray, slots_a: int, slots_b: int, plan: np.ndarray, C: int) -> Partition:
+    """Build the per-rank tables of one topology for a cluster of C ranks.
+
+    ia, ib: element endpoints in solver numbering; ell_other / ell_elem: the
+    global slot-major table of the free nodes (batch._topology)."""
+    nf = 3 * n_free
+    p = PlanView(plan)
+    cuts = cut_points(plan, nf, C)
+    C = len(cuts) - 1
+    leaf_start = np.asarray(p.leaf_start, dtype=np.int64)
+    owner = np.full(n_nodes, -1, dtype=np.int64)
+    local = np.full(n_nodes, -1, dtype=np.int64)
+    ranks_nodes = []
+    for r in range(C):
+        n0, n1 = cuts[r] // 3, cuts[r + 1] // 3
+        owner[n0:n1] = r
+        local[n0:n1] = np.arange(n1 - n0)
+        ranks_nodes.append((n0, n1))
+    elem_ids = np.arange(len(ia))
+    ns = slots_a + slots_b
+    ranks = []
+    halo_lists = []
+    for r, (n0, n1) in enumerate(ranks_nodes):
+        n_own = n1 - n0
+        own_a = (ia >= n0) & (ia < n1)
+        own_b = (ib >= n0) & (ib < n1)
+        act = elem_ids[own_a | own_b]
+        ends = np.concatenate([ia[act], ib[act]])
+        halo = np.unique(ends[(ends < n_free) & ((ends < n0) | (ends >= n1))])
+        halo_lists.append(halo)
+        n_local = n_own + len(halo)
+
+        def to_local(g, n0=n0, n1=n1, halo=halo, n_local=n_local, n_own=n_own):
+            g = np.asarray(g, dtype=np.int64)
+            out = np.empty_like(g)
+            own = (g >= n0) & (g < n1)
+            fixed = g >= n_free
+            hal = ~own & ~fixed
+            out[own] = g[own] - n0
+            out[fixed] = n_local + (g[fixed] - n_free)
+            out[hal] = n_own + np.searchsorted(halo, g[hal])
+            return out
+
+        act_index = np.full(len(ia), -1, dtype=np.int64)
+        act_index[act] = np.arange(len(act))
+        stride = max(32, 32 * ((n_own + 31) // 32))
+        ell_o = np.full((ns, stride), -1, dtype=np.int32)
+        ell_c = np.full((ns, stride), -1, dtype=np.int32)
+        if n_own and ns:
+            go = ell_other[:, n0:n1]
+            ge = ell_elem[:, n0:n1]
+            valid = go >= 0
+            lo = np.where(valid, to_local(np.where(valid, go, 0)), -1)
+            ell_o[:, :n_own] = lo
+            ell_c[:, :n_own] = np.where(valid, act_index[ge], -1)
+        act_ab = np.stack([to_local(ia[act]), to_local(ib[act])], axis=1).astype(np.int32)
+        lstarts = np.flatnonzero((leaf_start >= cuts[r]) & (leaf_start < cuts[r + 1]))
+        ranks.append(RankTables(node0=n0, n_own=n_own, n_local=n_local,
+                                leaf0=int(lstarts[0]) if len(lstarts) else 0,
+                                n_leaves=len(lstarts), ell_o=ell_o, ell_c=ell_c, act_ab=act_ab,
+                                act_elem=act.astype(np.int64), halo_g=halo.astype(np.int32),
+                                send=np.full((n_own, MAX_SEND), -1, dtype=np.int32)))
+    # send lists: rank q keeps node g as halo at local index n_own_q + k
+    for q, halo in enumerate(halo_lists):
+        for k, g in enumerate(halo):
+            r = int(owner[g])
+            row = ranks[r].send[g - ranks[r].node0]
+            slot = int(np.flatnonzero(row < 0)[0]) if (row < 0).any() else -1
+            if slot < 0:
+                raise ValueError("node is halo to more than two ranks; use a smaller cluster")
+            row[slot] = (q << 24) | (ranks[q].n_own + k)
+    return Partition(C=C, slots_a=slots_a, slots_b=slots_b, ranks=ranks)
+
+
+def rank_smem_bytes(rt: RankTables, n_leaves_total: int) -> int:
+    """Dynamic SMEM of one rank (mirror of frb_rank_smem_bytes):
+    positions [3][n_local] (a DOF's own position slot doubles as its sq
+    entry between the force and update phases), f, f_prev (8 B per own DOF
+    each), coefficients / sq2 max(own DOFs, n_act), tree slots [2L-1][3] and
+    the tree's int32 combine program."""
+    return smem_bytes(rt.n_local, rt.n_own, rt.n_act, n_leaves_total)
+
+
+def smem_bytes(n_local: int, n_own: int, n_act: int, n_leaves_total: int) -> int:
+    nf = 3 * n_own
+    L = n_leaves_total
+    slots = 2 * L - 1 if L > 0 else 1
+    levels = (L - 1).bit_length() + 1 if L > 1 else 0
+    prog = (levels + 1) + 3 * (L - 1 if L > 0 else 0)
+    return 8 * (3 * n_local + 2 * nf + max(nf, n_act) + 3 * slots) + 4 * ((prog + 1) & ~1)

@@ -21,24 +21,26 @@ def test_library_exports_every_declared_symbol():
     assert set(names) == set(nat.EXPORTS)
     for name in names:
         assert hasattr(lib, name), name
-    assert lib.frb_abi_version() == 1
+    assert lib.frb_abi_version() == nat.ABI_VERSION
 
 
 def test_struct_layouts():
     assert C.sizeof(nat.FrbConfig) == 48
-    assert C.sizeof(nat.FrbBatch) == 16 + 22 * 8
-    assert nat.PROBLEM_DTYPE.itemsize == 200
+    assert C.sizeof(nat.FrbBatch) == 8 + 25 * 8
+    assert nat.PROBLEM_DTYPE.itemsize == 168
+    assert nat.PART_DTYPE.itemsize == 80
+    assert nat.GROUP_DTYPE.itemsize == 32
     assert nat.RESULT_DTYPE.itemsize == 144
 
 
-def test_cta_smem_bytes_matches_host_mirror():
-    from paper_2305_07030_b200.batch import cta_smem_bytes
-    for nfn, nff, L in [(2197, 6084, 64), (150, 360, 4), (0, 0, 0), (1, 0, 1), (63, 400, 2)]:
-        assert nat.lib().frb_cta_smem_bytes(nfn, nff, L) == cta_smem_bytes(nfn, nff, L)
+def test_dofs_per_thread_cap_matches_host():
+    from paper_2305_07030_b200.batch import dofs_per_thread_cap
+    for t in (64, 256, 512, 544, 768, 800, 1024):
+        assert nat.lib().frb_max_dofs_per_thread(t) == dofs_per_thread_cap(t)
 
 
 def test_invalid_arguments_fail_loudly():
     lib = nat.lib()
-    rc = lib.frb_solve_batch(None, None, 128, 0, None)
+    rc = lib.frb_solve_batch(None, None, None)
     assert rc == nat.FRB_E_INVALID
     assert b"null" in lib.frb_last_error()

@@ -1,22 +1,29 @@
 """Host packing invariants (no GPU): incidence order equals the reference's
-bincount summation order, slot tables mirror the CSR, plans and SMEM sizes."""
+bincount summation order, slot tables mirror the CSR, cluster partitions are
+consistent, SMEM mirrors agree with the library."""
 
 import numpy as np
 import pytest
 
-import paper_2305_07030_b200 as frb
-from paper_2305_07030_b200 import batch as fb
-from paper_2305_07030_b200 import _native as nat
 import golden_cases as gc
+import paper_2305_07030_b200 as frb
+from paper_2305_07030_b200 import _native as nat
+from paper_2305_07030_b200 import batch as fb
+from paper_2305_07030_b200.partition import rank_smem_bytes
+from paper_2305_07030_b200.plan import PlanView
 
 
 def _nets():
     yield frb.generate_lattice(5, 6, 7, 0.3, 1)
     yield gc.load("random90_fixed").network
     yield gc.load("lat2_allfixed").network
+    yield frb.generate_lattice(12, 12, 12, 0.3, 2)
 
 
-@pytest.mark.parametrize("net", list(_nets()))
+NETS = list(_nets())
+
+
+@pytest.mark.parametrize("net", NETS)
 def test_csr_is_role_then_element_order(net):
     p = fb.build_problem(net, frb.AffineBC(np.eye(3)))
     t = p.topo
@@ -33,40 +40,109 @@ def test_csr_is_role_then_element_order(net):
         assert list(ent[na:, 1]) == list(eb) and list(ent[na:, 0]) == list(ia[eb])
 
 
-@pytest.mark.parametrize("net", list(_nets()))
+@pytest.mark.parametrize("net", NETS)
 def test_slot_table_mirrors_csr(net):
-    p = fb.build_problem(net, frb.AffineBC(np.eye(3)))
-    t = p.topo
+    t = fb.build_problem(net, frb.AffineBC(np.eye(3))).topo
     for i in range(t.n_free_nodes):
         first, packed = t.inc_node[i]
         na, nb = packed & 0xffff, packed >> 16
         ent = t.inc[first:first + na + nb]
-        a = [o for o in t.ell_other[:t.ell_slots_a, i] if o >= 0]
-        b = [o for o in t.ell_other[t.ell_slots_a:, i] if o >= 0]
+        a = [o for o in t.ell_other[:t.slots_a, i] if o >= 0]
+        b = [o for o in t.ell_other[t.slots_a:, i] if o >= 0]
         assert a == list(ent[:na, 0]) and b == list(ent[na:, 0])
-        # padding only at the end of each role block
-        col = t.ell_other[:t.ell_slots_a, i]
-        assert all(col[k] >= 0 for k in range(na)) and all(col[k] < 0 for k in range(na, t.ell_slots_a))
+        col = t.ell_other[:t.slots_a, i]
+        assert all(col[k] >= 0 for k in range(na)) and all(col[k] < 0 for k in range(na, t.slots_a))
 
 
-def test_pack_offsets_and_dedup():
+@pytest.mark.parametrize("net", NETS)
+@pytest.mark.parametrize("C", [1, 2, 4])
+def test_partition_tables(net, C):
+    t = fb.build_problem(net, frb.AffineBC(np.eye(3))).topo
+    part = t.partition(C)
+    NF = t.n_free_nodes
+    ia, ib = t.elem_ab[:, 0], t.elem_ab[:, 1]
+    starts = PlanView(t.plan).leaf_start
+    nxt = 0
+    leaf = 0
+    for r, rt in enumerate(part.ranks):
+        assert rt.node0 == nxt
+        nxt += rt.n_own
+        assert rt.leaf0 == leaf
+        leaf += rt.n_leaves
+        if rt.n_leaves:
+            assert starts[rt.leaf0] == 3 * rt.node0   # leaf-aligned, node-aligned cut
+        own = set(range(rt.node0, rt.node0 + rt.n_own))
+        halo = list(rt.halo_g)
+
+        def glob(l):
+            if l < rt.n_own:
+                return rt.node0 + l
+            if l < rt.n_local:
+                return halo[l - rt.n_own]
+            return NF + (l - rt.n_local)
+
+        act = set(np.flatnonzero(np.isin(ia, list(own)) | np.isin(ib, list(own))))
+        assert set(rt.act_elem) == act
+        for e, (a, b) in zip(rt.act_elem, rt.act_ab):
+            assert (glob(a), glob(b)) == (ia[e], ib[e])
+        for i in range(rt.n_own):
+            for k in range(part.slots_a + part.slots_b):
+                o, c = rt.ell_o[k, i], rt.ell_c[k, i]
+                go = t.ell_other[k, rt.node0 + i]
+                assert (o < 0) == (go < 0)
+                if o >= 0:
+                    assert glob(o) == go
+                    assert rt.act_elem[c] == t.ell_elem[k, rt.node0 + i]
+        # every halo node is sent here by its owner at the right local index
+        for k, g in enumerate(halo):
+            owner = next(q for q in part.ranks if q.node0 <= g < q.node0 + q.n_own)
+            q = part.ranks.index(owner)
+            targets = [s for s in owner.send[g - owner.node0] if s >= 0]
+            assert (r << 24 | (rt.n_own + k)) in targets and q != r
+    assert nxt == NF and leaf == t.n_leaves
+
+
+def test_rank_smem_mirror_matches_library():
+    for n_local, n_own, n_act, L in [(3375, 2197, 7098, 64), (1300, 1099, 3600, 64), (150, 150, 400, 4),
+                                     (0, 0, 0, 0), (1, 1, 0, 1), (63, 63, 400, 2)]:
+        from paper_2305_07030_b200.partition import smem_bytes
+        assert nat.lib().frb_rank_smem_bytes(n_local, n_own, n_act, L) == smem_bytes(n_local, n_own, n_act, L)
+
+
+def test_c2_networks_use_two_ranks_and_fit():
+    t = fb.build_problem(frb.generate_lattice(15, 15, 15, 0.3, 0), frb.AffineBC(np.eye(3))).topo
+    part = t.choose_cluster()
+    assert part.C == 2
+    assert max(rank_smem_bytes(r, t.n_leaves) for r in part.ranks) <= fb.SMEM_BUDGET
+
+
+def test_pack_offsets_groups_and_dedup():
     nets = [frb.generate_lattice(6, 6, 6, 0.3, s) for s in range(4)] + [frb.generate_lattice(5, 5, 5, 0.3, 0)]
     b = frb.pack_batch(nets, [frb.AffineBC(np.eye(3))] * 5)
     assert list(b.node_base) == [0, 216, 432, 648, 864, 989]
-    # equal topologies share one incidence table
-    assert len({int(d["inc_base"]) for d in b.desc[:4]}) == 1
+    assert len({int(d["inc_base"]) for d in b.desc[:4]}) == 1      # shared topology tables
     assert b.arrays["inc"].shape[0] == 2 * (540 + 300)
-    assert b.smem_bytes == max(fb.cta_smem_bytes(p.n_free_nodes, len(p.topo.ff_elem), p.topo.n_leaves)
-                               for p in b.problems)
-    assert "ell_EA" not in b.arrays        # uniform EA -> scalar per problem
+    assert "act_EA" not in b.arrays                                  # uniform EA -> scalar
     assert all(d["flags"] & nat.PF_EA_UNIFORM for d in b.desc)
-    assert b.desc.dtype.itemsize == 200
+    assert len(b.groups) == 1 and b.groups[0]["cluster"] == 1 and b.groups[0]["count"] == 5
+    assert sorted(b.arrays["order"].tolist()) == list(range(5))
+    assert b.arrays["order"][-1] == 4                                # largest first
+    g = b.groups[0]
+    assert g["smem_bytes"] == max(rank_smem_bytes(r, p.topo.n_leaves)
+                                  for p in b.problems for r in p.topo.partition(1).ranks)
 
 
-def test_mixed_materials_carry_slot_ea():
+def test_mixed_sizes_form_cluster_groups():
+    nets = [frb.generate_lattice(15, 15, 15, 0.3, 0), frb.generate_lattice(6, 6, 6, 0.3, 0)]
+    b = frb.pack_batch(nets, [frb.AffineBC(np.eye(3))] * 2)
+    assert [int(g["cluster"]) for g in b.groups] == [1, 2]
+    assert [int(d["cluster"]) for d in b.desc] == [2, 1]
+
+
+def test_mixed_materials_carry_element_ea():
     net = gc.load("random90_fixed").network
     b = frb.pack_batch([net], [frb.AffineBC(np.eye(3))])
-    assert "ell_EA" in b.arrays and not (b.desc[0]["flags"] & nat.PF_EA_UNIFORM)
+    assert "act_EA" in b.arrays and not (b.desc[0]["flags"] & nat.PF_EA_UNIFORM)
 
 
 def test_pack_length_mismatch():
@@ -85,19 +161,3 @@ def test_isolated_node_is_mass_error():
                            [frb.Material(1, 1, 1)], frozenset({0}))
     with pytest.raises(frb.NetworkMassError):
         frb.pack_batch([net], [frb.AffineBC(np.eye(3))])
-
-
-@pytest.mark.parametrize("net", list(_nets()))
-def test_free_free_coefficient_slots(net):
-    p = fb.build_problem(net, frb.AffineBC(np.eye(3)))
-    t = p.topo
-    nfn = t.n_free_nodes
-    for k in range(t.ell_slots_a + t.ell_slots_b):
-        for i in range(nfn):
-            o, c = t.ell_other[k, i], t.ell_c[k, i]
-            if o < 0 or o >= nfn:
-                assert c == -1
-            else:
-                a, b = t.ff_ab[c]
-                assert {int(a), int(b)} == {i, int(o)}
-                assert t.ff_elem[c] == t.ell_elem[k, i]
