@@ -15,7 +15,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "lib", "libfrb200.so")
 
-ABI_VERSION = 2
+ABI_VERSION = 3
 MAX_CLUSTER = 16
 FRB_OK, FRB_E_INVALID, FRB_E_TOO_LARGE, FRB_E_CUDA, FRB_E_UNSUPPORTED = 0, -1, -2, -3, -4
 STATUS_CONVERGED, STATUS_MAX_ITERS, STATUS_SINGULAR = 0, 1, 2
@@ -33,9 +33,9 @@ class FrbConfig(C.Structure):
                 ("energy_check_interval", C.c_int32), ("bc_ramp_iters", C.c_int32)]
 
 
-BATCH_POINTERS = ("groups", "problems", "parts", "order", "X", "node_mass", "inc_node", "inc",
-                  "elem_ab", "elem_L", "elem_EA", "plans", "ell_o", "ell_c", "act_ab", "act_L",
-                  "act_EA", "halo_g", "send", "u", "f", "work", "results", "queue",
+BATCH_POINTERS = ("groups", "problems", "parts", "order", "X", "dof_mass", "inc_node", "inc",
+                  "elem_ab", "elem_L", "elem_EA", "plans", "ell", "act_ab", "act_L",
+                  "act_EA", "halo_g", "send", "fix_g", "u", "f", "work", "results", "queue",
                   "phase_cycles")
 
 
@@ -54,10 +54,10 @@ PROBLEM_DTYPE = np.dtype([
 ])
 PART_DTYPE = np.dtype([
     ("ell_base", "<i8"), ("act_base", "<i8"), ("actv_off", "<i8"), ("halo_base", "<i8"),
-    ("send_base", "<i8"),
+    ("send_base", "<i8"), ("fix_base", "<i8"),
     ("node0", "<i4"), ("n_own", "<i4"), ("n_local", "<i4"), ("n_act", "<i4"),
     ("ell_stride", "<i4"), ("slots_a", "<i4"), ("slots_b", "<i4"), ("leaf0", "<i4"),
-    ("n_leaves", "<i4"), ("pad", "<i4"),
+    ("n_leaves", "<i4"), ("n_fix", "<i4"),
 ])
 GROUP_DTYPE = np.dtype([
     ("cluster", "<i4"), ("first", "<i4"), ("count", "<i4"), ("block_threads", "<i4"),
@@ -68,7 +68,7 @@ RESULT_DTYPE = np.dtype([
     ("final_residual", "<f8"), ("r_ref", "<f8"), ("energy_residual", "<f8"),
     ("avg_stress", "<f8", (9,)), ("energy", "<f8", (4,)),
 ])
-assert PROBLEM_DTYPE.itemsize == 168 and PART_DTYPE.itemsize == 80
+assert PROBLEM_DTYPE.itemsize == 168 and PART_DTYPE.itemsize == 88
 assert GROUP_DTYPE.itemsize == 32 and RESULT_DTYPE.itemsize == 144
 
 

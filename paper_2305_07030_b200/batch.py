@@ -309,8 +309,8 @@ def _pack(networks, bcs, probs, cluster: int | None = None) -> Batch:
     plan_slot: dict[int, int] = {}
     shared_slot: dict[tuple, list] = {}       # (topo, C) -> per-rank base offsets
     topo_slot: dict[bytes, int] = {}
-    inc, plans, ell_o, ell_c, act_ab, halo_g, send = [], [], [], [], [], [], []
-    n_inc = n_plan = n_ell = n_act = n_halo = n_send = 0
+    inc, plans, ell, act_ab, halo_g, send, fix_g = [], [], [], [], [], [], []
+    n_inc = n_plan = n_ell = n_act = n_halo = n_send = n_fix = 0
     X, mass, EL, EA, inc_node, elem_ab, act_L, act_EA = [], [], [], [], [], [], [], []
     parts_rows = []
     elem_base = actv_base = 0
@@ -328,16 +328,17 @@ def _pack(networks, bcs, probs, cluster: int | None = None) -> Batch:
         if key not in shared_slot:
             bases = []
             for rt in part.ranks:
-                bases.append((n_ell, n_act, n_halo, n_send))
-                ell_o.append(rt.ell_o.reshape(-1))
-                ell_c.append(rt.ell_c.reshape(-1))
+                bases.append((n_ell, n_act, n_halo, n_send, n_fix))
+                ell.append(rt.ell.reshape(-1))
                 act_ab.append(rt.act_ab)
                 halo_g.append(rt.halo_g)
                 send.append(rt.send)
+                fix_g.append(rt.fix_g)
                 n_ell += rt.ell_o.size
                 n_act += len(rt.act_ab)
                 n_halo += len(rt.halo_g)
                 n_send += len(rt.send)
+                n_fix += rt.n_fix
             shared_slot[key] = bases
         nf = 3 * t.n_free_nodes
         if nf not in plan_slot:
@@ -365,10 +366,11 @@ def _pack(networks, bcs, probs, cluster: int | None = None) -> Batch:
         d["ea"] = ea[0] if ea.size else 0.0
         d["F"] = p.F.reshape(9)
         off = 0
-        for rt, (b_ell, b_act, b_halo, b_send) in zip(part.ranks, shared_slot[key]):
+        for rt, (b_ell, b_act, b_halo, b_send, b_fix) in zip(part.ranks, shared_slot[key]):
             row = np.zeros((), dtype=nat.PART_DTYPE)
             row["ell_base"], row["act_base"], row["actv_off"] = b_ell, b_act, off
-            row["halo_base"], row["send_base"] = b_halo, b_send
+            row["halo_base"], row["send_base"], row["fix_base"] = b_halo, b_send, b_fix
+            row["n_fix"] = rt.n_fix
             row["node0"], row["n_own"], row["n_local"], row["n_act"] = rt.node0, rt.n_own, rt.n_local, rt.n_act
             row["ell_stride"], row["slots_a"], row["slots_b"] = rt.stride, part.slots_a, part.slots_b
             row["leaf0"], row["n_leaves"] = rt.leaf0, rt.n_leaves
@@ -379,7 +381,7 @@ def _pack(networks, bcs, probs, cluster: int | None = None) -> Batch:
         actv_base += off
         node_base[i + 1] = node_base[i] + p.n_nodes
         X.append(p.X.reshape(-1))
-        mass.append(p.node_mass)
+        mass.append(np.repeat(p.node_mass, 3))
         EL.append(L)
         EA.append(ea)
         inc_node.append(t.inc_node)
@@ -402,11 +404,11 @@ def _pack(networks, bcs, probs, cluster: int | None = None) -> Batch:
         groups.append(g)
         order.extend(ids)
     arrays = dict(
-        X=_cat(X, np.float64), node_mass=_cat(mass, np.float64),
+        X=_cat(X, np.float64), dof_mass=_cat(mass, np.float64),
         inc_node=_cat(inc_node, np.int32, 2), inc=_cat(inc, np.int32, 2),
         elem_ab=_cat(elem_ab, np.int32, 2), elem_L=_cat(EL, np.float64),
         elem_EA=_cat(EA, np.float64), plans=_cat(plans, np.int32),
-        ell_o=_cat(ell_o, np.int32), ell_c=_cat(ell_c, np.int32),
+        ell=_cat(ell, np.uint32).view(np.int32), fix_g=_cat(fix_g, np.int32),
         act_ab=_cat(act_ab, np.int32, 2), act_L=_cat(act_L, np.float64),
         halo_g=_cat(halo_g, np.int32), send=_cat(send, np.int32, MAX_SEND),
         order=np.asarray(order, dtype=np.int32),
@@ -497,8 +499,8 @@ class DeviceBatch:
         fb.n_groups = len(groups)
         fb.groups = groups_c.ctypes.data
         t = self.t
-        for k in ("parts", "order", "X", "node_mass", "inc_node", "inc", "elem_ab", "elem_L", "elem_EA",
-                  "plans", "ell_o", "ell_c", "act_ab", "act_L", "act_EA", "halo_g", "send"):
+        for k in ("parts", "order", "X", "dof_mass", "inc_node", "inc", "elem_ab", "elem_L", "elem_EA",
+                  "plans", "ell", "act_ab", "act_L", "act_EA", "halo_g", "send", "fix_g"):
             setattr(fb, k, t[k].data_ptr() if k in t and t[k].numel() else None)
         fb.problems = desc_t.data_ptr()
         fb.u, fb.f, fb.work = u.data_ptr(), f.data_ptr(), work.data_ptr()

@@ -4,11 +4,9 @@
 // pulled from a device work queue (the spec's TeamBatched strategy,
 // SPEC.md:361; the paper's "one team per sub-problem" kernel,
 // PAPER.md:76-82).  C = 1 for networks that fit one SM; larger networks are
-// split over the cluster by node range and exchange halo positions and
-// pairwise-leaf sums through distributed shared memory (DSMEM).  The whole
-// Fig.-1 loop of the reference (_relax, pkg/src/fibrelax/microsolver.py:
-// 379-530) runs inside the kernel; finalize_result (:549-564) runs in its
-// epilogue.
+// split over the cluster by node range.  The whole Fig.-1 loop of the
+// reference (_relax, pkg/src/fibrelax/microsolver.py:379-530) runs inside the
+// kernel; finalize_result (:549-564) runs in its epilogue.
 //
 // Bit-exactness contract.  Every FP64 operation is an
 // explicit round-to-nearest operation (intrinsics, or the branch-free fast
@@ -33,18 +31,31 @@
 //   C  chains  per (own leaf, chain): ordered sums -> all ranks' tree slots
 //   T  tree    warp 0: pairwise combine, c, residual, convergence
 //   U  per DOF a = -f/m - c v, two half kicks, drift, positions (+ halo push)
-// Cluster barriers follow C (leaf sums) and U (halo positions).
+//
+// Cluster exchange (C > 1).  Halo positions (U -> next F) and leaf sums
+// (C -> T) travel as st.async stores into the peers' shared memory, each
+// completing a transaction on the receiver's mbarrier; a rank waits on its
+// own mbarriers only.  There is no cluster-wide barrier inside the loop: a
+// cluster barrier's acquire invalidates L1 (CCTL.IVALL), which evicted the
+// read-only tables the loop streams through L1 (profiles/r01_v4_ncu_c2.md).
+// Each rank posts the byte count it expects for a phase (arrive.expect_tx)
+// before any peer can send into that phase: the next halo phase is posted in
+// A (peers send halos only after receiving this rank's leaf sums of C), the
+// next leaf-sum phase right after the current one completes (peers send leaf
+// sums only after this rank's halo push of U).  When a problem ends, the two
+// phases posted for an iteration that will not happen are completed locally
+// (mbarrier.complete_tx) so the barriers are idle for the next problem.
 //
 // Shared memory per rank (offsets identical on every rank of a problem so a
 // peer's buffer is addressed by the same offset):
-//   pos  [3][PS]  positions of own + halo nodes (SoA).  An own DOF's slot
-//                 holds its sq between F and U.
+//   pos  [PN][3]  positions (AoS) of own, halo and fixed local nodes; an own
+//                 DOF's slot holds its sq between A and U.
 //   fcur [NFO]    f from F2; after A it holds ff
 //   fprv [NFO]    f of the previous iteration; after A the current f
 //   cf   [CF]     F1 element coefficients, then sq2
-//   slot [2L-1][3] pairwise-tree slots;  prog: the tree's combine program
-// u and v of a thread's own DOFs live in registers; fixed-node positions
-// (constant unless the BC ramps) live in global scratch, read through L1.
+//   slot [2L-1][3] pairwise-tree slots;  flag[16]: peers' singular flags
+//   prog          the tree's combine program
+// u and v of a thread's own DOFs live in registers.
 
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
@@ -63,6 +74,7 @@ namespace {
 constexpr int kMaxThreads = 1024;
 constexpr int kMaxWarps = kMaxThreads / 32;
 constexpr double kCollapse = 1e-12;  // microsolver.py:30
+constexpr uint32_t kEllPad = 0xFFFFFFFFu;
 
 __device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
@@ -77,6 +89,56 @@ __device__ __forceinline__ double len2(double dx, double dy, double dz) {
 }
 __device__ __forceinline__ double seg_len(double dx, double dy, double dz) { return dsqrt(len2(dx, dy, dz)); }
 
+// ------------------------------------------------------------------ cluster primitives
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+// shared::cluster address of the same variable in CTA `rank`
+__device__ __forceinline__ uint32_t mapa(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+// 8-byte store into a peer's shared memory, completing 8 transaction bytes
+// on the peer's mbarrier
+__device__ __forceinline__ void st_async(uint32_t addr, double v, uint32_t bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];"
+               :
+               : "r"(addr), "l"(__double_as_longlong(v)), "r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" : : "r"(smem_u32(bar)), "r"(count) : "memory");
+}
+// this CTA's arrival for the current phase + the bytes the phase waits for
+__device__ __forceinline__ void mbar_expect(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+               :
+               : "r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+// complete `bytes` of the current phase locally (no data will arrive)
+__device__ __forceinline__ void mbar_complete(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.complete_tx.shared::cluster.relaxed.cluster.b64 [%0], %1;"
+               :
+               : "r"(mapa(smem_u32(bar), cg::this_cluster().block_rank())), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  uint32_t done;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.b32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(a), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+
 // ------------------------------------------------------------------ problem views
 
 struct Net {
@@ -85,28 +147,29 @@ struct Net {
   double dt, hdt, volume, ea;
   double g[9];  // F - I
   const double* X;
-  const double* mass;
+  const double* mass3;  // per DOF
   const int2* incn;
   const int2* inc;
   const int2* eab;
   const double* EL;
   const double* EA;
   const int* plan;
-  double* posg;  // [N][3] positions scratch (fixed nodes always; free at the end)
+  double* posg;  // [N][3] positions scratch (init checks, singular path, epilogue)
   int64_t node_base;
 };
 
 struct Rank {
-  int node0, n_own, n_local, n_act;
+  int node0, n_own, n_local, n_fix, n_act;
   int S, SA, SB, leaf0, n_leaves;
-  int PS, NFO, CF;  // uniform SMEM strides of the problem (max over ranks)
-  const int* ell_o;
-  const int* ell_c;
+  int PN, NFO, CF;  // uniform SMEM extents of the problem (max over ranks)
+  uint32_t halo_bytes, leaf_bytes;  // transaction bytes this rank receives per phase
+  const uint32_t* ell;
   const int2* act_ab;
   const double* act_L;
   const double* act_EA;
   const int* halo_g;
   const int2* send;
+  const int* fix_g;
 };
 
 __device__ void load_views(Net& n, Rank& R, const frb_batch& b, int p, int r) {
@@ -124,7 +187,7 @@ __device__ void load_views(Net& n, Rank& R, const frb_batch& b, int p, int r) {
     for (int c = 0; c < 3; ++c) n.g[3 * i + c] = dsub(P.F[3 * i + c], i == c ? 1.0 : 0.0);
   n.node_base = P.node_base;
   n.X = b.X + 3 * P.node_base;
-  n.mass = b.node_mass + P.node_base;
+  n.mass3 = b.dof_mass + 3 * P.node_base;
   n.incn = reinterpret_cast<const int2*>(b.inc_node) + P.node_base;
   n.inc = reinterpret_cast<const int2*>(b.inc) + P.inc_base;
   n.eab = reinterpret_cast<const int2*>(b.elem_ab) + P.elem_base;
@@ -139,28 +202,31 @@ __device__ void load_views(Net& n, Rank& R, const frb_batch& b, int p, int r) {
   R.node0 = Q.node0;
   R.n_own = Q.n_own;
   R.n_local = Q.n_local;
+  R.n_fix = Q.n_fix;
   R.n_act = Q.n_act;
   R.S = Q.ell_stride;
   R.SA = Q.slots_a;
   R.SB = Q.slots_b;
   R.leaf0 = Q.leaf0;
   R.n_leaves = Q.n_leaves;
-  // uniform strides: maxima over the problem's ranks
-  R.PS = R.NFO = R.CF = 0;
+  R.halo_bytes = 24u * static_cast<uint32_t>(Q.n_local - Q.n_own);
+  R.leaf_bytes = 24u * static_cast<uint32_t>(n.L - Q.n_leaves) + 8u * static_cast<uint32_t>(n.C - 1);
+  // uniform extents: maxima over the problem's ranks
+  R.PN = R.NFO = R.CF = 0;
   for (int q = 0; q < n.C; ++q) {
     const frb_part& Qq = b.parts[P.part_base + q];
-    R.PS = max(R.PS, Qq.n_local);
+    R.PN = max(R.PN, Qq.n_local + Qq.n_fix);
     R.NFO = max(R.NFO, 3 * Qq.n_own);
     R.CF = max(R.CF, Qq.n_act);
   }
   R.CF = max(R.CF, R.NFO);
-  R.ell_o = b.ell_o + Q.ell_base;
-  R.ell_c = b.ell_c + Q.ell_base;
+  R.ell = b.ell + Q.ell_base;
   R.act_ab = reinterpret_cast<const int2*>(b.act_ab) + Q.act_base;
   R.act_L = b.act_L + P.actv_base + Q.actv_off;
   R.act_EA = (b.act_EA && !n.ea_uniform) ? b.act_EA + P.actv_base + Q.actv_off : nullptr;
   R.halo_g = b.halo_g + Q.halo_base;
   R.send = reinterpret_cast<const int2*>(b.send) + Q.send_base;
+  R.fix_g = b.fix_g + Q.fix_base;
 }
 
 // u_presc[i][j] = x @ (F-I)^T as OpenBLAS evaluates it (microsolver.py:320-322):
@@ -182,16 +248,6 @@ __device__ __forceinline__ double fixed_u(const Net& n, int node, int j, double 
 
 // ------------------------------------------------------------------ positions
 
-// Rank-local numbering: own + halo nodes in SMEM (SoA, stride PS), fixed
-// nodes from the global scratch (AoS by solver id).
-struct PosRank {
-  const double* p;
-  const double* posg;
-  int PS, n_local, NF;
-  __device__ __forceinline__ double operator()(int node, int axis) const {
-    return node < n_local ? p[axis * PS + node] : posg[3 * (NF + node - n_local) + axis];
-  }
-};
 // Solver numbering, all positions from global memory.
 struct PosGlobalAll {
   const double* posg;
@@ -203,6 +259,15 @@ struct PosGlobal {
   const double* u;
   __device__ __forceinline__ double operator()(int node, int axis) const {
     return dadd(X[3 * node + axis], u[3 * node + axis]);
+  }
+};
+// Fixed nodes only: X + fixed_u(alpha), evaluated on the fly.
+struct PosFixed {
+  const Net* n;
+  double alpha;
+  bool ramp;
+  __device__ __forceinline__ double operator()(int node, int axis) const {
+    return dadd(n->X[3 * node + axis], fixed_u(*n, node, axis, alpha, ramp));
   }
 };
 
@@ -254,8 +319,8 @@ __device__ __forceinline__ bool element_force(double dx, double dy, double dz, d
 // Internal force at node i from the CSR incidence lists (all nodes, solver
 // numbering; used by the epilogue, the singular path and internal_forces).
 template <class Pos>
-__device__ __noinline__ bool node_force_csr(const Net& n, const Pos& pos, int i, double& fx,
-                                               double& fy, double& fz) {
+__device__ __noinline__ bool node_force_csr(const Net& n, const Pos& pos, int i, double& fx, double& fy,
+                                            double& fz) {
   const int2 meta = n.incn[i];
   const int first = meta.x;
   const int na = meta.y & 0xffff;
@@ -288,18 +353,20 @@ __device__ __noinline__ bool node_force_csr(const Net& n, const Pos& pos, int i,
 // Phase F1: coefficient EA (l - L) / (L l) of every active element of the
 // rank, once per iteration (microsolver.py:196-211).  Elements cut by a rank
 // boundary are evaluated by both ranks from identical operands.
-__device__ __forceinline__ void act_one(const Rank& R, double ea, const PosRank& P, int e, int2 ab, double L,
-                                        double* __restrict__ cf, bool& bad) {
+__device__ __forceinline__ void act_one(const Rank& R, double ea, const double* __restrict__ pos, int e, int2 ab,
+                                        double L, double* __restrict__ cf, bool& bad) {
   const double EA = R.act_EA ? __ldg(R.act_EA + e) : ea;
-  const double dx = dsub(P(ab.y, 0), P(ab.x, 0));
-  const double dy = dsub(P(ab.y, 1), P(ab.x, 1));
-  const double dz = dsub(P(ab.y, 2), P(ab.x, 2));
+  const double* pa = pos + 3 * ab.x;
+  const double* pb = pos + 3 * ab.y;
+  const double dx = dsub(pb[0], pa[0]);
+  const double dy = dsub(pb[1], pa[1]);
+  const double dz = dsub(pb[2], pa[2]);
   const LenCoef lc = len_coef(dx, dy, dz, L, EA);
   bad |= lc.l < dmul(kCollapse, L);
   cf[e] = lc.coef;
 }
 
-__device__ __forceinline__ bool element_coefs(const Rank& R, double ea, const PosRank& P,
+__device__ __forceinline__ bool element_coefs(const Rank& R, double ea, const double* __restrict__ pos,
                                               double* __restrict__ cf) {
   bool bad = false;
   const int T = blockDim.x;
@@ -307,10 +374,10 @@ __device__ __forceinline__ bool element_coefs(const Rank& R, double ea, const Po
   for (; e + T < R.n_act; e += 2 * T) {  // two elements per step: their loads overlap
     const int2 ab0 = __ldg(R.act_ab + e), ab1 = __ldg(R.act_ab + e + T);
     const double L0 = __ldg(R.act_L + e), L1 = __ldg(R.act_L + e + T);
-    act_one(R, ea, P, e, ab0, L0, cf, bad);
-    act_one(R, ea, P, e + T, ab1, L1, cf, bad);
+    act_one(R, ea, pos, e, ab0, L0, cf, bad);
+    act_one(R, ea, pos, e + T, ab1, L1, cf, bad);
   }
-  if (e < R.n_act) act_one(R, ea, P, e, __ldg(R.act_ab + e), __ldg(R.act_L + e), cf, bad);
+  if (e < R.n_act) act_one(R, ea, pos, e, __ldg(R.act_ab + e), __ldg(R.act_L + e), cf, bad);
   return bad;
 }
 
@@ -319,43 +386,43 @@ __device__ __forceinline__ bool element_coefs(const Rank& R, double ea, const Po
 // 0 + nd + nd ...  nd = d * coef with d = P[b] - P[a] recomputed from the
 // operands F1 used, so it is bitwise the reference's per-element value.
 // Padding slots are skipped (exact: the reference adds nothing there).  The
-// slot table of a chunk is loaded up front so its latencies overlap.
-constexpr int kSlots = 6;
+// slot words of a group are loaded up front so their latencies overlap.
+constexpr int kSlots = 4;
 
-__device__ __forceinline__ void node_force_ell(const Rank& R, const double* __restrict__ cf, const PosRank& P,
-                                               int i, double& fx, double& fy, double& fz) {
-  const double px = P(i, 0), py = P(i, 1), pz = P(i, 2);
-  double ax = 0.0, ay = 0.0, az = 0.0, bx = 0.0, by = 0.0, bz = 0.0;
-  const int ns = R.SA + R.SB;
-  for (int k0 = 0; k0 < ns; k0 += kSlots) {
-    int o[kSlots], c[kSlots];
+template <bool kRoleA>
+__device__ __forceinline__ void gather_role(const Rank& R, const double* __restrict__ cf,
+                                            const double* __restrict__ pos, int i, int k_begin, int k_end,
+                                            double px, double py, double pz, double& sx, double& sy,
+                                            double& sz) {
+  for (int k0 = k_begin; k0 < k_end; k0 += kSlots) {
+    uint32_t w[kSlots];
+#pragma unroll
+    for (int q = 0; q < kSlots; ++q) w[q] = k0 + q < k_end ? __ldg(R.ell + (k0 + q) * R.S + i) : kEllPad;
 #pragma unroll
     for (int q = 0; q < kSlots; ++q) {
-      const int k = k0 + q;
-      o[q] = k < ns ? __ldg(R.ell_o + k * R.S + i) : -1;
-      c[q] = k < ns ? __ldg(R.ell_c + k * R.S + i) : 0;
-    }
-#pragma unroll
-    for (int q = 0; q < kSlots; ++q) {
-      if (o[q] < 0) continue;
-      const bool role_a = k0 + q < R.SA;
-      const double ox = P(o[q], 0), oy = P(o[q], 1), oz = P(o[q], 2);
-      const double coef = cf[c[q]];
-      const double dx = role_a ? dsub(ox, px) : dsub(px, ox);
-      const double dy = role_a ? dsub(oy, py) : dsub(py, oy);
-      const double dz = role_a ? dsub(oz, pz) : dsub(pz, oz);
-      const double nx = dmul(dx, coef), ny = dmul(dy, coef), nz = dmul(dz, coef);
-      if (role_a) {  // bincount(ia, -nd): 0 + (-nd) + ...
-        ax = dsub(ax, nx);
-        ay = dsub(ay, ny);
-        az = dsub(az, nz);
-      } else {  // bincount(ib, nd)
-        bx = dadd(bx, nx);
-        by = dadd(by, ny);
-        bz = dadd(bz, nz);
+      if (w[q] == kEllPad) continue;
+      const double* po = pos + 3 * (w[q] >> 16);
+      const double coef = cf[w[q] & 0xffffu];
+      if (kRoleA) {  // bincount(ia, -nd): 0 + (-nd) + ...,  d = P[o] - P[i]
+        sx = dsub(sx, dmul(dsub(po[0], px), coef));
+        sy = dsub(sy, dmul(dsub(po[1], py), coef));
+        sz = dsub(sz, dmul(dsub(po[2], pz), coef));
+      } else {  // bincount(ib, nd),  d = P[i] - P[o]
+        sx = dadd(sx, dmul(dsub(px, po[0]), coef));
+        sy = dadd(sy, dmul(dsub(py, po[1]), coef));
+        sz = dadd(sz, dmul(dsub(pz, po[2]), coef));
       }
     }
   }
+}
+
+__device__ __forceinline__ void node_force_ell(const Rank& R, const double* __restrict__ cf,
+                                               const double* __restrict__ pos, int i, double& fx, double& fy,
+                                               double& fz) {
+  const double px = pos[3 * i], py = pos[3 * i + 1], pz = pos[3 * i + 2];
+  double ax = 0.0, ay = 0.0, az = 0.0, bx = 0.0, by = 0.0, bz = 0.0;
+  gather_role<true>(R, cf, pos, i, 0, R.SA, px, py, pz, ax, ay, az);
+  gather_role<false>(R, cf, pos, i, R.SA, R.SA + R.SB, px, py, pz, bx, by, bz);
   fx = dadd(ax, bx);
   fy = dadd(ay, by);
   fz = dadd(az, bz);
@@ -370,6 +437,9 @@ struct Scalars {
   double red[kMaxWarps * 9];
   int ired[kMaxWarps];
   int problem, done, converged, singular;
+  uint32_t peer_smem[FRB_MAX_CLUSTER];  // shared::cluster base of each rank's dynamic SMEM
+  uint32_t peer_bar_h[FRB_MAX_CLUSTER]; // each rank's halo mbarrier
+  uint32_t peer_bar_s[FRB_MAX_CLUSTER]; // each rank's leaf-sum mbarrier
 };
 
 // Phase timing: thread 0 charges the cycles since the previous mark to
@@ -463,9 +533,9 @@ __device__ __noinline__ int singular_argmin(const Net& n, const Pos& pos, Scalar
 
 // Length check of elements whose endpoints are both fixed (their only motion
 // is the BC ramp; every other element is checked in F1).  With all_elements,
-// every element is checked (init, positions from posg).  Sets sc.singular.
+// every element is checked.
 template <class Pos>
-__device__ __noinline__ void check_elements(const Net& n, const Pos& pos, Scalars& sc, bool all_elements) {
+__device__ __noinline__ bool check_elements(const Net& n, const Pos& pos, bool all_elements) {
   bool bad = false;
   for (int e = threadIdx.x; e < n.M; e += blockDim.x) {
     const int2 ab = n.eab[e];
@@ -475,13 +545,22 @@ __device__ __noinline__ void check_elements(const Net& n, const Pos& pos, Scalar
     const double dz = dsub(pos(ab.y, 2), pos(ab.x, 2));
     bad |= seg_len(dx, dy, dz) < dmul(kCollapse, n.EL[e]);
   }
-  if (bad) sc.singular = 1;
+  return bad;
 }
 
 // Fixed-node positions into global scratch, split over the cluster's ranks.
 __device__ __noinline__ void set_fixed_positions(const Net& n, int rank, double alpha, bool ramp) {
   for (int i = n.NF + rank * blockDim.x + threadIdx.x; i < n.N; i += n.C * blockDim.x)
     for (int j = 0; j < 3; ++j) n.posg[3 * i + j] = dadd(n.X[3 * i + j], fixed_u(n, i, j, alpha, ramp));
+}
+
+// Fixed-node positions of the rank's local copies (SMEM).
+__device__ __forceinline__ void set_local_fixed(const Net& n, const Rank& R, double* pos, double alpha, bool ramp) {
+  for (int k = threadIdx.x; k < R.n_fix; k += blockDim.x) {
+    const int g = __ldg(R.fix_g + k);
+    double* p = pos + 3 * (R.n_local + k);
+    for (int j = 0; j < 3; ++j) p[j] = dadd(n.X[3 * g + j], fixed_u(n, g, j, alpha, ramp));
+  }
 }
 
 __device__ __forceinline__ double ramp_alpha(int it_plus_1, int ramp) {
@@ -506,6 +585,7 @@ __device__ __forceinline__ void batched_div(Has has, Num num, Den den, Use use) 
 
 // Cluster-wide barrier with release/acquire semantics (DSMEM and global
 // memory writes before it are visible after it); a CTA barrier when C == 1.
+// Used once or twice per problem, never inside the relaxation loop.
 __device__ __forceinline__ void csync(int C) {
   if (C > 1) {
     cg::this_cluster().sync();
@@ -560,44 +640,75 @@ __device__ __noinline__ void fixed_forces_and_stress(const frb_batch& b, int p, 
   }
 }
 
+__device__ __forceinline__ void write_singular(const frb_batch& b, int p, int bad, int iters) {
+  frb_result& r = b.results[p];
+  r.status = FRB_STATUS_SINGULAR;
+  r.bad_element = bad;
+  r.iters = iters;
+  r.converged = 0;
+  r.final_residual = r.r_ref = r.energy_residual = qnan();
+}
+
 // ------------------------------------------------------------------ the solve
 
 struct Smem {
-  double* pos;   // [3][PS]
+  double* pos;   // [PN][3]
   double* fcur;  // [NFO]
   double* fprv;  // [NFO]
   double* cf;    // [CF]
   double* slot;  // [2L-1][3]
+  double* flag;  // [16] singular flags of the cluster's ranks
   int* prog;     // [levels+1] level offsets, then dst, left, right
 };
 
 __device__ __forceinline__ Smem carve(double* smem, const Net& n, const Rank& R) {
   Smem s;
   s.pos = smem;
-  s.fcur = s.pos + 3 * R.PS;
+  s.fcur = s.pos + 3 * R.PN;
   s.fprv = s.fcur + R.NFO;
   s.cf = s.fprv + R.NFO;
   s.slot = s.cf + R.CF;
-  s.prog = reinterpret_cast<int*>(s.slot + 3 * (n.L > 0 ? 2 * n.L - 1 : 1));
+  s.flag = s.slot + 3 * (n.L > 0 ? 2 * n.L - 1 : 1);
+  s.prog = reinterpret_cast<int*>(s.flag + 16);
   return s;
+}
+
+struct Mbar {
+  uint64_t* h;   // halo positions
+  uint64_t* s;   // leaf sums + flags
+  uint32_t ph_h, ph_s;
+};
+
+// Complete the two phases posted for an iteration that will not run, so the
+// barriers are idle for the next problem (see the header comment).
+__device__ __forceinline__ void drain(Mbar& mb, const Rank& R) {
+  if (threadIdx.x == 0) {
+    mbar_complete(mb.h, R.halo_bytes);
+    mbar_complete(mb.s, R.leaf_bytes);
+  }
+  mbar_wait(mb.h, mb.ph_h);
+  mbar_wait(mb.s, mb.ph_s);
+  mb.ph_h ^= 1u;
+  mb.ph_s ^= 1u;
 }
 
 template <int MAXK>
 __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, int rank, double* smem,
-                              Scalars& sc, const Net& n, const Rank& R) {
+                              Scalars& sc, Mbar& mb, const Net& n, const Rank& R) {
   const int T = blockDim.x, t = threadIdx.x, lane = t & 31;
-  const int C = n.C, NF = n.NF, L = n.L, n_own = R.n_own, nfo = 3 * n_own;
+  const int C = n.C, L = n.L, n_own = R.n_own, nfo = 3 * n_own;
   const Smem S = carve(smem, n, R);
   double* __restrict__ pos = S.pos;
   double* __restrict__ fcur = S.fcur;
   double* __restrict__ fprv = S.fprv;
   double* __restrict__ cf = S.cf;
   double* __restrict__ slot = S.slot;
-  const int PS = R.PS;
-  const PosRank P{pos, n.posg, PS, R.n_local, NF};
   const double* __restrict__ Xg = n.X;
-  const double* __restrict__ mass = n.mass;
+  const double* __restrict__ mass3 = n.mass3;
   const int dof0 = 3 * R.node0;
+  const uint32_t off_pos = smem_u32(pos) - smem_u32(smem);
+  const uint32_t off_slot = smem_u32(slot) - smem_u32(smem);
+  const uint32_t off_flag = smem_u32(S.flag) - smem_u32(smem);
 
   // the tree's combine program lives in SMEM (warp 0 walks it every iteration)
   const int n_ops = L > 0 ? L - 1 : 0;
@@ -644,81 +755,89 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
     nt = lsize - 8 * q;
   }
 
-  // new position of own DOF dl: local SoA slot + the halo copies of peers
+  // new position of own DOF dl: local slot + the halo copies of peers
   auto put_pos = [&](int dl, double x) {
-    const int node = dl / 3, axis = dl - 3 * node;
-    pos[axis * PS + node] = x;
+    pos[dl] = x;
     if (C > 1) {
+      const int node = dl / 3, axis = dl - 3 * node;
       const int2 tg = __ldg(R.send + node);
-      if (tg.x >= 0) peer(pos, tg.x >> 24)[axis * PS + (tg.x & 0xffffff)] = x;
-      if (tg.y >= 0) peer(pos, tg.y >> 24)[axis * PS + (tg.y & 0xffffff)] = x;
+      if (tg.x >= 0) {
+        const int qr = tg.x >> 24;
+        st_async(sc.peer_smem[qr] + off_pos + 8u * (3u * (tg.x & 0xffffff) + axis), x, sc.peer_bar_h[qr]);
+      }
+      if (tg.y >= 0) {
+        const int qr = tg.y >> 24;
+        st_async(sc.peer_smem[qr] + off_pos + 8u * (3u * (tg.y & 0xffffff) + axis), x, sc.peer_bar_h[qr]);
+      }
     }
   };
 
   // ---- prologue: BCs, initial positions (microsolver.py:400-411) ---------
+  // post the first halo and leaf-sum phases before any peer may send
+  if (C > 1 && t == 0) {
+    mbar_expect(mb.h, R.halo_bytes);
+    mbar_expect(mb.s, R.leaf_bytes);
+  }
   for (int l = t; l < R.n_local; l += T) {
     const int g = l < n_own ? R.node0 + l : R.halo_g[l - n_own];
-    for (int a = 0; a < 3; ++a) pos[a * PS + l] = dadd(Xg[3 * g + a], 0.0);
+    for (int a = 0; a < 3; ++a) pos[3 * l + a] = dadd(Xg[3 * g + a], 0.0);
   }
+  set_local_fixed(n, R, pos, alpha, ramp);
   set_fixed_positions(n, rank, alpha, ramp);
   // initial free positions to global too (the all-element check reads posg)
   for (int l = t; l < n_own; l += T)
     for (int a = 0; a < 3; ++a) n.posg[3 * (R.node0 + l) + a] = dadd(Xg[3 * (R.node0 + l) + a], 0.0);
   csync(C);
-  check_elements(n, PosGlobalAll{n.posg}, sc, true);
+  if (check_elements(n, PosGlobalAll{n.posg}, true)) sc.singular = 1;
   __syncthreads();
   if (sc.singular) {
+    if (C > 1) drain(mb, R);
     const int bad = singular_argmin(n, PosGlobalAll{n.posg}, sc);
-    if (rank == 0 && t == 0) {
-      frb_result& r = b.results[p];
-      r.status = FRB_STATUS_SINGULAR;
-      r.bad_element = bad;
-      r.iters = 0;
-      r.converged = 0;
-      r.final_residual = r.r_ref = r.energy_residual = qnan();
-    }
+    if (rank == 0 && t == 0) write_singular(b, p, bad, 0);
     return;
   }
   // initial internal forces on own nodes (:413-420), kept as f_prev
-  element_coefs(R, n.ea, P, cf);
+  element_coefs(R, n.ea, pos, cf);
   __syncthreads();
   for (int i = t; i < n_own; i += T) {
     double fx, fy, fz;
-    node_force_ell(R, cf, P, i, fx, fy, fz);
+    node_force_ell(R, cf, pos, i, fx, fy, fz);
     fprv[3 * i] = fx;
     fprv[3 * i + 1] = fy;
     fprv[3 * i + 2] = fz;
   }
   __syncthreads();
   // a = -f/m (:428-430), then iteration 0's kick + drift (:443-448)
-  {
-    batched_div<MAXK>(
-        has, [&](int k) { return -fprv[t + k * T]; }, [&](int k) { return __ldg(mass + (dof0 + t + k * T) / 3); },
-        [&](int k, double a) {
-          const int dl = t + k * T;
-          v[k] = dadd(0.0, dmul(hdt, a));
-          u[k] = dadd(0.0, dmul(dt, v[k]));
-          put_pos(dl, dadd(__ldg(Xg + dof0 + dl), u[k]));
-        });
-  }
+  batched_div<MAXK>(
+      has, [&](int k) { return -fprv[t + k * T]; }, [&](int k) { return __ldg(mass3 + dof0 + t + k * T); },
+      [&](int k, double a) {
+        const int dl = t + k * T;
+        v[k] = dadd(0.0, dmul(hdt, a));
+        u[k] = dadd(0.0, dmul(dt, v[k]));
+        put_pos(dl, dadd(__ldg(Xg + dof0 + dl), u[k]));
+      });
   if (ramp) {  // iteration 0's ramp step (:449-453)
     alpha = ramp_alpha(1, ramp_n);
-    set_fixed_positions(n, rank, alpha, ramp);
+    set_local_fixed(n, R, pos, alpha, ramp);
   }
-  csync(C);
+  __syncthreads();
 
   // ---- relaxation loop (microsolver.py:434-530) ---------------------------
   mark(sc, prof, 7);
   int it = 0;
   for (;; ++it) {
+    if (C > 1) {  // halo positions of this iteration
+      mbar_wait(mb.h, mb.ph_h);
+      mb.ph_h ^= 1u;
+    }
     // F: internal forces at the drifted positions (:456-465)
-    bool bad = element_coefs(R, n.ea, P, cf);
-    if (ramp && it < ramp_n) check_elements(n, PosGlobalAll{n.posg}, sc, false);  // fixed-fixed
+    bool bad = element_coefs(R, n.ea, pos, cf);
+    if (ramp && it < ramp_n && rank == 0) bad |= check_elements(n, PosFixed{&n, alpha, ramp}, false);
     __syncthreads();
     mark(sc, prof, 0);
     for (int i = t; i < n_own; i += T) {
       double fx, fy, fz;
-      node_force_ell(R, cf, P, i, fx, fy, fz);
+      node_force_ell(R, cf, pos, i, fx, fy, fz);
       fcur[3 * i] = fx;
       fcur[3 * i + 1] = fy;
       fcur[3 * i + 2] = fz;
@@ -731,23 +850,21 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
     // np.maximum(k_hat, 0) (:468-476); sq = (u k_hat) u, sq2 = (u m) u,
     // ff = f f (:489).  Outputs: sq -> own position slot, sq2 -> cf,
     // ff -> fcur, f -> fprv.
-    {
-      batched_div<MAXK>(
-          has, [&](int k) { return dsub(fcur[t + k * T], fprv[t + k * T]); },
-          [&](int k) { return adaptive ? dmul(dt, v[k]) : 0.0; },
-          [&](int k, double kh) {
-            const int dl = t + k * T;
-            const double f = fcur[dl];
-            if (adaptive) {
-              kh = (kh > 0.0 || isnan(kh)) ? kh : 0.0;
-              const int node = dl / 3;
-              pos[(dl - 3 * node) * PS + node] = dmul(dmul(u[k], kh), u[k]);
-              cf[dl] = dmul(dmul(u[k], __ldg(mass + (dof0 + dl) / 3)), u[k]);
-            }
-            fcur[dl] = dmul(f, f);
-            fprv[dl] = f;
-          });
-    }
+    if (C > 1 && t == 0) mbar_expect(mb.h, R.halo_bytes);  // next halo phase
+    batched_div<MAXK>(
+        has, [&](int k) { return dsub(fcur[t + k * T], fprv[t + k * T]); },
+        [&](int k) { return adaptive ? dmul(dt, v[k]) : 0.0; },
+        [&](int k, double kh) {
+          const int dl = t + k * T;
+          const double f = fcur[dl];
+          if (adaptive) {
+            kh = (kh > 0.0 || isnan(kh)) ? kh : 0.0;
+            pos[dl] = dmul(dmul(u[k], kh), u[k]);
+            cf[dl] = dmul(dmul(u[k], __ldg(mass3 + dof0 + dl)), u[k]);
+          }
+          fcur[dl] = dmul(f, f);
+          fprv[dl] = f;
+        });
     __syncthreads();
     mark(sc, prof, 2);
 
@@ -756,27 +873,23 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
     if ((t & ~31) < 8 * R.n_leaves) {  // warp holds at least one chain
       double r0 = 0.0, r1 = 0.0, r2 = 0.0;
       double t0 = 0.0, t1 = 0.0, t2 = 0.0;
-      auto sqv = [&](int dl) {
-        const int node = dl / 3;
-        return pos[(dl - 3 * node) * PS + node];
-      };
       if (chain) {
         int dl = lstart + j;
         if (q > 0) {
-          r0 = sqv(dl);
+          r0 = pos[dl];
           r1 = cf[dl];
           r2 = fcur[dl];
 #pragma unroll 4
           for (int k = 1; k < q; ++k) {
             dl += 8;
-            r0 = dadd(r0, sqv(dl));
+            r0 = dadd(r0, pos[dl]);
             r1 = dadd(r1, cf[dl]);
             r2 = dadd(r2, fcur[dl]);
           }
         }
         if (j < nt) {
           const int dtl = lstart + 8 * q + j;
-          t0 = sqv(dtl);
+          t0 = pos[dtl];
           t1 = cf[dtl];
           t2 = fcur[dtl];
         }
@@ -803,34 +916,44 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
       }
       if (chain && j == 0) {
         const int s = 3 * (R.leaf0 + lloc);
+        slot[s] = r0;
+        slot[s + 1] = r1;
+        slot[s + 2] = r2;
         for (int qr = 0; qr < C; ++qr) {
-          double* ds = C > 1 ? peer(slot, qr) : slot;
-          ds[s] = r0;
-          ds[s + 1] = r1;
-          ds[s + 2] = r2;
+          if (qr == rank) continue;
+          const uint32_t a = sc.peer_smem[qr] + off_slot + 8u * s;
+          st_async(a, r0, sc.peer_bar_s[qr]);
+          st_async(a + 8, r1, sc.peer_bar_s[qr]);
+          st_async(a + 16, r2, sc.peer_bar_s[qr]);
         }
       }
     }
-    if (C > 1 && t == 0 && sc.singular)
-      for (int qr = 0; qr < C; ++qr) *peer(&sc.singular, qr) = 1;
-    csync(C);
+    if (C > 1 && t == 0) {
+      const double fl = sc.singular ? 1.0 : 0.0;
+      for (int qr = 0; qr < C; ++qr)
+        if (qr != rank) st_async(sc.peer_smem[qr] + off_flag + 8u * rank, fl, sc.peer_bar_s[qr]);
+    }
+    __syncthreads();
+    if (C > 1) {  // every peer's leaf sums and flag
+      mbar_wait(mb.s, mb.ph_s);
+      mb.ph_s ^= 1u;
+      if (t == 0) mbar_expect(mb.s, R.leaf_bytes);  // next leaf-sum phase
+    }
     mark(sc, prof, 3);
-    if (sc.singular) {
-      // positions of every free node to global memory, then the argmin over
-      // all elements (each rank redundantly; rank 0 reports)
+    bool singular = sc.singular != 0;
+    if (C > 1)
+      for (int qr = 0; qr < C; ++qr) singular |= (qr != rank) && S.flag[qr] != 0.0;
+    if (singular) {
+      if (C > 1) drain(mb, R);
+      // positions of every node to global memory, then the argmin over all
+      // elements (each rank redundantly; rank 0 reports)
 #pragma unroll
       for (int k = 0; k < MAXK; ++k)
         if (has(k)) n.posg[dof0 + t + k * T] = dadd(__ldg(Xg + dof0 + t + k * T), u[k]);
+      set_fixed_positions(n, rank, alpha, ramp);
       csync(C);
       const int badi = singular_argmin(n, PosGlobalAll{n.posg}, sc);
-      if (rank == 0 && t == 0) {
-        frb_result& r = b.results[p];
-        r.status = FRB_STATUS_SINGULAR;
-        r.bad_element = badi;
-        r.iters = it;
-        r.converged = 0;
-        r.final_residual = r.r_ref = r.energy_residual = qnan();
-      }
+      if (rank == 0 && t == 0) write_singular(b, p, badi, it);
       return;
     }
 
@@ -892,27 +1015,27 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
     // iteration's first half-kick and drift (:443-453) unless finished
     const double c = sc.c;
     const bool done = sc.done != 0;
-    {
-      batched_div<MAXK>(
-          has, [&](int k) { return -fprv[t + k * T]; }, [&](int k) { return __ldg(mass + (dof0 + t + k * T) / 3); },
-          [&](int k, double fm) {
-            const double a = dsub(fm, dmul(c, v[k]));
+    batched_div<MAXK>(
+        has, [&](int k) { return -fprv[t + k * T]; }, [&](int k) { return __ldg(mass3 + dof0 + t + k * T); },
+        [&](int k, double fm) {
+          const double a = dsub(fm, dmul(c, v[k]));
+          v[k] = dadd(v[k], dmul(hdt, a));
+          if (!done) {
             v[k] = dadd(v[k], dmul(hdt, a));
-            if (!done) {
-              v[k] = dadd(v[k], dmul(hdt, a));
-              u[k] = dadd(u[k], dmul(dt, v[k]));
-              put_pos(t + k * T, dadd(__ldg(Xg + dof0 + t + k * T), u[k]));
-            }
-          });
-    }
+            u[k] = dadd(u[k], dmul(dt, v[k]));
+            put_pos(t + k * T, dadd(__ldg(Xg + dof0 + t + k * T), u[k]));
+          }
+        });
     if (!done && ramp && alpha < 1.0) {
       alpha = ramp_alpha(it + 2, ramp_n);
-      set_fixed_positions(n, rank, alpha, ramp);
+      set_local_fixed(n, R, pos, alpha, ramp);
     }
-    csync(C);
-    mark(sc, prof, 5);
     if (done) break;
+    __syncthreads();
+    mark(sc, prof, 5);
   }
+  if (C > 1) drain(mb, R);
+  mark(sc, prof, 5);
 
   // ---- epilogue: outputs in solver order + stress (:549-564, :285-299) ----
   double* uo = b.u + 3 * n.node_base;
@@ -926,6 +1049,7 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
       n.posg[d] = dadd(__ldg(Xg + d), u[k]);  // x = X + u, all free nodes
     }
   }
+  set_fixed_positions(n, rank, alpha, ramp);
   csync(C);
   if (rank == 0) fixed_forces_and_stress(b, p, n, sc, it, alpha, ramp, full_bc_iter);
   __syncthreads();
@@ -939,12 +1063,25 @@ __global__ void __launch_bounds__(MAXT, 1)
   __shared__ Scalars sc;
   __shared__ Net net;
   __shared__ Rank rk;
+  __shared__ uint64_t bars[2];
   const int C = static_cast<int>(cg::this_cluster().num_blocks());
   const int rank = C > 1 ? static_cast<int>(cg::this_cluster().block_rank()) : 0;
   if (threadIdx.x == 0) {
     for (int k = 0; k < 8; ++k) sc.clk[k] = 0;
     sc.t_last = clock64();
+    if (C > 1) {
+      mbar_init(&bars[0], 1);
+      mbar_init(&bars[1], 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      for (int q = 0; q < C; ++q) {
+        sc.peer_smem[q] = mapa(smem_u32(smem), q);
+        sc.peer_bar_h[q] = mapa(smem_u32(&bars[0]), q);
+        sc.peer_bar_s[q] = mapa(smem_u32(&bars[1]), q);
+      }
+    }
   }
+  Mbar mb{&bars[0], &bars[1], 0u, 0u};
+  csync(C);  // barriers initialised cluster-wide before any remote use
   for (;;) {
     if (rank == 0 && threadIdx.x == 0) {
       const int idx = atomicAdd(queue, 1);
@@ -962,7 +1099,7 @@ __global__ void __launch_bounds__(MAXT, 1)
       sc.threshold = __longlong_as_double(0x7ff0000000000000ULL);  // +inf until set
     }
     __syncthreads();
-    solve_problem<MAXK>(b, cfg, p, rank, smem, sc, net, rk);
+    solve_problem<MAXK>(b, cfg, p, rank, smem, sc, mb, net, rk);
     csync(C);  // no rank reuses its SMEM before every peer is done with it
   }
   if (b.phase_cycles && threadIdx.x == 0) {
@@ -977,10 +1114,11 @@ __global__ void __launch_bounds__(256) frb_forces_kernel(frb_batch b, const doub
   __shared__ Scalars sc;
   __shared__ Net n;
   __shared__ Rank rk;
+  __shared__ int any_bad;
   const int p = blockIdx.x;
   if (threadIdx.x == 0) {
     load_views(n, rk, b, p, 0);
-    sc.singular = 0;
+    any_bad = 0;
   }
   __syncthreads();
   const PosGlobal pos{n.X, u + 3 * n.node_base};
@@ -993,10 +1131,10 @@ __global__ void __launch_bounds__(256) frb_forces_kernel(frb_batch b, const doub
     fp[3 * i + 1] = fy;
     fp[3 * i + 2] = fz;
   }
-  if (bad) sc.singular = 1;
+  if (bad) any_bad = 1;
   __syncthreads();
   int badi = -1;
-  if (sc.singular) badi = singular_argmin(n, pos, sc);
+  if (any_bad) badi = singular_argmin(n, pos, sc);
   if (threadIdx.x == 0) {
     b.results[p].status = badi >= 0 ? FRB_STATUS_SINGULAR : FRB_STATUS_CONVERGED;
     b.results[p].bad_element = badi;
@@ -1109,13 +1247,13 @@ int frb_device_info(int device, int* n_sm, int* smem_optin, int* cc_major, int* 
   return FRB_OK;
 }
 
-int64_t frb_rank_smem_bytes(int32_t n_local, int32_t n_own, int32_t n_act, int32_t n_leaves_total) {
+int64_t frb_rank_smem_bytes(int32_t n_pos, int32_t n_own, int32_t n_act, int32_t n_leaves_total) {
   const int64_t nf = 3 * static_cast<int64_t>(n_own);
   const int64_t L = n_leaves_total;
   const int64_t slots = L > 0 ? 2 * L - 1 : 1;
   const int64_t levels = L > 1 ? 64 - __builtin_clzll(static_cast<uint64_t>(L - 1)) + 1 : 0;  // >= tree height
   const int64_t prog_ints = (levels + 1) + 3 * (L > 0 ? L - 1 : 0);
-  return 8 * (3 * static_cast<int64_t>(n_local) + 2 * nf + (nf > n_act ? nf : n_act) + 3 * slots) +
+  return 8 * (3 * static_cast<int64_t>(n_pos) + 2 * nf + (nf > n_act ? nf : n_act) + 3 * slots + 16) +
          4 * ((prog_ints + 1) & ~1LL);
 }
 

@@ -8,16 +8,19 @@ per-DOF work, the ordered chain sums and the force gather of a node all stay
 on one rank.  Cuts are chosen among leaf starts that are multiples of 3,
 nearest to the even split.
 
-Per rank the kernel works in *local* node numbering:
-    [0, n_own)            own free nodes (global solver ids node0 ...)
-    [n_own, n_local)      halo: free neighbours owned by other ranks
-    n_local + (g - NF)    fixed node g (positions live in global scratch)
+Per rank the kernel works in *local* node numbering; every local node's
+position lives in the rank's shared memory (AoS, 3 doubles per node):
+    [0, n_own)                 own free nodes (global solver ids node0 ...)
+    [n_own, n_local)           halo: free neighbours owned by other ranks
+    [n_local, n_local + n_fix) fixed nodes that end an active element
 Tables built here (all int32, shared by networks of equal topology):
     ell_o / ell_c   slot-major incidence of the own nodes (other endpoint in
-                    local numbering, index into the rank's active list)
+                    local numbering, index into the rank's active list); the
+                    device gets them packed as one u32 per slot (``ell``)
     act_ab          active elements (>= 1 own endpoint) in local numbering
     act_elem        their global element ids (per-network L / EA lookups)
     halo_g          global solver id of each halo node
+    fix_g           global solver id of each local fixed node
     send            per own node up to two (rank << 24 | local index) targets
                     that keep it as halo (-1 = none)
 """
@@ -31,6 +34,8 @@ import numpy as np
 from .plan import PlanView
 
 MAX_SEND = 2
+ELL_PAD = 0xFFFFFFFF          # padding slot of the packed incidence table
+MAX_LOCAL = 0xFFFF            # local node ids and active-element ids are 16 bit
 
 
 @dataclass
@@ -46,10 +51,24 @@ class RankTables:
     act_elem: np.ndarray     # (n_act,) int64
     halo_g: np.ndarray       # (n_local - n_own,) int32
     send: np.ndarray         # (n_own, MAX_SEND) int32
+    fix_g: np.ndarray = None # (n_fix,) int32
 
     @property
     def stride(self) -> int:
         return self.ell_o.shape[1]
+
+    @property
+    def n_fix(self) -> int:
+        return len(self.fix_g)
+
+    @property
+    def ell(self) -> np.ndarray:
+        """Packed slot table for the device: (other << 16) | active index,
+        ELL_PAD on padding (uint32, same shape as ell_o)."""
+        pad = self.ell_o < 0
+        w = (self.ell_o.astype(np.int64) << 16) | self.ell_c.astype(np.int64)
+        w[pad] = ELL_PAD
+        return w.astype(np.uint32)
 
     @property
     def n_act(self) -> int:
@@ -116,17 +135,21 @@ def partition(n_nodes: int, n_free: int, ia: np.ndarray, ib: np.ndarray, ell_oth
         act = elem_ids[own_a | own_b]
         ends = np.concatenate([ia[act], ib[act]])
         halo = np.unique(ends[(ends < n_free) & ((ends < n0) | (ends >= n1))])
+        fix = np.unique(ends[ends >= n_free])
         halo_lists.append(halo)
         n_local = n_own + len(halo)
+        if n_local + len(fix) > MAX_LOCAL or len(act) > MAX_LOCAL:
+            raise ValueError(f"rank {r} needs {n_local + len(fix)} local nodes / {len(act)} elements "
+                             f"(limit {MAX_LOCAL}); use a larger cluster")
 
-        def to_local(g, n0=n0, n1=n1, halo=halo, n_local=n_local, n_own=n_own):
+        def to_local(g, n0=n0, n1=n1, halo=halo, fix=fix, n_local=n_local, n_own=n_own):
             g = np.asarray(g, dtype=np.int64)
             out = np.empty_like(g)
             own = (g >= n0) & (g < n1)
             fixed = g >= n_free
             hal = ~own & ~fixed
             out[own] = g[own] - n0
-            out[fixed] = n_local + (g[fixed] - n_free)
+            out[fixed] = n_local + np.searchsorted(fix, g[fixed])
             out[hal] = n_own + np.searchsorted(halo, g[hal])
             return out
 
@@ -148,7 +171,8 @@ def partition(n_nodes: int, n_free: int, ia: np.ndarray, ib: np.ndarray, ell_oth
                                 leaf0=int(lstarts[0]) if len(lstarts) else 0,
                                 n_leaves=len(lstarts), ell_o=ell_o, ell_c=ell_c, act_ab=act_ab,
                                 act_elem=act.astype(np.int64), halo_g=halo.astype(np.int32),
-                                send=np.full((n_own, MAX_SEND), -1, dtype=np.int32)))
+                                send=np.full((n_own, MAX_SEND), -1, dtype=np.int32),
+                                fix_g=fix.astype(np.int32)))
     # send lists: rank q keeps node g as halo at local index n_own_q + k
     for q, halo in enumerate(halo_lists):
         for k, g in enumerate(halo):
@@ -163,17 +187,17 @@ def partition(n_nodes: int, n_free: int, ia: np.ndarray, ib: np.ndarray, ell_oth
 
 def rank_smem_bytes(rt: RankTables, n_leaves_total: int) -> int:
     """Dynamic SMEM of one rank (mirror of frb_rank_smem_bytes):
-    positions [3][n_local] (a DOF's own position slot doubles as its sq
-    entry between the force and update phases), f, f_prev (8 B per own DOF
-    each), coefficients / sq2 max(own DOFs, n_act), tree slots [2L-1][3] and
-    the tree's int32 combine program."""
-    return smem_bytes(rt.n_local, rt.n_own, rt.n_act, n_leaves_total)
+    positions [n_local + n_fix][3] (a DOF's own position slot doubles as its
+    sq entry between the force and update phases), f, f_prev (8 B per own
+    DOF each), coefficients / sq2 max(own DOFs, n_act), tree slots [2L-1][3],
+    16 cluster flag words and the tree's int32 combine program."""
+    return smem_bytes(rt.n_local + rt.n_fix, rt.n_own, rt.n_act, n_leaves_total)
 
 
-def smem_bytes(n_local: int, n_own: int, n_act: int, n_leaves_total: int) -> int:
+def smem_bytes(n_pos: int, n_own: int, n_act: int, n_leaves_total: int) -> int:
     nf = 3 * n_own
     L = n_leaves_total
     slots = 2 * L - 1 if L > 0 else 1
     levels = (L - 1).bit_length() + 1 if L > 1 else 0
     prog = (levels + 1) + 3 * (L - 1 if L > 0 else 0)
-    return 8 * (3 * n_local + 2 * nf + max(nf, n_act) + 3 * slots) + 4 * ((prog + 1) & ~1)
+    return 8 * (3 * n_pos + 2 * nf + max(nf, n_act) + 3 * slots + 16) + 4 * ((prog + 1) & ~1)

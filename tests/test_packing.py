@@ -79,10 +79,16 @@ def test_partition_tables(net, C):
                 return rt.node0 + l
             if l < rt.n_local:
                 return halo[l - rt.n_own]
-            return NF + (l - rt.n_local)
+            return int(rt.fix_g[l - rt.n_local])
 
         act = set(np.flatnonzero(np.isin(ia, list(own)) | np.isin(ib, list(own))))
         assert set(rt.act_elem) == act
+        ends = np.concatenate([ia[rt.act_elem], ib[rt.act_elem]])
+        assert list(rt.fix_g) == sorted(set(ends[ends >= NF].tolist()))   # fixed ends of active elements
+        w = rt.ell.astype(np.int64)
+        pad = rt.ell_o < 0
+        assert (w[pad] == 0xFFFFFFFF).all()
+        assert (w[~pad] >> 16 == rt.ell_o[~pad]).all() and (w[~pad] & 0xFFFF == rt.ell_c[~pad]).all()
         for e, (a, b) in zip(rt.act_elem, rt.act_ab):
             assert (glob(a), glob(b)) == (ia[e], ib[e])
         for i in range(rt.n_own):
