@@ -74,7 +74,7 @@ namespace {
 constexpr int kMaxThreads = 1024;
 constexpr int kMaxWarps = kMaxThreads / 32;
 constexpr double kCollapse = 1e-12;  // microsolver.py:30
-constexpr uint32_t kEllPad = 0xFFFFFFFFu;
+constexpr int kChunk = 4;  // per-DOF phases process a thread's DOFs in chunks of this many
 
 __device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
@@ -287,13 +287,6 @@ __device__ __noinline__ LenCoef exact_len_coef(double dx, double dy, double dz, 
 }
 __device__ __noinline__ double exact_div(double a, double b) { return ddiv(a, b); }
 
-// a / b through the branch-free fast path, exact fallback out of line.
-__device__ __forceinline__ double div_rn(double a, double b) {
-  bool ok;
-  const double q = frb_arith::div_fast(a, b, ok);
-  return ok ? q : exact_div(a, b);
-}
-
 // Length and force coefficient of one element through the fast paths.
 __device__ __forceinline__ LenCoef len_coef(double dx, double dy, double dz, double L, double EA) {
   bool ok1, ok2;
@@ -350,34 +343,33 @@ __device__ __noinline__ bool node_force_csr(const Net& n, const Pos& pos, int i,
   return bad;
 }
 
+// The rank's dynamic shared memory.  Hot loops index it with integer
+// offsets (never through generic pointers), so every access is an LDS/STS
+// with the CTA's shared window base held in one register.
+extern __shared__ __align__(16) double g_smem[];
+
 // Phase F1: coefficient EA (l - L) / (L l) of every active element of the
 // rank, once per iteration (microsolver.py:196-211).  Elements cut by a rank
 // boundary are evaluated by both ranks from identical operands.
-__device__ __forceinline__ void act_one(const Rank& R, double ea, const double* __restrict__ pos, int e, int2 ab,
-                                        double L, double* __restrict__ cf, bool& bad) {
-  const double EA = R.act_EA ? __ldg(R.act_EA + e) : ea;
-  const double* pa = pos + 3 * ab.x;
-  const double* pb = pos + 3 * ab.y;
-  const double dx = dsub(pb[0], pa[0]);
-  const double dy = dsub(pb[1], pa[1]);
-  const double dz = dsub(pb[2], pa[2]);
-  const LenCoef lc = len_coef(dx, dy, dz, L, EA);
-  bad |= lc.l < dmul(kCollapse, L);
-  cf[e] = lc.coef;
-}
-
-__device__ __forceinline__ bool element_coefs(const Rank& R, double ea, const double* __restrict__ pos,
-                                              double* __restrict__ cf) {
+__device__ __forceinline__ bool element_coefs(int n_act, const int2* __restrict__ act_ab,
+                                              const double* __restrict__ act_L, const double* __restrict__ act_EA,
+                                              double ea, int o_pos, int o_cf) {
   bool bad = false;
   const int T = blockDim.x;
-  int e = threadIdx.x;
-  for (; e + T < R.n_act; e += 2 * T) {  // two elements per step: their loads overlap
-    const int2 ab0 = __ldg(R.act_ab + e), ab1 = __ldg(R.act_ab + e + T);
-    const double L0 = __ldg(R.act_L + e), L1 = __ldg(R.act_L + e + T);
-    act_one(R, ea, pos, e, ab0, L0, cf, bad);
-    act_one(R, ea, pos, e + T, ab1, L1, cf, bad);
+#pragma unroll 2
+  for (int e = threadIdx.x; e < n_act; e += T) {
+    const int2 ab = __ldg(act_ab + e);
+    const double L = __ldg(act_L + e);
+    const double EA = act_EA ? __ldg(act_EA + e) : ea;
+    const double* pa = &g_smem[o_pos + 3 * ab.x];
+    const double* pb = &g_smem[o_pos + 3 * ab.y];
+    const double dx = dsub(pb[0], pa[0]);
+    const double dy = dsub(pb[1], pa[1]);
+    const double dz = dsub(pb[2], pa[2]);
+    const LenCoef lc = len_coef(dx, dy, dz, L, EA);
+    bad |= lc.l < dmul(kCollapse, L);
+    g_smem[o_cf + e] = lc.coef;
   }
-  if (e < R.n_act) act_one(R, ea, pos, e, __ldg(R.act_ab + e), __ldg(R.act_L + e), cf, bad);
   return bad;
 }
 
@@ -385,24 +377,27 @@ __device__ __forceinline__ bool element_coefs(const Rank& R, double ea, const do
 // (= element) order: role a accumulates 0 - nd - nd ..., role b
 // 0 + nd + nd ...  nd = d * coef with d = P[b] - P[a] recomputed from the
 // operands F1 used, so it is bitwise the reference's per-element value.
-// Padding slots are skipped (exact: the reference adds nothing there).  The
-// slot words of a group are loaded up front so their latencies overlap.
-constexpr int kSlots = 4;
+// Padding slots point at node i itself (partition.py RankTables.ell): their
+// d is +0 and they add a signed zero, which leaves the sums unchanged, so
+// the gather is branch-free.  The slot words of a group are loaded up front
+// so their latencies overlap.
+constexpr int kSlots = 3;
 
 template <bool kRoleA>
-__device__ __forceinline__ void gather_role(const Rank& R, const double* __restrict__ cf,
-                                            const double* __restrict__ pos, int i, int k_begin, int k_end,
-                                            double px, double py, double pz, double& sx, double& sy,
-                                            double& sz) {
-  for (int k0 = k_begin; k0 < k_end; k0 += kSlots) {
+__device__ __forceinline__ void gather_role(const uint32_t* __restrict__ ell_i, int S, int n_slots, int i,
+                                            int o_pos, int o_cf, double px, double py, double pz, double& sx,
+                                            double& sy, double& sz) {
+  for (int k0 = 0; k0 < n_slots; k0 += kSlots) {
     uint32_t w[kSlots];
+    w[0] = __ldg(ell_i + k0 * S);
+    // slots past the end become self-padding of node i (a +-0 contribution)
+    const uint32_t self_pad = (static_cast<uint32_t>(i) << 16) | (w[0] & 0xffffu);
 #pragma unroll
-    for (int q = 0; q < kSlots; ++q) w[q] = k0 + q < k_end ? __ldg(R.ell + (k0 + q) * R.S + i) : kEllPad;
+    for (int q = 1; q < kSlots; ++q) w[q] = k0 + q < n_slots ? __ldg(ell_i + (k0 + q) * S) : self_pad;
 #pragma unroll
     for (int q = 0; q < kSlots; ++q) {
-      if (w[q] == kEllPad) continue;
-      const double* po = pos + 3 * (w[q] >> 16);
-      const double coef = cf[w[q] & 0xffffu];
+      const double* po = &g_smem[o_pos + 3 * static_cast<int>(w[q] >> 16)];
+      const double coef = g_smem[o_cf + static_cast<int>(w[q] & 0xffffu)];
       if (kRoleA) {  // bincount(ia, -nd): 0 + (-nd) + ...,  d = P[o] - P[i]
         sx = dsub(sx, dmul(dsub(po[0], px), coef));
         sy = dsub(sy, dmul(dsub(po[1], py), coef));
@@ -416,16 +411,18 @@ __device__ __forceinline__ void gather_role(const Rank& R, const double* __restr
   }
 }
 
-__device__ __forceinline__ void node_force_ell(const Rank& R, const double* __restrict__ cf,
-                                               const double* __restrict__ pos, int i, double& fx, double& fy,
-                                               double& fz) {
-  const double px = pos[3 * i], py = pos[3 * i + 1], pz = pos[3 * i + 2];
-  double ax = 0.0, ay = 0.0, az = 0.0, bx = 0.0, by = 0.0, bz = 0.0;
-  gather_role<true>(R, cf, pos, i, 0, R.SA, px, py, pz, ax, ay, az);
-  gather_role<false>(R, cf, pos, i, R.SA, R.SA + R.SB, px, py, pz, bx, by, bz);
-  fx = dadd(ax, bx);
-  fy = dadd(ay, by);
-  fz = dadd(az, bz);
+// f of every own node into g_smem[o_out + 3 i + axis]
+__device__ __forceinline__ void node_forces(int n_own, const uint32_t* __restrict__ ell, int S, int SA, int SB,
+                                            int o_pos, int o_cf, int o_out) {
+  for (int i = threadIdx.x; i < n_own; i += blockDim.x) {
+    const double px = g_smem[o_pos + 3 * i], py = g_smem[o_pos + 3 * i + 1], pz = g_smem[o_pos + 3 * i + 2];
+    double ax = 0.0, ay = 0.0, az = 0.0, bx = 0.0, by = 0.0, bz = 0.0;
+    gather_role<true>(ell + i, S, SA, i, o_pos, o_cf, px, py, pz, ax, ay, az);
+    gather_role<false>(ell + SA * S + i, S, SB, i, o_pos, o_cf, px, py, pz, bx, by, bz);
+    g_smem[o_out + 3 * i] = dadd(ax, bx);
+    g_smem[o_out + 3 * i + 1] = dadd(ay, by);
+    g_smem[o_out + 3 * i + 2] = dadd(az, bz);
+  }
 }
 
 // ------------------------------------------------------------------ block helpers
@@ -569,20 +566,6 @@ __device__ __forceinline__ double ramp_alpha(int it_plus_1, int ramp) {
   return x < 1.0 ? x : 1.0;
 }
 
-// Quotients num(k)/den(k) for the DOFs k < MAXK a thread owns (has(k)); use
-// (k, q) consumes them in DOF order.  den(k) == 0 yields q = 0 (the caller
-// decides what a zero denominator means).
-template <int MAXK, class Has, class Num, class Den, class Use>
-__device__ __forceinline__ void batched_div(Has has, Num num, Den den, Use use) {
-#pragma unroll
-  for (int k = 0; k < MAXK; ++k) {
-    if (has(k)) {
-      const double dk = den(k);
-      use(k, dk == 0.0 ? 0.0 : div_rn(num(k), dk));
-    }
-  }
-}
-
 // Cluster-wide barrier with release/acquire semantics (DSMEM and global
 // memory writes before it are visible after it); a CTA barrier when C == 1.
 // Used once or twice per problem, never inside the relaxation loop.
@@ -651,26 +634,22 @@ __device__ __forceinline__ void write_singular(const frb_batch& b, int p, int ba
 
 // ------------------------------------------------------------------ the solve
 
-struct Smem {
-  double* pos;   // [PN][3]
-  double* fcur;  // [NFO]
-  double* fprv;  // [NFO]
-  double* cf;    // [CF]
-  double* slot;  // [2L-1][3]
-  double* flag;  // [16] singular flags of the cluster's ranks
-  int* prog;     // [levels+1] level offsets, then dst, left, right
+// SMEM layout of a problem, in doubles from g_smem (identical on every
+// rank of the problem, so a peer's buffer is addressed by the same offset).
+struct Layout {
+  int pos, fcur, fprv, cf, slot, flag, prog;  // prog: int32 index
 };
 
-__device__ __forceinline__ Smem carve(double* smem, const Net& n, const Rank& R) {
-  Smem s;
-  s.pos = smem;
-  s.fcur = s.pos + 3 * R.PN;
-  s.fprv = s.fcur + R.NFO;
-  s.cf = s.fprv + R.NFO;
-  s.slot = s.cf + R.CF;
-  s.flag = s.slot + 3 * (n.L > 0 ? 2 * n.L - 1 : 1);
-  s.prog = reinterpret_cast<int*>(s.flag + 16);
-  return s;
+__device__ __forceinline__ Layout layout(const Net& n, const Rank& R) {
+  Layout o;
+  o.pos = 0;
+  o.fcur = 3 * R.PN;
+  o.fprv = o.fcur + R.NFO;
+  o.cf = o.fprv + R.NFO;
+  o.slot = o.cf + R.CF;
+  o.flag = o.slot + 3 * (n.L > 0 ? 2 * n.L - 1 : 1);
+  o.prog = 2 * (o.flag + 16);
+  return o;
 }
 
 struct Mbar {
@@ -693,26 +672,30 @@ __device__ __forceinline__ void drain(Mbar& mb, const Rank& R) {
 }
 
 template <int MAXK>
-__device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, int rank, double* smem,
-                              Scalars& sc, Mbar& mb, const Net& n, const Rank& R) {
+__device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, int rank, Scalars& sc, Mbar& mb,
+                              const Net& n, const Rank& R) {
   const int T = blockDim.x, t = threadIdx.x, lane = t & 31;
   const int C = n.C, L = n.L, n_own = R.n_own, nfo = 3 * n_own;
-  const Smem S = carve(smem, n, R);
-  double* __restrict__ pos = S.pos;
-  double* __restrict__ fcur = S.fcur;
-  double* __restrict__ fprv = S.fprv;
-  double* __restrict__ cf = S.cf;
-  double* __restrict__ slot = S.slot;
+  const Layout o = layout(n, R);
   const double* __restrict__ Xg = n.X;
   const double* __restrict__ mass3 = n.mass3;
   const int dof0 = 3 * R.node0;
-  const uint32_t off_pos = smem_u32(pos) - smem_u32(smem);
-  const uint32_t off_slot = smem_u32(slot) - smem_u32(smem);
-  const uint32_t off_flag = smem_u32(S.flag) - smem_u32(smem);
+  const int dl_max = nfo > 0 ? nfo - 1 : 0;  // clamp for unconditional per-DOF loads
+  // hot per-rank tables and sizes, held in registers
+  const uint32_t* __restrict__ ell = R.ell;
+  const int S = R.S, SA = R.SA, SB = R.SB, n_act = R.n_act;
+  const int2* __restrict__ act_ab = R.act_ab;
+  const double* __restrict__ act_L = R.act_L;
+  const double* __restrict__ act_EA = R.act_EA;
+  const double ea = n.ea;
+  const int2* __restrict__ send = R.send;
+  const uint32_t peer_pos = 8u * o.pos;  // byte offsets in a peer's dynamic SMEM
+  const uint32_t peer_slot = 8u * o.slot, peer_flag = 8u * o.flag;
 
   // the tree's combine program lives in SMEM (warp 0 walks it every iteration)
   const int n_ops = L > 0 ? L - 1 : 0;
-  int* lvl_s = S.prog;
+  int* prog = reinterpret_cast<int*>(g_smem) + o.prog;
+  int* lvl_s = prog;
   int* dst_s = lvl_s + n.n_levels + 1;
   int* lft_s = dst_s + n_ops;
   int* rgt_s = lft_s + n_ops;
@@ -736,7 +719,6 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
   const bool prof = b.phase_cycles != nullptr;
 
   // own DOF dl = t + k*T (local DOF; global DOF dof0 + dl)
-  auto has = [&](int k) { return t + k * T < nfo; };
   double u[MAXK], v[MAXK];
 #pragma unroll
   for (int k = 0; k < MAXK; ++k) u[k] = v[k] = 0.0;
@@ -757,17 +739,45 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
 
   // new position of own DOF dl: local slot + the halo copies of peers
   auto put_pos = [&](int dl, double x) {
-    pos[dl] = x;
+    g_smem[o.pos + dl] = x;
     if (C > 1) {
       const int node = dl / 3, axis = dl - 3 * node;
-      const int2 tg = __ldg(R.send + node);
+      const int2 tg = __ldg(send + node);
       if (tg.x >= 0) {
         const int qr = tg.x >> 24;
-        st_async(sc.peer_smem[qr] + off_pos + 8u * (3u * (tg.x & 0xffffff) + axis), x, sc.peer_bar_h[qr]);
+        st_async(sc.peer_smem[qr] + peer_pos + 8u * (3u * (tg.x & 0xffffff) + axis), x, sc.peer_bar_h[qr]);
       }
       if (tg.y >= 0) {
         const int qr = tg.y >> 24;
-        st_async(sc.peer_smem[qr] + off_pos + 8u * (3u * (tg.y & 0xffffff) + axis), x, sc.peer_bar_h[qr]);
+        st_async(sc.peer_smem[qr] + peer_pos + 8u * (3u * (tg.y & 0xffffff) + axis), x, sc.peer_bar_h[qr]);
+      }
+    }
+  };
+
+  // a = (-f)/m for every own DOF (f = g_smem[o.fprv + dl]), then use(k, dl, a)
+  // for the valid ones; divisions are issued together, rare exact fallback
+  auto accel = [&](auto use) {
+#pragma unroll
+    for (int k0 = 0; k0 < MAXK; k0 += kChunk) {
+      constexpr int KC = MAXK < kChunk ? MAXK : kChunk;
+      double a[KC];
+      bool ok[KC];
+#pragma unroll
+      for (int kk = 0; kk < KC; ++kk) {
+        const int dl = min(t + (k0 + kk) * T, dl_max);
+        a[kk] = frb_arith::div_fast(-g_smem[o.fprv + dl], __ldg(mass3 + dof0 + dl), ok[kk]);
+      }
+#pragma unroll
+      for (int kk = 0; kk < KC; ++kk) {
+        if (!ok[kk]) {
+          const int dl = min(t + (k0 + kk) * T, dl_max);
+          a[kk] = exact_div(-g_smem[o.fprv + dl], __ldg(mass3 + dof0 + dl));
+        }
+      }
+#pragma unroll
+      for (int kk = 0; kk < KC; ++kk) {
+        const int dl = t + (k0 + kk) * T;
+        if (k0 + kk < MAXK && dl < nfo) use(k0 + kk, dl, a[kk]);
       }
     }
   };
@@ -780,9 +790,9 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
   }
   for (int l = t; l < R.n_local; l += T) {
     const int g = l < n_own ? R.node0 + l : R.halo_g[l - n_own];
-    for (int a = 0; a < 3; ++a) pos[3 * l + a] = dadd(Xg[3 * g + a], 0.0);
+    for (int a = 0; a < 3; ++a) g_smem[o.pos + 3 * l + a] = dadd(Xg[3 * g + a], 0.0);
   }
-  set_local_fixed(n, R, pos, alpha, ramp);
+  set_local_fixed(n, R, &g_smem[o.pos], alpha, ramp);
   set_fixed_positions(n, rank, alpha, ramp);
   // initial free positions to global too (the all-element check reads posg)
   for (int l = t; l < n_own; l += T)
@@ -797,28 +807,19 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
     return;
   }
   // initial internal forces on own nodes (:413-420), kept as f_prev
-  element_coefs(R, n.ea, pos, cf);
+  element_coefs(n_act, act_ab, act_L, act_EA, ea, o.pos, o.cf);
   __syncthreads();
-  for (int i = t; i < n_own; i += T) {
-    double fx, fy, fz;
-    node_force_ell(R, cf, pos, i, fx, fy, fz);
-    fprv[3 * i] = fx;
-    fprv[3 * i + 1] = fy;
-    fprv[3 * i + 2] = fz;
-  }
+  node_forces(n_own, ell, S, SA, SB, o.pos, o.cf, o.fprv);
   __syncthreads();
   // a = -f/m (:428-430), then iteration 0's kick + drift (:443-448)
-  batched_div<MAXK>(
-      has, [&](int k) { return -fprv[t + k * T]; }, [&](int k) { return __ldg(mass3 + dof0 + t + k * T); },
-      [&](int k, double a) {
-        const int dl = t + k * T;
-        v[k] = dadd(0.0, dmul(hdt, a));
-        u[k] = dadd(0.0, dmul(dt, v[k]));
-        put_pos(dl, dadd(__ldg(Xg + dof0 + dl), u[k]));
-      });
+  accel([&](int k, int dl, double a) {
+    v[k] = dadd(0.0, dmul(hdt, a));
+    u[k] = dadd(0.0, dmul(dt, v[k]));
+    put_pos(dl, dadd(__ldg(Xg + dof0 + dl), u[k]));
+  });
   if (ramp) {  // iteration 0's ramp step (:449-453)
     alpha = ramp_alpha(1, ramp_n);
-    set_local_fixed(n, R, pos, alpha, ramp);
+    set_local_fixed(n, R, &g_smem[o.pos], alpha, ramp);
   }
   __syncthreads();
 
@@ -831,17 +832,11 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
       mb.ph_h ^= 1u;
     }
     // F: internal forces at the drifted positions (:456-465)
-    bool bad = element_coefs(R, n.ea, pos, cf);
+    bool bad = element_coefs(n_act, act_ab, act_L, act_EA, ea, o.pos, o.cf);
     if (ramp && it < ramp_n && rank == 0) bad |= check_elements(n, PosFixed{&n, alpha, ramp}, false);
     __syncthreads();
     mark(sc, prof, 0);
-    for (int i = t; i < n_own; i += T) {
-      double fx, fy, fz;
-      node_force_ell(R, cf, pos, i, fx, fy, fz);
-      fcur[3 * i] = fx;
-      fcur[3 * i + 1] = fy;
-      fcur[3 * i + 2] = fz;
-    }
+    node_forces(n_own, ell, S, SA, SB, o.pos, o.cf, o.fcur);
     if (bad) sc.singular = 1;
     __syncthreads();
     mark(sc, prof, 1);
@@ -851,20 +846,52 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
     // ff = f f (:489).  Outputs: sq -> own position slot, sq2 -> cf,
     // ff -> fcur, f -> fprv.
     if (C > 1 && t == 0) mbar_expect(mb.h, R.halo_bytes);  // next halo phase
-    batched_div<MAXK>(
-        has, [&](int k) { return dsub(fcur[t + k * T], fprv[t + k * T]); },
-        [&](int k) { return adaptive ? dmul(dt, v[k]) : 0.0; },
-        [&](int k, double kh) {
-          const int dl = t + k * T;
-          const double f = fcur[dl];
-          if (adaptive) {
-            kh = (kh > 0.0 || isnan(kh)) ? kh : 0.0;
-            pos[dl] = dmul(dmul(u[k], kh), u[k]);
-            cf[dl] = dmul(dmul(u[k], __ldg(mass3 + dof0 + dl)), u[k]);
+#pragma unroll
+    for (int k0 = 0; k0 < MAXK; k0 += kChunk) {
+      constexpr int KC = MAXK < kChunk ? MAXK : kChunk;
+      double f[KC], kh[KC], m[KC];
+      bool ok[KC];
+#pragma unroll
+      for (int kk = 0; kk < KC; ++kk) {
+        const int dl = min(t + (k0 + kk) * T, dl_max);
+        f[kk] = g_smem[o.fcur + dl];
+        kh[kk] = g_smem[o.fprv + dl];  // f_prev, until the quotient replaces it
+        m[kk] = __ldg(mass3 + dof0 + dl);
+      }
+      if (adaptive) {
+#pragma unroll
+        for (int kk = 0; kk < KC; ++kk) {
+          const double vk = k0 + kk < MAXK ? v[k0 + kk] : 0.0;
+          const double den = dmul(dt, vk);
+          const double num = dsub(f[kk], kh[kk]);
+          kh[kk] = frb_arith::div_fast(num, den, ok[kk]);
+          if (den == 0.0) {
+            kh[kk] = 0.0;
+            ok[kk] = true;
           }
-          fcur[dl] = dmul(f, f);
-          fprv[dl] = f;
-        });
+        }
+#pragma unroll
+        for (int kk = 0; kk < KC; ++kk) {
+          if (!ok[kk]) {
+            const int dl = min(t + (k0 + kk) * T, dl_max);
+            kh[kk] = exact_div(dsub(f[kk], g_smem[o.fprv + dl]), dmul(dt, v[k0 + kk]));
+          }
+        }
+      }
+#pragma unroll
+      for (int kk = 0; kk < KC; ++kk) {
+        const int k = k0 + kk, dl = t + k * T;
+        if (k < MAXK && dl < nfo) {
+          if (adaptive) {
+            const double khc = (kh[kk] > 0.0 || isnan(kh[kk])) ? kh[kk] : 0.0;
+            g_smem[o.pos + dl] = dmul(dmul(u[k], khc), u[k]);
+            g_smem[o.cf + dl] = dmul(dmul(u[k], m[kk]), u[k]);
+          }
+          g_smem[o.fcur + dl] = dmul(f[kk], f[kk]);
+          g_smem[o.fprv + dl] = f[kk];
+        }
+      }
+    }
     __syncthreads();
     mark(sc, prof, 2);
 
@@ -876,30 +903,30 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
       if (chain) {
         int dl = lstart + j;
         if (q > 0) {
-          r0 = pos[dl];
-          r1 = cf[dl];
-          r2 = fcur[dl];
+          r0 = g_smem[o.pos + dl];
+          r1 = g_smem[o.cf + dl];
+          r2 = g_smem[o.fcur + dl];
 #pragma unroll 4
           for (int k = 1; k < q; ++k) {
             dl += 8;
-            r0 = dadd(r0, pos[dl]);
-            r1 = dadd(r1, cf[dl]);
-            r2 = dadd(r2, fcur[dl]);
+            r0 = dadd(r0, g_smem[o.pos + dl]);
+            r1 = dadd(r1, g_smem[o.cf + dl]);
+            r2 = dadd(r2, g_smem[o.fcur + dl]);
           }
         }
         if (j < nt) {
           const int dtl = lstart + 8 * q + j;
-          t0 = pos[dtl];
-          t1 = cf[dtl];
-          t2 = fcur[dtl];
+          t0 = g_smem[o.pos + dtl];
+          t1 = g_smem[o.cf + dtl];
+          t2 = g_smem[o.fcur + dtl];
         }
         if (!adaptive) r0 = r1 = t0 = t1 = 0.0;
       }
 #pragma unroll
-      for (int o = 1; o < 8; o <<= 1) {
-        r0 = dadd(r0, __shfl_xor_sync(0xffffffffu, r0, o));
-        r1 = dadd(r1, __shfl_xor_sync(0xffffffffu, r1, o));
-        r2 = dadd(r2, __shfl_xor_sync(0xffffffffu, r2, o));
+      for (int sh = 1; sh < 8; sh <<= 1) {
+        r0 = dadd(r0, __shfl_xor_sync(0xffffffffu, r0, sh));
+        r1 = dadd(r1, __shfl_xor_sync(0xffffffffu, r1, sh));
+        r2 = dadd(r2, __shfl_xor_sync(0xffffffffu, r2, sh));
       }
       const int base = lane & ~7;
       const int my_nt = chain ? nt : 0;
@@ -915,23 +942,23 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
         }
       }
       if (chain && j == 0) {
-        const int s = 3 * (R.leaf0 + lloc);
-        slot[s] = r0;
-        slot[s + 1] = r1;
-        slot[s + 2] = r2;
+        const int sl = 3 * (R.leaf0 + lloc);
+        g_smem[o.slot + sl] = r0;
+        g_smem[o.slot + sl + 1] = r1;
+        g_smem[o.slot + sl + 2] = r2;
         for (int qr = 0; qr < C; ++qr) {
           if (qr == rank) continue;
-          const uint32_t a = sc.peer_smem[qr] + off_slot + 8u * s;
-          st_async(a, r0, sc.peer_bar_s[qr]);
-          st_async(a + 8, r1, sc.peer_bar_s[qr]);
-          st_async(a + 16, r2, sc.peer_bar_s[qr]);
+          const uint32_t ad = sc.peer_smem[qr] + peer_slot + 8u * sl;
+          st_async(ad, r0, sc.peer_bar_s[qr]);
+          st_async(ad + 8, r1, sc.peer_bar_s[qr]);
+          st_async(ad + 16, r2, sc.peer_bar_s[qr]);
         }
       }
     }
     if (C > 1 && t == 0) {
       const double fl = sc.singular ? 1.0 : 0.0;
       for (int qr = 0; qr < C; ++qr)
-        if (qr != rank) st_async(sc.peer_smem[qr] + off_flag + 8u * rank, fl, sc.peer_bar_s[qr]);
+        if (qr != rank) st_async(sc.peer_smem[qr] + peer_flag + 8u * rank, fl, sc.peer_bar_s[qr]);
     }
     __syncthreads();
     if (C > 1) {  // every peer's leaf sums and flag
@@ -942,14 +969,14 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
     mark(sc, prof, 3);
     bool singular = sc.singular != 0;
     if (C > 1)
-      for (int qr = 0; qr < C; ++qr) singular |= (qr != rank) && S.flag[qr] != 0.0;
+      for (int qr = 0; qr < C; ++qr) singular |= (qr != rank) && g_smem[o.flag + qr] != 0.0;
     if (singular) {
       if (C > 1) drain(mb, R);
       // positions of every node to global memory, then the argmin over all
       // elements (each rank redundantly; rank 0 reports)
 #pragma unroll
       for (int k = 0; k < MAXK; ++k)
-        if (has(k)) n.posg[dof0 + t + k * T] = dadd(__ldg(Xg + dof0 + t + k * T), u[k]);
+        if (t + k * T < nfo) n.posg[dof0 + t + k * T] = dadd(__ldg(Xg + dof0 + t + k * T), u[k]);
       set_fixed_positions(n, rank, alpha, ramp);
       csync(C);
       const int badi = singular_argmin(n, PosGlobalAll{n.posg}, sc);
@@ -959,6 +986,7 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
 
     // T: tree combine + scalar bookkeeping (warp 0 of every rank)
     if (t < 32) {
+      double* slot = &g_smem[o.slot];
       for (int lev = 0; lev < n.n_levels; ++lev) {
         const int k1 = lvl_s[lev + 1];
         for (int k = lvl_s[lev] + lane; k < k1; k += 32) {
@@ -1015,20 +1043,18 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
     // iteration's first half-kick and drift (:443-453) unless finished
     const double c = sc.c;
     const bool done = sc.done != 0;
-    batched_div<MAXK>(
-        has, [&](int k) { return -fprv[t + k * T]; }, [&](int k) { return __ldg(mass3 + dof0 + t + k * T); },
-        [&](int k, double fm) {
-          const double a = dsub(fm, dmul(c, v[k]));
-          v[k] = dadd(v[k], dmul(hdt, a));
-          if (!done) {
-            v[k] = dadd(v[k], dmul(hdt, a));
-            u[k] = dadd(u[k], dmul(dt, v[k]));
-            put_pos(t + k * T, dadd(__ldg(Xg + dof0 + t + k * T), u[k]));
-          }
-        });
+    accel([&](int k, int dl, double fm) {
+      const double a = dsub(fm, dmul(c, v[k]));
+      v[k] = dadd(v[k], dmul(hdt, a));
+      if (!done) {
+        v[k] = dadd(v[k], dmul(hdt, a));
+        u[k] = dadd(u[k], dmul(dt, v[k]));
+        put_pos(dl, dadd(__ldg(Xg + dof0 + dl), u[k]));
+      }
+    });
     if (!done && ramp && alpha < 1.0) {
       alpha = ramp_alpha(it + 2, ramp_n);
-      set_local_fixed(n, R, pos, alpha, ramp);
+      set_local_fixed(n, R, &g_smem[o.pos], alpha, ramp);
     }
     if (done) break;
     __syncthreads();
@@ -1042,10 +1068,11 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
   double* fo = b.f + 3 * n.node_base;
 #pragma unroll
   for (int k = 0; k < MAXK; ++k) {
-    if (has(k)) {
-      const int d = dof0 + t + k * T;
+    const int dl = t + k * T;
+    if (dl < nfo) {
+      const int d = dof0 + dl;
       uo[d] = u[k];
-      fo[d] = fprv[t + k * T];
+      fo[d] = g_smem[o.fprv + dl];
       n.posg[d] = dadd(__ldg(Xg + d), u[k]);  // x = X + u, all free nodes
     }
   }
@@ -1058,8 +1085,8 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
 
 template <int MAXK, int MAXT>
 __global__ void __launch_bounds__(MAXT, 1)
-    frb_relax_kernel(frb_batch b, frb_config cfg, int first, int count, int32_t* queue) {
-  extern __shared__ __align__(16) double smem[];
+    frb_relax_kernel(const __grid_constant__ frb_batch b, const __grid_constant__ frb_config cfg, int first,
+                     int count, int32_t* queue) {
   __shared__ Scalars sc;
   __shared__ Net net;
   __shared__ Rank rk;
@@ -1074,7 +1101,7 @@ __global__ void __launch_bounds__(MAXT, 1)
       mbar_init(&bars[1], 1);
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
       for (int q = 0; q < C; ++q) {
-        sc.peer_smem[q] = mapa(smem_u32(smem), q);
+        sc.peer_smem[q] = mapa(smem_u32(g_smem), q);
         sc.peer_bar_h[q] = mapa(smem_u32(&bars[0]), q);
         sc.peer_bar_s[q] = mapa(smem_u32(&bars[1]), q);
       }
@@ -1099,7 +1126,7 @@ __global__ void __launch_bounds__(MAXT, 1)
       sc.threshold = __longlong_as_double(0x7ff0000000000000ULL);  // +inf until set
     }
     __syncthreads();
-    solve_problem<MAXK>(b, cfg, p, rank, smem, sc, mb, net, rk);
+    solve_problem<MAXK>(b, cfg, p, rank, sc, mb, net, rk);
     csync(C);  // no rank reuses its SMEM before every peer is done with it
   }
   if (b.phase_cycles && threadIdx.x == 0) {
@@ -1109,7 +1136,7 @@ __global__ void __launch_bounds__(MAXT, 1)
 
 // One-shot forces for every node of problem blockIdx.x (reference
 // internal_forces, microsolver.py:221-238), same element math as the solver.
-__global__ void __launch_bounds__(256) frb_forces_kernel(frb_batch b, const double* __restrict__ u,
+__global__ void __launch_bounds__(256) frb_forces_kernel(const __grid_constant__ frb_batch b, const double* __restrict__ u,
                                                           double* __restrict__ f) {
   __shared__ Scalars sc;
   __shared__ Net n;

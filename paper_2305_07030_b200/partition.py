@@ -34,7 +34,6 @@ import numpy as np
 from .plan import PlanView
 
 MAX_SEND = 2
-ELL_PAD = 0xFFFFFFFF          # padding slot of the packed incidence table
 MAX_LOCAL = 0xFFFF            # local node ids and active-element ids are 16 bit
 
 
@@ -63,11 +62,22 @@ class RankTables:
 
     @property
     def ell(self) -> np.ndarray:
-        """Packed slot table for the device: (other << 16) | active index,
-        ELL_PAD on padding (uint32, same shape as ell_o)."""
+        """Packed slot table for the device: (other << 16) | active index
+        (uint32, same shape as ell_o).  A padding slot of own node i points
+        at i itself and at the element of i's first slot: its d is exactly
+        +0, so it adds a zero of either sign to the running sum.  The sums
+        start at +0 and round to nearest, so they are never -0 and adding
+        +-0 leaves them unchanged -- the gather needs no branch."""
         pad = self.ell_o < 0
+        n_own = self.n_own
         w = (self.ell_o.astype(np.int64) << 16) | self.ell_c.astype(np.int64)
-        w[pad] = ELL_PAD
+        if pad.any():
+            valid = ~pad[:, :n_own]
+            first = np.where(valid.any(axis=0), np.argmax(valid, axis=0), 0)
+            c_first = np.where(valid.any(axis=0), self.ell_c[first, np.arange(n_own)], 0)
+            self_w = (np.arange(n_own, dtype=np.int64) << 16) | c_first.astype(np.int64)
+            w[:, :n_own] = np.where(pad[:, :n_own], self_w[None, :], w[:, :n_own])
+            w[:, n_own:] = 0
         return w.astype(np.uint32)
 
     @property

@@ -85,10 +85,14 @@ def test_partition_tables(net, C):
         assert set(rt.act_elem) == act
         ends = np.concatenate([ia[rt.act_elem], ib[rt.act_elem]])
         assert list(rt.fix_g) == sorted(set(ends[ends >= NF].tolist()))   # fixed ends of active elements
-        w = rt.ell.astype(np.int64)
-        pad = rt.ell_o < 0
-        assert (w[pad] == 0xFFFFFFFF).all()
-        assert (w[~pad] >> 16 == rt.ell_o[~pad]).all() and (w[~pad] & 0xFFFF == rt.ell_c[~pad]).all()
+        w = rt.ell.astype(np.int64)[:, :rt.n_own]
+        pad = rt.ell_o[:, :rt.n_own] < 0
+        lo, lc = rt.ell_o[:, :rt.n_own], rt.ell_c[:, :rt.n_own]
+        assert (w[~pad] >> 16 == lo[~pad]).all() and (w[~pad] & 0xFFFF == lc[~pad]).all()
+        # padding points at the node itself (d = +0 exactly) and a real element of it
+        assert ((w >> 16)[pad] == np.nonzero(pad)[1]).all()
+        for k, i in zip(*np.nonzero(pad)):
+            assert (w[k, i] & 0xFFFF) in set(lc[~pad[:, i], i].tolist())
         for e, (a, b) in zip(rt.act_elem, rt.act_ab):
             assert (glob(a), glob(b)) == (ia[e], ib[e])
         for i in range(rt.n_own):
