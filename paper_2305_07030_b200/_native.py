@@ -15,7 +15,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "lib", "libfrb200.so")
 
-ABI_VERSION = 3
+ABI_VERSION = 4
 MAX_CLUSTER = 16
 FRB_OK, FRB_E_INVALID, FRB_E_TOO_LARGE, FRB_E_CUDA, FRB_E_UNSUPPORTED = 0, -1, -2, -3, -4
 STATUS_CONVERGED, STATUS_MAX_ITERS, STATUS_SINGULAR = 0, 1, 2
@@ -35,7 +35,7 @@ class FrbConfig(C.Structure):
 
 BATCH_POINTERS = ("groups", "problems", "parts", "order", "X", "dof_mass", "inc_node", "inc",
                   "elem_ab", "elem_L", "elem_EA", "plans", "ell", "act_ab", "act_L",
-                  "act_EA", "halo_g", "send", "fix_g", "u", "f", "work", "results", "queue",
+                  "act_EA", "halo_g", "send", "fix_g", "trees", "u", "f", "work", "results", "queue",
                   "phase_cycles")
 
 
@@ -54,21 +54,21 @@ PROBLEM_DTYPE = np.dtype([
 ])
 PART_DTYPE = np.dtype([
     ("ell_base", "<i8"), ("act_base", "<i8"), ("actv_off", "<i8"), ("halo_base", "<i8"),
-    ("send_base", "<i8"), ("fix_base", "<i8"),
+    ("send_base", "<i8"), ("fix_base", "<i8"), ("tree_base", "<i8"),
     ("node0", "<i4"), ("n_own", "<i4"), ("n_local", "<i4"), ("n_act", "<i4"),
     ("ell_stride", "<i4"), ("slots_a", "<i4"), ("slots_b", "<i4"), ("leaf0", "<i4"),
-    ("n_leaves", "<i4"), ("n_fix", "<i4"),
+    ("n_leaves", "<i4"), ("n_fix", "<i4"), ("tree_len", "<i4"), ("pad", "<i4"),
 ])
 GROUP_DTYPE = np.dtype([
     ("cluster", "<i4"), ("first", "<i4"), ("count", "<i4"), ("block_threads", "<i4"),
-    ("smem_bytes", "<i4"), ("max_own_dofs", "<i4"), ("grid_clusters", "<i4"), ("pad", "<i4"),
+    ("smem_bytes", "<i4"), ("max_own_dofs", "<i4"), ("grid_clusters", "<i4"), ("fprv_global", "<i4"),
 ])
 RESULT_DTYPE = np.dtype([
     ("status", "<i4"), ("iters", "<i4"), ("bad_element", "<i4"), ("converged", "<i4"),
     ("final_residual", "<f8"), ("r_ref", "<f8"), ("energy_residual", "<f8"),
     ("avg_stress", "<f8", (9,)), ("energy", "<f8", (4,)),
 ])
-assert PROBLEM_DTYPE.itemsize == 168 and PART_DTYPE.itemsize == 88
+assert PROBLEM_DTYPE.itemsize == 168 and PART_DTYPE.itemsize == 104
 assert GROUP_DTYPE.itemsize == 32 and RESULT_DTYPE.itemsize == 144
 
 
@@ -94,7 +94,7 @@ def lib() -> C.CDLL:
     h.frb_last_error.restype = C.c_char_p
     h.frb_device_info.argtypes = [C.c_int] + [C.POINTER(C.c_int)] * 4
     h.frb_rank_smem_bytes.restype = C.c_int64
-    h.frb_rank_smem_bytes.argtypes = [C.c_int32] * 4
+    h.frb_rank_smem_bytes.argtypes = [C.c_int32] * 6
     h.frb_max_dofs_per_thread.argtypes = [C.c_int]
     h.frb_solve_batch.argtypes = [C.POINTER(FrbBatch), C.POINTER(FrbConfig), C.c_void_p]
     h.frb_internal_forces.argtypes = [C.POINTER(FrbBatch), C.c_void_p, C.c_void_p, C.c_void_p]

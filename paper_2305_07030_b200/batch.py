@@ -42,7 +42,7 @@ from .microsolver import (
 )
 from .network import AffineBC, FiberNetwork
 from .packed import PackedStorage
-from .partition import MAX_SEND, Partition, partition, rank_smem_bytes
+from .partition import MAX_SEND, Partition, partition, partition_smem_bytes
 from .plan import reduction_plan
 
 __all__ = ["Batch", "DeviceBatch", "ExecutionStrategy", "NaiveLoop", "SerialReference",
@@ -121,17 +121,19 @@ class Topology:
                                       self.slots_a, self.slots_b, self.plan, C)
         return self.parts[C]
 
-    def choose_cluster(self) -> Partition:
+    def choose_cluster(self) -> tuple[Partition, bool]:
         """Smallest cluster with at most DOFS_PER_RANK free DOFs per rank whose
-        ranks fit the SMEM budget (more ranks if SMEM demands it)."""
+        ranks fit the SMEM budget (more ranks if SMEM demands it), and whether
+        f_prev must live in global memory instead of SMEM to fit."""
         nf = 3 * self.n_free_nodes
         want = max(1, math.ceil(nf / DOFS_PER_RANK))
         for C in CLUSTER_SIZES:
             if C < want and C != CLUSTER_SIZES[-1]:
                 continue
             part = self.partition(C)
-            if max(rank_smem_bytes(r, self.n_leaves) for r in part.ranks) <= SMEM_BUDGET:
-                return part
+            for fprv_global in (False, True):
+                if partition_smem_bytes(part, fprv_global) <= SMEM_BUDGET:
+                    return part, fprv_global
         raise nat.NativeError(nat.FRB_E_TOO_LARGE,
                               f"network with {nf} free DOFs does not fit a {CLUSTER_SIZES[-1]}-CTA cluster")
 
@@ -288,7 +290,8 @@ def _cat(parts, dtype, width=None):
     return np.ascontiguousarray(np.concatenate(parts).astype(dtype, copy=False))
 
 
-def _group_threads(max_own_dofs: int, max_rank_leaves: int, n_problems: int, cluster: int) -> int:
+def _group_threads(max_own_dofs: int, max_rank_leaves: int, n_problems: int, cluster: int,
+                   fprv_global: bool = False) -> int:
     """Threads per CTA for a group: 8 per pairwise leaf at least, few enough
     DOFs per thread for the register budget; more threads when there are too
     few problems to fill the GPU (latency), fewer when many small problems
@@ -296,6 +299,8 @@ def _group_threads(max_own_dofs: int, max_rank_leaves: int, n_problems: int, clu
     need = max(64, 8 * max_rank_leaves, math.ceil(max_own_dofs / 16))
     if max_own_dofs > 1024 or n_problems * cluster < 148:
         need = max(need, min(512, 32 * math.ceil(max_own_dofs / 32)))
+    if fprv_global:  # the global-f_prev kernels exist for 768 and 1024 threads
+        need = max(need, 768)
     threads = min(MAX_CTA_THREADS, 32 * math.ceil(need / 32))
     while max_own_dofs > dofs_per_thread_cap(threads) * threads and threads < MAX_CTA_THREADS:
         threads += 32
@@ -309,17 +314,18 @@ def _pack(networks, bcs, probs, cluster: int | None = None) -> Batch:
     plan_slot: dict[int, int] = {}
     shared_slot: dict[tuple, list] = {}       # (topo, C) -> per-rank base offsets
     topo_slot: dict[bytes, int] = {}
-    inc, plans, ell, act_ab, halo_g, send, fix_g = [], [], [], [], [], [], []
-    n_inc = n_plan = n_ell = n_act = n_halo = n_send = n_fix = 0
+    inc, plans, ell, act_ab, halo_g, send, fix_g, trees = [], [], [], [], [], [], [], []
+    n_inc = n_plan = n_ell = n_act = n_halo = n_send = n_fix = n_tree = 0
     X, mass, EL, EA, inc_node, elem_ab, act_L, act_EA = [], [], [], [], [], [], [], []
     parts_rows = []
     elem_base = actv_base = 0
     any_nonuniform = False
-    part_of = []
+    part_of, fglob_of = [], []
     for i, p in enumerate(probs):
         t = p.topo
-        part = t.partition(cluster) if cluster else t.choose_cluster()
+        part, fglob = (t.partition(cluster), False) if cluster else t.choose_cluster()
         part_of.append(part)
+        fglob_of.append(fglob)
         if p.topo_key not in topo_slot:
             topo_slot[p.topo_key] = n_inc
             inc.append(t.inc)
@@ -328,7 +334,9 @@ def _pack(networks, bcs, probs, cluster: int | None = None) -> Batch:
         if key not in shared_slot:
             bases = []
             for rt in part.ranks:
-                bases.append((n_ell, n_act, n_halo, n_send, n_fix))
+                bases.append((n_ell, n_act, n_halo, n_send, n_fix, n_tree))
+                trees.append(rt.tree)
+                n_tree += len(rt.tree)
                 ell.append(rt.ell.reshape(-1))
                 act_ab.append(rt.act_ab)
                 halo_g.append(rt.halo_g)
@@ -366,11 +374,12 @@ def _pack(networks, bcs, probs, cluster: int | None = None) -> Batch:
         d["ea"] = ea[0] if ea.size else 0.0
         d["F"] = p.F.reshape(9)
         off = 0
-        for rt, (b_ell, b_act, b_halo, b_send, b_fix) in zip(part.ranks, shared_slot[key]):
+        for rt, (b_ell, b_act, b_halo, b_send, b_fix, b_tree) in zip(part.ranks, shared_slot[key]):
             row = np.zeros((), dtype=nat.PART_DTYPE)
             row["ell_base"], row["act_base"], row["actv_off"] = b_ell, b_act, off
             row["halo_base"], row["send_base"], row["fix_base"] = b_halo, b_send, b_fix
             row["n_fix"] = rt.n_fix
+            row["tree_base"], row["tree_len"] = b_tree, len(rt.tree)
             row["node0"], row["n_own"], row["n_local"], row["n_act"] = rt.node0, rt.n_own, rt.n_local, rt.n_act
             row["ell_stride"], row["slots_a"], row["slots_b"] = rt.stride, part.slots_a, part.slots_b
             row["leaf0"], row["n_leaves"] = rt.leaf0, rt.n_leaves
@@ -391,16 +400,17 @@ def _pack(networks, bcs, probs, cluster: int | None = None) -> Batch:
     parts = np.array(parts_rows, dtype=nat.PART_DTYPE) if parts_rows else np.zeros(0, nat.PART_DTYPE)
     # launch groups by cluster size, longest problems first inside a group
     order, groups = [], []
-    for C in sorted({pt.C for pt in part_of}):
-        ids = [i for i in range(P) if part_of[i].C == C]
+    for C, fglob in sorted({(pt.C, fg) for pt, fg in zip(part_of, fglob_of)}):
+        ids = [i for i in range(P) if part_of[i].C == C and fglob_of[i] == fglob]
         ids.sort(key=lambda i: -probs[i].n_nodes)
-        smem = max(rank_smem_bytes(rt, probs[i].topo.n_leaves) for i in ids for rt in part_of[i].ranks)
+        smem = max(partition_smem_bytes(part_of[i], fglob) for i in ids)
         own = max(3 * rt.n_own for i in ids for rt in part_of[i].ranks)
         leaves = max(rt.n_leaves for i in ids for rt in part_of[i].ranks)
         g = np.zeros((), dtype=nat.GROUP_DTYPE)
         g["cluster"], g["first"], g["count"] = C, len(order), len(ids)
-        g["block_threads"] = _group_threads(own, leaves, len(ids), C)
+        g["block_threads"] = _group_threads(own, leaves, len(ids), C, fglob)
         g["smem_bytes"], g["max_own_dofs"] = smem, own
+        g["fprv_global"] = int(fglob)
         groups.append(g)
         order.extend(ids)
     arrays = dict(
@@ -410,7 +420,7 @@ def _pack(networks, bcs, probs, cluster: int | None = None) -> Batch:
         elem_EA=_cat(EA, np.float64), plans=_cat(plans, np.int32),
         ell=_cat(ell, np.uint32).view(np.int32), fix_g=_cat(fix_g, np.int32),
         act_ab=_cat(act_ab, np.int32, 2), act_L=_cat(act_L, np.float64),
-        halo_g=_cat(halo_g, np.int32), send=_cat(send, np.int32, MAX_SEND),
+        halo_g=_cat(halo_g, np.int32), send=_cat(send, np.int32, MAX_SEND), trees=_cat(trees, np.int32),
         order=np.asarray(order, dtype=np.int32),
         problems=desc.view(np.uint8).copy(), parts=parts.view(np.uint8).copy(),
     )
@@ -500,7 +510,7 @@ class DeviceBatch:
         fb.groups = groups_c.ctypes.data
         t = self.t
         for k in ("parts", "order", "X", "dof_mass", "inc_node", "inc", "elem_ab", "elem_L", "elem_EA",
-                  "plans", "ell", "act_ab", "act_L", "act_EA", "halo_g", "send", "fix_g"):
+                  "plans", "ell", "act_ab", "act_L", "act_EA", "halo_g", "send", "fix_g", "trees"):
             setattr(fb, k, t[k].data_ptr() if k in t and t[k].numel() else None)
         fb.problems = desc_t.data_ptr()
         fb.u, fb.f, fb.work = u.data_ptr(), f.data_ptr(), work.data_ptr()

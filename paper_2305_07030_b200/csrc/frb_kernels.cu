@@ -162,7 +162,10 @@ struct Rank {
   int node0, n_own, n_local, n_fix, n_act;
   int S, SA, SB, leaf0, n_leaves;
   int PN, NFO, CF;  // uniform SMEM extents of the problem (max over ranks)
+  int LS, TS, PI;   // tree: local slots, top slots, block words (uniform)
+  int tree_len, n_exp, root_top;
   uint32_t halo_bytes, leaf_bytes;  // transaction bytes this rank receives per phase
+  const int* tree;
   const uint32_t* ell;
   const int2* act_ab;
   const double* act_L;
@@ -209,8 +212,15 @@ __device__ void load_views(Net& n, Rank& R, const frb_batch& b, int p, int r) {
   R.SB = Q.slots_b;
   R.leaf0 = Q.leaf0;
   R.n_leaves = Q.n_leaves;
+  R.tree = b.trees + Q.tree_base;
+  R.tree_len = Q.tree_len;
+  R.LS = R.tree[0];
+  R.TS = R.tree[1];
+  R.PI = R.tree[2];
+  R.n_exp = R.tree[6];
+  R.root_top = R.tree[7];
   R.halo_bytes = 24u * static_cast<uint32_t>(Q.n_local - Q.n_own);
-  R.leaf_bytes = 24u * static_cast<uint32_t>(n.L - Q.n_leaves) + 8u * static_cast<uint32_t>(n.C - 1);
+  R.leaf_bytes = 24u * static_cast<uint32_t>(R.tree[8] - R.n_exp) + 8u * static_cast<uint32_t>(n.C - 1);
   // uniform extents: maxima over the problem's ranks
   R.PN = R.NFO = R.CF = 0;
   for (int q = 0; q < n.C; ++q) {
@@ -637,19 +647,43 @@ __device__ __forceinline__ void write_singular(const frb_batch& b, int p, int ba
 // SMEM layout of a problem, in doubles from g_smem (identical on every
 // rank of the problem, so a peer's buffer is addressed by the same offset).
 struct Layout {
-  int pos, fcur, fprv, cf, slot, flag, prog;  // prog: int32 index
+  int pos, fcur, fprv, cf, lslot, tslot, flag, prog;  // prog: int32 index
 };
 
-__device__ __forceinline__ Layout layout(const Net& n, const Rank& R) {
+template <bool kFG>
+__device__ __forceinline__ Layout layout(const Rank& R) {
   Layout o;
   o.pos = 0;
   o.fcur = 3 * R.PN;
   o.fprv = o.fcur + R.NFO;
-  o.cf = o.fprv + R.NFO;
-  o.slot = o.cf + R.CF;
-  o.flag = o.slot + 3 * (n.L > 0 ? 2 * n.L - 1 : 1);
+  o.cf = o.fprv + (kFG ? 0 : R.NFO);
+  o.lslot = o.cf + R.CF;
+  o.tslot = o.lslot + 3 * R.LS;
+  o.flag = o.tslot + 3 * R.TS;
   o.prog = 2 * (o.flag + 16);
   return o;
+}
+
+// Replay one combine program (plan.py _program layout) on slot array
+// g_smem[o_slot + 3 s + {0,1,2}] with the calling warp; ops of a level are
+// independent, one lane per op.
+__device__ __forceinline__ void run_prog(const int* prog, int o_slot, int lane) {
+  const int nlev = prog[0];
+  const int* off = prog + 1;
+  const int K = off[nlev];
+  const int* dst = prog + nlev + 2;
+  const int* lf = dst + K;
+  const int* rt = lf + K;
+  for (int lev = 0; lev < nlev; ++lev) {
+    const int k1 = off[lev + 1];
+    for (int k = off[lev] + lane; k < k1; k += 32) {
+      const int d = o_slot + 3 * dst[k], a = o_slot + 3 * lf[k], c = o_slot + 3 * rt[k];
+      g_smem[d] = dadd(g_smem[a], g_smem[c]);
+      g_smem[d + 1] = dadd(g_smem[a + 1], g_smem[c + 1]);
+      g_smem[d + 2] = dadd(g_smem[a + 2], g_smem[c + 2]);
+    }
+    __syncwarp();
+  }
 }
 
 struct Mbar {
@@ -671,12 +705,12 @@ __device__ __forceinline__ void drain(Mbar& mb, const Rank& R) {
   mb.ph_s ^= 1u;
 }
 
-template <int MAXK>
+template <int MAXK, bool kFG>
 __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, int rank, Scalars& sc, Mbar& mb,
                               const Net& n, const Rank& R) {
   const int T = blockDim.x, t = threadIdx.x, lane = t & 31;
   const int C = n.C, L = n.L, n_own = R.n_own, nfo = 3 * n_own;
-  const Layout o = layout(n, R);
+  const Layout o = layout<kFG>(R);
   const double* __restrict__ Xg = n.X;
   const double* __restrict__ mass3 = n.mass3;
   const int dof0 = 3 * R.node0;
@@ -690,25 +724,19 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
   const double ea = n.ea;
   const int2* __restrict__ send = R.send;
   const uint32_t peer_pos = 8u * o.pos;  // byte offsets in a peer's dynamic SMEM
-  const uint32_t peer_slot = 8u * o.slot, peer_flag = 8u * o.flag;
+  const uint32_t peer_tslot = 8u * o.tslot, peer_flag = 8u * o.flag;
+  // f_prev of own DOF dl: SMEM, or the `f` output array for networks too
+  // large for the cluster's SMEM (it ends up holding the final f either way)
+  double* const fprv_g = b.f + 3 * n.node_base + dof0;
+  auto FPRV = [&](int dl) -> double& { return kFG ? fprv_g[dl] : g_smem[o.fprv + dl]; };
 
-  // the tree's combine program lives in SMEM (warp 0 walks it every iteration)
-  const int n_ops = L > 0 ? L - 1 : 0;
-  int* prog = reinterpret_cast<int*>(g_smem) + o.prog;
-  int* lvl_s = prog;
-  int* dst_s = lvl_s + n.n_levels + 1;
-  int* lft_s = dst_s + n_ops;
-  int* rgt_s = lft_s + n_ops;
-  {
-    const int* level_off = n.plan + 4 + 2 * L;
-    const int* op = level_off + n.n_levels + 1;
-    for (int k = t; k <= n.n_levels; k += T) lvl_s[k] = level_off[k];
-    for (int k = t; k < n_ops; k += T) {
-      dst_s[k] = op[k];
-      lft_s[k] = op[n_ops + k];
-      rgt_s[k] = op[2 * n_ops + k];
-    }
-  }
+  // the rank's tree block (local + top programs, exports) lives in SMEM
+  int* const prog = reinterpret_cast<int*>(g_smem) + o.prog;
+  for (int k = t; k < R.tree_len; k += T) prog[k] = __ldg(R.tree + k);
+  const int* const lprog = prog + R.tree[3];
+  const int* const tprog = prog + R.tree[4];
+  const int* const exps = prog + R.tree[5];
+  const int n_exp = R.n_exp, root_top = R.root_top;
 
   const bool adaptive = cfg.damping == FRB_DAMPING_ADAPTIVE;
   const int ramp_n = cfg.bc_ramp_iters;
@@ -765,13 +793,13 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
 #pragma unroll
       for (int kk = 0; kk < KC; ++kk) {
         const int dl = min(t + (k0 + kk) * T, dl_max);
-        a[kk] = frb_arith::div_fast(-g_smem[o.fprv + dl], __ldg(mass3 + dof0 + dl), ok[kk]);
+        a[kk] = frb_arith::div_fast(-FPRV(dl), __ldg(mass3 + dof0 + dl), ok[kk]);
       }
 #pragma unroll
       for (int kk = 0; kk < KC; ++kk) {
         if (!ok[kk]) {
           const int dl = min(t + (k0 + kk) * T, dl_max);
-          a[kk] = exact_div(-g_smem[o.fprv + dl], __ldg(mass3 + dof0 + dl));
+          a[kk] = exact_div(-FPRV(dl), __ldg(mass3 + dof0 + dl));
         }
       }
 #pragma unroll
@@ -809,7 +837,9 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
   // initial internal forces on own nodes (:413-420), kept as f_prev
   element_coefs(n_act, act_ab, act_L, act_EA, ea, o.pos, o.cf);
   __syncthreads();
-  node_forces(n_own, ell, S, SA, SB, o.pos, o.cf, o.fprv);
+  node_forces(n_own, ell, S, SA, SB, o.pos, o.cf, o.fcur);
+  __syncthreads();
+  for (int dl = t; dl < nfo; dl += T) FPRV(dl) = g_smem[o.fcur + dl];
   __syncthreads();
   // a = -f/m (:428-430), then iteration 0's kick + drift (:443-448)
   accel([&](int k, int dl, double a) {
@@ -855,7 +885,7 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
       for (int kk = 0; kk < KC; ++kk) {
         const int dl = min(t + (k0 + kk) * T, dl_max);
         f[kk] = g_smem[o.fcur + dl];
-        kh[kk] = g_smem[o.fprv + dl];  // f_prev, until the quotient replaces it
+        kh[kk] = FPRV(dl);  // f_prev, until the quotient replaces it
         m[kk] = __ldg(mass3 + dof0 + dl);
       }
       if (adaptive) {
@@ -874,7 +904,7 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
         for (int kk = 0; kk < KC; ++kk) {
           if (!ok[kk]) {
             const int dl = min(t + (k0 + kk) * T, dl_max);
-            kh[kk] = exact_div(dsub(f[kk], g_smem[o.fprv + dl]), dmul(dt, v[k0 + kk]));
+            kh[kk] = exact_div(dsub(f[kk], FPRV(dl)), dmul(dt, v[k0 + kk]));
           }
         }
       }
@@ -888,7 +918,7 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
             g_smem[o.cf + dl] = dmul(dmul(u[k], m[kk]), u[k]);
           }
           g_smem[o.fcur + dl] = dmul(f[kk], f[kk]);
-          g_smem[o.fprv + dl] = f[kk];
+          FPRV(dl) = f[kk];
         }
       }
     }
@@ -942,35 +972,94 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
         }
       }
       if (chain && j == 0) {
-        const int sl = 3 * (R.leaf0 + lloc);
-        g_smem[o.slot + sl] = r0;
-        g_smem[o.slot + sl + 1] = r1;
-        g_smem[o.slot + sl + 2] = r2;
+        const int sl = o.lslot + 3 * lloc;  // local leaf lloc
+        g_smem[sl] = r0;
+        g_smem[sl + 1] = r1;
+        g_smem[sl + 2] = r2;
+      }
+    }
+    __syncthreads();
+    mark(sc, prof, 3);
+
+    // T (warp 0): local subtrees of this rank's leaves, their roots to every
+    // rank (with this rank's singular flag), the top tree over all ranks'
+    // exports, then the scalar bookkeeping
+    if (t < 32) {
+      run_prog(lprog, o.lslot, lane);
+      for (int x = lane; x < n_exp; x += 32) {
+        const int ls = o.lslot + 3 * exps[2 * x], ts = 3 * exps[2 * x + 1];
+        const double v0 = g_smem[ls], v1 = g_smem[ls + 1], v2 = g_smem[ls + 2];
+        g_smem[o.tslot + ts] = v0;
+        g_smem[o.tslot + ts + 1] = v1;
+        g_smem[o.tslot + ts + 2] = v2;
         for (int qr = 0; qr < C; ++qr) {
           if (qr == rank) continue;
-          const uint32_t ad = sc.peer_smem[qr] + peer_slot + 8u * sl;
-          st_async(ad, r0, sc.peer_bar_s[qr]);
-          st_async(ad + 8, r1, sc.peer_bar_s[qr]);
-          st_async(ad + 16, r2, sc.peer_bar_s[qr]);
+          const uint32_t ad = sc.peer_smem[qr] + peer_tslot + 8u * ts;
+          st_async(ad, v0, sc.peer_bar_s[qr]);
+          st_async(ad + 8, v1, sc.peer_bar_s[qr]);
+          st_async(ad + 16, v2, sc.peer_bar_s[qr]);
+        }
+      }
+      if (C > 1) {
+        if (lane == 0) {
+          const double fl = sc.singular ? 1.0 : 0.0;
+          for (int qr = 0; qr < C; ++qr)
+            if (qr != rank) st_async(sc.peer_smem[qr] + peer_flag + 8u * rank, fl, sc.peer_bar_s[qr]);
+        }
+        mbar_wait(mb.s, mb.ph_s);  // every peer's exports and flag
+        if (lane == 0) mbar_expect(mb.s, R.leaf_bytes);  // next exchange phase
+      }
+      __syncwarp();
+      bool singular = sc.singular != 0;
+      for (int qr = 0; qr < C; ++qr) singular |= (qr != rank) && g_smem[o.flag + qr] != 0.0;
+      if (!singular) run_prog(tprog, o.tslot, lane);
+      if (t == 0) {
+        if (singular) {
+          sc.singular = 1;
+        } else {
+          double s_sq = 0.0, s_m = 0.0, s_f = 0.0;
+          if (root_top >= 0) {
+            s_sq = g_smem[o.tslot + 3 * root_top];
+            s_m = g_smem[o.tslot + 3 * root_top + 1];
+            s_f = g_smem[o.tslot + 3 * root_top + 2];
+          }
+          // np.sum adds the pairwise result to the identity 0.0
+          s_sq = dadd(0.0, s_sq);
+          s_m = dadd(0.0, s_m);
+          s_f = dadd(0.0, s_f);
+          double c = cfg.damping_c;
+          if (adaptive) {
+            if (s_m > 0.0) {
+              const double lam = ddiv(s_sq, s_m);
+              c = lam > 0.0 ? dmul(2.0, dsqrt(lam)) : 0.0;
+            } else {
+              c = 0.0;
+            }
+          }
+          const double res = dsqrt(s_f);
+          if (it == full_bc_iter) {
+            sc.r_ref = res;
+            const double th = dmul(cfg.tol_rel, res);
+            sc.threshold = th > cfg.tol_abs ? th : cfg.tol_abs;  // max(tol_abs, .)
+          }
+          int done = 0, conv = 0;
+          if (it >= full_bc_iter && res <= sc.threshold) {
+            done = 1;
+            conv = 1;
+          } else if (it + 1 >= cfg.max_iters) {
+            done = 1;
+          }
+          sc.c = c;
+          sc.residual = res;
+          sc.done = done;
+          sc.converged = conv;
         }
       }
     }
-    if (C > 1 && t == 0) {
-      const double fl = sc.singular ? 1.0 : 0.0;
-      for (int qr = 0; qr < C; ++qr)
-        if (qr != rank) st_async(sc.peer_smem[qr] + peer_flag + 8u * rank, fl, sc.peer_bar_s[qr]);
-    }
+    mb.ph_s ^= 1u;
     __syncthreads();
-    if (C > 1) {  // every peer's leaf sums and flag
-      mbar_wait(mb.s, mb.ph_s);
-      mb.ph_s ^= 1u;
-      if (t == 0) mbar_expect(mb.s, R.leaf_bytes);  // next leaf-sum phase
-    }
-    mark(sc, prof, 3);
-    bool singular = sc.singular != 0;
-    if (C > 1)
-      for (int qr = 0; qr < C; ++qr) singular |= (qr != rank) && g_smem[o.flag + qr] != 0.0;
-    if (singular) {
+    mark(sc, prof, 4);
+    if (sc.singular) {
       if (C > 1) drain(mb, R);
       // positions of every node to global memory, then the argmin over all
       // elements (each rank redundantly; rank 0 reports)
@@ -983,61 +1072,6 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
       if (rank == 0 && t == 0) write_singular(b, p, badi, it);
       return;
     }
-
-    // T: tree combine + scalar bookkeeping (warp 0 of every rank)
-    if (t < 32) {
-      double* slot = &g_smem[o.slot];
-      for (int lev = 0; lev < n.n_levels; ++lev) {
-        const int k1 = lvl_s[lev + 1];
-        for (int k = lvl_s[lev] + lane; k < k1; k += 32) {
-          const int dd = dst_s[k], la = lft_s[k], rb = rgt_s[k];
-          slot[3 * dd] = dadd(slot[3 * la], slot[3 * rb]);
-          slot[3 * dd + 1] = dadd(slot[3 * la + 1], slot[3 * rb + 1]);
-          slot[3 * dd + 2] = dadd(slot[3 * la + 2], slot[3 * rb + 2]);
-        }
-        __syncwarp();
-      }
-      if (t == 0) {
-        double s_sq = 0.0, s_m = 0.0, s_f = 0.0;
-        if (L > 0) {
-          s_sq = slot[3 * n.root];
-          s_m = slot[3 * n.root + 1];
-          s_f = slot[3 * n.root + 2];
-        }
-        // np.sum adds the pairwise result to the identity 0.0
-        s_sq = dadd(0.0, s_sq);
-        s_m = dadd(0.0, s_m);
-        s_f = dadd(0.0, s_f);
-        double c = cfg.damping_c;
-        if (adaptive) {
-          if (s_m > 0.0) {
-            const double lam = ddiv(s_sq, s_m);
-            c = lam > 0.0 ? dmul(2.0, dsqrt(lam)) : 0.0;
-          } else {
-            c = 0.0;
-          }
-        }
-        const double res = dsqrt(s_f);
-        if (it == full_bc_iter) {
-          sc.r_ref = res;
-          const double th = dmul(cfg.tol_rel, res);
-          sc.threshold = th > cfg.tol_abs ? th : cfg.tol_abs;  // max(tol_abs, .)
-        }
-        int done = 0, conv = 0;
-        if (it >= full_bc_iter && res <= sc.threshold) {
-          done = 1;
-          conv = 1;
-        } else if (it + 1 >= cfg.max_iters) {
-          done = 1;
-        }
-        sc.c = c;
-        sc.residual = res;
-        sc.done = done;
-        sc.converged = conv;
-      }
-    }
-    __syncthreads();
-    mark(sc, prof, 4);
 
     // U: accelerations and second half-kick (:501-507); then the next
     // iteration's first half-kick and drift (:443-453) unless finished
@@ -1072,7 +1106,7 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
     if (dl < nfo) {
       const int d = dof0 + dl;
       uo[d] = u[k];
-      fo[d] = g_smem[o.fprv + dl];
+      if (!kFG) fo[d] = g_smem[o.fprv + dl];
       n.posg[d] = dadd(__ldg(Xg + d), u[k]);  // x = X + u, all free nodes
     }
   }
@@ -1083,7 +1117,7 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
   mark(sc, prof, 6);
 }
 
-template <int MAXK, int MAXT>
+template <int MAXK, int MAXT, bool kFG>
 __global__ void __launch_bounds__(MAXT, 1)
     frb_relax_kernel(const __grid_constant__ frb_batch b, const __grid_constant__ frb_config cfg, int first,
                      int count, int32_t* queue) {
@@ -1126,7 +1160,7 @@ __global__ void __launch_bounds__(MAXT, 1)
       sc.threshold = __longlong_as_double(0x7ff0000000000000ULL);  // +inf until set
     }
     __syncthreads();
-    solve_problem<MAXK>(b, cfg, p, rank, sc, mb, net, rk);
+    solve_problem<MAXK, kFG>(b, cfg, p, rank, sc, mb, net, rk);
     csync(C);  // no rank reuses its SMEM before every peer is done with it
   }
   if (b.phase_cycles && threadIdx.x == 0) {
@@ -1196,10 +1230,10 @@ int cuda_check(cudaError_t e, const char* where) {
 
 int dofs_cap(int threads) { return threads > 768 ? 8 : threads > 512 ? 12 : 16; }
 
-template <int MAXK, int MAXT>
+template <int MAXK, int MAXT, bool kFG>
 int launch_group(const frb_batch* batch, const frb_config* cfg, const frb_group& g, int32_t* queue,
                  cudaStream_t s) {
-  auto kern = frb_relax_kernel<MAXK, MAXT>;
+  auto kern = frb_relax_kernel<MAXK, MAXT, kFG>;
   const int C = g.cluster;
   int rc = cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, g.smem_bytes),
                       "cudaFuncSetAttribute(smem)");
@@ -1239,18 +1273,30 @@ int launch_group(const frb_batch* batch, const frb_config* cfg, const frb_group&
 template <int MAXT>
 int dispatch_k(const frb_batch* batch, const frb_config* cfg, const frb_group& g, int32_t* queue,
                cudaStream_t s, int k) {
-  if (k <= 1) return launch_group<1, MAXT>(batch, cfg, g, queue, s);
-  if (k <= 2) return launch_group<2, MAXT>(batch, cfg, g, queue, s);
-  if (k <= 4) return launch_group<4, MAXT>(batch, cfg, g, queue, s);
-  if (k <= 6) return launch_group<6, MAXT>(batch, cfg, g, queue, s);
-  if (k <= 8) return launch_group<8, MAXT>(batch, cfg, g, queue, s);
+  if (g.fprv_global) {  // large networks: CTAs of 768 / 1024 threads, >= 4 DOFs per thread
+    if constexpr (MAXT >= 768) {
+      if (k <= 4) return launch_group<4, MAXT, true>(batch, cfg, g, queue, s);
+      if (k <= 6) return launch_group<6, MAXT, true>(batch, cfg, g, queue, s);
+      if (k <= 8) return launch_group<8, MAXT, true>(batch, cfg, g, queue, s);
+      if constexpr (MAXT <= 768) {
+        if (k <= 10) return launch_group<10, MAXT, true>(batch, cfg, g, queue, s);
+        if (k <= 12) return launch_group<12, MAXT, true>(batch, cfg, g, queue, s);
+      }
+    }
+    return set_err(FRB_E_INVALID, "fprv_global groups need 513..1024 threads per CTA");
+  }
+  if (k <= 1) return launch_group<1, MAXT, false>(batch, cfg, g, queue, s);
+  if (k <= 2) return launch_group<2, MAXT, false>(batch, cfg, g, queue, s);
+  if (k <= 4) return launch_group<4, MAXT, false>(batch, cfg, g, queue, s);
+  if (k <= 6) return launch_group<6, MAXT, false>(batch, cfg, g, queue, s);
+  if (k <= 8) return launch_group<8, MAXT, false>(batch, cfg, g, queue, s);
   if constexpr (MAXT <= 768) {
-    if (k <= 10) return launch_group<10, MAXT>(batch, cfg, g, queue, s);
-    if (k <= 12) return launch_group<12, MAXT>(batch, cfg, g, queue, s);
+    if (k <= 10) return launch_group<10, MAXT, false>(batch, cfg, g, queue, s);
+    if (k <= 12) return launch_group<12, MAXT, false>(batch, cfg, g, queue, s);
   }
   if constexpr (MAXT <= 512) {
-    if (k <= 14) return launch_group<14, MAXT>(batch, cfg, g, queue, s);
-    if (k <= 16) return launch_group<16, MAXT>(batch, cfg, g, queue, s);
+    if (k <= 14) return launch_group<14, MAXT, false>(batch, cfg, g, queue, s);
+    if (k <= 16) return launch_group<16, MAXT, false>(batch, cfg, g, queue, s);
   }
   return set_err(FRB_E_TOO_LARGE, "too many free DOFs per thread for this CTA size");
 }
@@ -1274,14 +1320,12 @@ int frb_device_info(int device, int* n_sm, int* smem_optin, int* cc_major, int* 
   return FRB_OK;
 }
 
-int64_t frb_rank_smem_bytes(int32_t n_pos, int32_t n_own, int32_t n_act, int32_t n_leaves_total) {
+int64_t frb_rank_smem_bytes(int32_t n_pos, int32_t n_own, int32_t n_act, int32_t n_slots, int32_t n_prog,
+                            int32_t fprv_global) {
   const int64_t nf = 3 * static_cast<int64_t>(n_own);
-  const int64_t L = n_leaves_total;
-  const int64_t slots = L > 0 ? 2 * L - 1 : 1;
-  const int64_t levels = L > 1 ? 64 - __builtin_clzll(static_cast<uint64_t>(L - 1)) + 1 : 0;  // >= tree height
-  const int64_t prog_ints = (levels + 1) + 3 * (L > 0 ? L - 1 : 0);
-  return 8 * (3 * static_cast<int64_t>(n_pos) + 2 * nf + (nf > n_act ? nf : n_act) + 3 * slots + 16) +
-         4 * ((prog_ints + 1) & ~1LL);
+  return 8 * (3 * static_cast<int64_t>(n_pos) + (fprv_global ? 1 : 2) * nf + (nf > n_act ? nf : n_act) +
+              3 * static_cast<int64_t>(n_slots) + 16) +
+         4 * ((static_cast<int64_t>(n_prog) + 1) & ~1LL);
 }
 
 int frb_max_dofs_per_thread(int block_threads) { return dofs_cap(block_threads); }

@@ -31,7 +31,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from .plan import PlanView
+from .plan import PlanView, tree_split
 
 MAX_SEND = 2
 MAX_LOCAL = 0xFFFF            # local node ids and active-element ids are 16 bit
@@ -51,6 +51,7 @@ class RankTables:
     halo_g: np.ndarray       # (n_local - n_own,) int32
     send: np.ndarray         # (n_own, MAX_SEND) int32
     fix_g: np.ndarray = None # (n_fix,) int32
+    tree: np.ndarray = None  # int32 block of plan.tree_split (local/top programs, exports)
 
     @property
     def stride(self) -> int:
@@ -183,6 +184,9 @@ def partition(n_nodes: int, n_free: int, ia: np.ndarray, ib: np.ndarray, ell_oth
                                 act_elem=act.astype(np.int64), halo_g=halo.astype(np.int32),
                                 send=np.full((n_own, MAX_SEND), -1, dtype=np.int32),
                                 fix_g=fix.astype(np.int32)))
+    blocks = tree_split(plan, [(rt.leaf0, rt.leaf0 + rt.n_leaves) for rt in ranks])
+    for rt, bk in zip(ranks, blocks):
+        rt.tree = bk
     # send lists: rank q keeps node g as halo at local index n_own_q + k
     for q, halo in enumerate(halo_lists):
         for k, g in enumerate(halo):
@@ -195,19 +199,28 @@ def partition(n_nodes: int, n_free: int, ia: np.ndarray, ib: np.ndarray, ell_oth
     return Partition(C=C, slots_a=slots_a, slots_b=slots_b, ranks=ranks)
 
 
-def rank_smem_bytes(rt: RankTables, n_leaves_total: int) -> int:
+def rank_smem_bytes(rt: RankTables, fprv_global: bool = False) -> int:
     """Dynamic SMEM of one rank (mirror of frb_rank_smem_bytes):
     positions [n_local + n_fix][3] (a DOF's own position slot doubles as its
-    sq entry between the force and update phases), f, f_prev (8 B per own
-    DOF each), coefficients / sq2 max(own DOFs, n_act), tree slots [2L-1][3],
-    16 cluster flag words and the tree's int32 combine program."""
-    return smem_bytes(rt.n_local + rt.n_fix, rt.n_own, rt.n_act, n_leaves_total)
+    sq entry between the force and update phases), f and -- unless it lives
+    in global memory -- f_prev (8 B per own DOF each), coefficients / sq2
+    max(own DOFs, n_act), local + top tree slots (3 doubles each), 16 cluster
+    flag words and the int32 tree block (programs + exports)."""
+    return smem_bytes(rt.n_local + rt.n_fix, rt.n_own, rt.n_act, int(rt.tree[0]) + int(rt.tree[1]),
+                      int(rt.tree[2]), fprv_global)
 
 
-def smem_bytes(n_pos: int, n_own: int, n_act: int, n_leaves_total: int) -> int:
+def partition_smem_bytes(part: "Partition", fprv_global: bool = False) -> int:
+    """Dynamic SMEM of every rank of a partitioned problem: the kernel lays
+    all ranks out identically (peers address each other's buffers by the same
+    offsets), each region sized by its maximum over the ranks."""
+    rs = part.ranks
+    return smem_bytes(max(r.n_local + r.n_fix for r in rs), max(r.n_own for r in rs),
+                      max(r.n_act for r in rs), int(rs[0].tree[0]) + int(rs[0].tree[1]), int(rs[0].tree[2]),
+                      fprv_global)
+
+
+def smem_bytes(n_pos: int, n_own: int, n_act: int, n_slots: int, n_prog: int, fprv_global: bool = False) -> int:
     nf = 3 * n_own
-    L = n_leaves_total
-    slots = 2 * L - 1 if L > 0 else 1
-    levels = (L - 1).bit_length() + 1 if L > 1 else 0
-    prog = (levels + 1) + 3 * (L - 1 if L > 0 else 0)
-    return 8 * (3 * n_pos + 2 * nf + max(nf, n_act) + 3 * slots + 16) + 4 * ((prog + 1) & ~1)
+    return 8 * (3 * n_pos + (1 if fprv_global else 2) * nf + max(nf, n_act) + 3 * n_slots + 16) + \
+        4 * ((n_prog + 1) & ~1)

@@ -136,3 +136,168 @@ def evaluate(flat: np.ndarray, a) -> float:
         for k in range(int(p.level_off[lev]), int(p.level_off[lev + 1])):
             slots[int(p.op_dst[k])] = slots[int(p.op_left[k])] + slots[int(p.op_right[k])]
     return slots[p.root]
+
+
+# ---------------------------------------------------------------- cluster split
+
+TREE_HEADER = 10
+
+
+def _program(ops: list[tuple[int, int, int, int]]) -> np.ndarray:
+    """Flat [n_levels, level_off[n_levels + 1], dst[K], left[K], right[K]]
+    from (height, dst, left, right); ops of one height are independent."""
+    ops = sorted(ops, key=lambda o: o[0])
+    heights = sorted({o[0] for o in ops})
+    level_off = [0]
+    for h in heights:
+        level_off.append(level_off[-1] + sum(1 for o in ops if o[0] == h))
+    return np.concatenate([
+        np.array([len(heights)], dtype=np.int32), np.array(level_off, dtype=np.int32),
+        np.array([o[1] for o in ops], dtype=np.int32), np.array([o[2] for o in ops], dtype=np.int32),
+        np.array([o[3] for o in ops], dtype=np.int32)])
+
+
+def tree_split(flat: np.ndarray, ranges: list[tuple[int, int]]) -> list[np.ndarray]:
+    """Split the pairwise tree over the cluster ranks that own the leaf
+    ranges [a_r, b_r).  A node is *local* to rank r when all its leaves are
+    r's; r evaluates its local nodes (the local program, over its own leaves
+    numbered 0.. followed by its local internal nodes) and exports the
+    maximal ones -- those whose parent is not local -- into a *top* slot
+    array that every rank holds: exports first (ordered by leaf position),
+    then the non-local internal nodes.  Every rank replays the same top
+    program, so all ranks obtain the identical root.  The combine order is
+    NumPy's throughout; only where each addition happens changes.
+
+    Returns one int32 block per rank:
+        [LS, TS, PI, lprog_off, tprog_off, exp_off, n_exp, root_top, E, 0,
+         local program, top program, exports (local slot, top slot) pairs]
+    LS / PI are maxima over the ranks (uniform SMEM layout), TS = E + #top
+    internal nodes, root_top = top slot of the root (-1: empty tree)."""
+    p = PlanView(flat)
+    L = p.n_leaves
+    C = len(ranges)
+    if L == 0:
+        blocks = []
+        for _ in range(C):
+            blocks.append(np.array([0, 0, TREE_HEADER, TREE_HEADER, TREE_HEADER + 2, TREE_HEADER + 4, 0, -1, 0, 0,
+                                    0, 0, 0, 0], dtype=np.int32))
+        return blocks
+    n_slots = 2 * L - 1
+    lo = np.zeros(n_slots, dtype=np.int64)
+    hi = np.zeros(n_slots, dtype=np.int64)
+    lo[:L] = np.arange(L)
+    hi[:L] = np.arange(L) + 1
+    parent = np.full(n_slots, -1, dtype=np.int64)
+    K = L - 1
+    for k in range(K):                         # ops are ordered by height
+        d, a, b = int(p.op_dst[k]), int(p.op_left[k]), int(p.op_right[k])
+        lo[d], hi[d] = lo[a], hi[b]
+        parent[a] = parent[b] = d
+    leaf_rank = np.empty(L, dtype=np.int64)
+    for r, (a, b) in enumerate(ranges):
+        leaf_rank[a:b] = r
+    owner = np.where(leaf_rank[lo] == leaf_rank[hi - 1], leaf_rank[lo], -1)
+    # every leaf range must be split exactly at rank boundaries
+    for r, (a, b) in enumerate(ranges):
+        if b > a:
+            assert (leaf_rank[a:b] == r).all()
+    exports = [s for s in range(n_slots)
+               if owner[s] >= 0 and (parent[s] < 0 or owner[parent[s]] != owner[s])]
+    exports.sort(key=lambda s: lo[s])
+    E = len(exports)
+    top_of = np.full(n_slots, -1, dtype=np.int64)
+    for i, s in enumerate(exports):
+        top_of[s] = i
+    top_internal = [k for k in range(K) if owner[int(p.op_dst[k])] < 0]
+    theight = {}
+    top_ops = []
+    for j, k in enumerate(top_internal):       # in height order
+        d, a, b = int(p.op_dst[k]), int(p.op_left[k]), int(p.op_right[k])
+        top_of[d] = E + j
+        h = 1 + max(theight.get(a, 0), theight.get(b, 0))
+        theight[d] = h
+        top_ops.append((h, int(top_of[d]), int(top_of[a]), int(top_of[b])))
+    TS = E + len(top_internal)
+    root_top = int(top_of[p.root])
+    tprog = _program(top_ops)
+    blocks = []
+    for r, (a, b) in enumerate(ranges):
+        local_idx = np.full(n_slots, -1, dtype=np.int64)
+        local_idx[a:b] = np.arange(b - a)
+        nl = b - a
+        lheight = {}
+        lops = []
+        for k in range(K):
+            d, x, y = int(p.op_dst[k]), int(p.op_left[k]), int(p.op_right[k])
+            if owner[d] != r:
+                continue
+            local_idx[d] = nl
+            nl += 1
+            h = 1 + max(lheight.get(x, 0), lheight.get(y, 0))
+            lheight[d] = h
+            lops.append((h, int(local_idx[d]), int(local_idx[x]), int(local_idx[y])))
+        lprog = _program(lops)
+        exp = np.array([(int(local_idx[s]), int(top_of[s])) for s in exports if owner[s] == r],
+                       dtype=np.int32).reshape(-1)
+        lprog_off = TREE_HEADER
+        tprog_off = lprog_off + len(lprog)
+        exp_off = tprog_off + len(tprog)
+        hdr = np.array([nl, TS, 0, lprog_off, tprog_off, exp_off, len(exp) // 2, root_top, E, 0],
+                       dtype=np.int32)
+        blocks.append(np.concatenate([hdr, lprog, tprog, exp]).astype(np.int32))
+    LS = max(int(bk[0]) for bk in blocks)
+    PI = max(len(bk) for bk in blocks)
+    for bk in blocks:
+        bk[0] = LS
+        bk[2] = PI
+    return blocks
+
+
+def evaluate_split(flat: np.ndarray, blocks: list[np.ndarray], ranges, a) -> float:
+    """Replay the split tree on the host exactly as the kernel does (test
+    helper proving tree_split preserves np.sum's result bit for bit)."""
+    p = PlanView(flat)
+    a = [float(x) for x in np.asarray(a, dtype=np.float64)]
+    if p.n_leaves == 0:
+        return 0.0
+    leaf = []
+    for l in range(p.n_leaves):
+        start, size = int(p.leaf_start[l]), int(p.leaf_size[l])
+        if size < 8:
+            s, body = 0.0, 0
+        else:
+            body = size - size % 8
+            r = []
+            for j in range(8):
+                acc = a[start + j]
+                for t in range(start + j + 8, start + body, 8):
+                    acc += a[t]
+                r.append(acc)
+            s = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]))
+        for t in range(start + body, start + size):
+            s += a[t]
+        leaf.append(s)
+
+    def run(prog, slots):
+        nlev = int(prog[0])
+        off = prog[1:nlev + 2]
+        K = int(off[-1]) if nlev else 0
+        dst = prog[nlev + 2:nlev + 2 + K]
+        lef = prog[nlev + 2 + K:nlev + 2 + 2 * K]
+        rig = prog[nlev + 2 + 2 * K:nlev + 2 + 3 * K]
+        for k in range(K):
+            slots[int(dst[k])] = slots[int(lef[k])] + slots[int(rig[k])]
+
+    TS = int(blocks[0][1])
+    top = [0.0] * TS
+    for bk, (ra, rb) in zip(blocks, ranges):
+        LS = int(bk[0])
+        loc = [0.0] * max(LS, 1)
+        loc[:rb - ra] = leaf[ra:rb]
+        run(bk[int(bk[3]):int(bk[4])], loc)
+        exp = bk[int(bk[5]):int(bk[5]) + 2 * int(bk[6])]
+        for i in range(0, len(exp), 2):
+            top[int(exp[i + 1])] = loc[int(exp[i])]
+    bk = blocks[0]
+    run(bk[int(bk[4]):int(bk[5])], top)
+    return top[int(bk[7])]

@@ -138,3 +138,20 @@ def test_identity_deformation_converges_in_one(cuda_device):
     r = frb.dynamic_relaxation_solve(net, frb.AffineBC(np.eye(3)))
     assert r.converged and r.iters == 1
     assert not r.u.any() and not r.avg_stress.any()
+
+
+@pytest.mark.parametrize("n,iters", [(14, 20000), (20, 60), (32, 40)])
+def test_cluster_paths_vs_oracle(cuda_device, n, iters):
+    """Networks split over 2 / 8 / 16-CTA clusters (the 32^3 one with f_prev
+    in global memory, config 3's path), bit-equal to the oracle.  The larger
+    ones stop at max_iters so the CPU oracle stays fast; u, f, residual and
+    the stress are compared at that iterate."""
+    net = frb.generate_lattice(n, n, n, 0.3, 3)
+    F = np.eye(3) + 0.2 * np.outer([1, 0, 0], [0, 1, 0])
+    cfg = frb.SolverConfig(max_iters=iters)
+    batch = frb.pack_batch([net], [frb.AffineBC(F)])
+    assert int(batch.desc[0]["cluster"]) == {14: 2, 20: 8, 32: 16}[n]
+    assert bool(batch.groups[0]["fprv_global"]) == (n == 32)
+    r = frb.solve_batch(batch, config=cfg)[0]
+    o = orc.solve(net, F, cfg)
+    assert_matches(r, o.u, o.iters, o.converged, o.residual, o.r_ref, o.sigma, label=f"{n}^3")

@@ -9,7 +9,7 @@ import golden_cases as gc
 import paper_2305_07030_b200 as frb
 from paper_2305_07030_b200 import _native as nat
 from paper_2305_07030_b200 import batch as fb
-from paper_2305_07030_b200.partition import rank_smem_bytes
+from paper_2305_07030_b200.partition import partition_smem_bytes, rank_smem_bytes
 from paper_2305_07030_b200.plan import PlanView
 
 
@@ -113,17 +113,47 @@ def test_partition_tables(net, C):
 
 
 def test_rank_smem_mirror_matches_library():
-    for n_local, n_own, n_act, L in [(3375, 2197, 7098, 64), (1300, 1099, 3600, 64), (150, 150, 400, 4),
-                                     (0, 0, 0, 0), (1, 1, 0, 1), (63, 63, 400, 2)]:
-        from paper_2305_07030_b200.partition import smem_bytes
-        assert nat.lib().frb_rank_smem_bytes(n_local, n_own, n_act, L) == smem_bytes(n_local, n_own, n_act, L)
+    from paper_2305_07030_b200.partition import smem_bytes
+    for args in [(3375, 2197, 7098, 127, 700, 0), (1300, 1099, 3600, 80, 301, 1), (150, 150, 400, 7, 41, 0),
+                 (0, 0, 0, 0, 14, 0), (1, 1, 0, 1, 15, 1), (63, 63, 400, 3, 20, 0)]:
+        assert nat.lib().frb_rank_smem_bytes(*args) == smem_bytes(*args[:5], bool(args[5]))
 
 
 def test_c2_networks_use_two_ranks_and_fit():
     t = fb.build_problem(frb.generate_lattice(15, 15, 15, 0.3, 0), frb.AffineBC(np.eye(3))).topo
-    part = t.choose_cluster()
-    assert part.C == 2
-    assert max(rank_smem_bytes(r, t.n_leaves) for r in part.ranks) <= fb.SMEM_BUDGET
+    part, fglob = t.choose_cluster()
+    assert part.C == 2 and not fglob
+    assert partition_smem_bytes(part) <= fb.SMEM_BUDGET
+    assert partition_smem_bytes(part) >= max(rank_smem_bytes(r) for r in part.ranks)
+
+
+def test_c3_networks_fit_a_16_cluster_with_global_fprev():
+    """100k-DOF networks (config 3): 16 ranks, f_prev in global memory."""
+    t = fb.build_problem(frb.generate_lattice(32, 32, 32, 0.3, 0), frb.AffineBC(np.eye(3))).topo
+    part, fglob = t.choose_cluster()
+    assert part.C == 16 and fglob
+    assert partition_smem_bytes(part, True) <= fb.SMEM_BUDGET
+
+
+@pytest.mark.parametrize("n", [1, 7, 100, 129, 450, 1029, 6591, 24000])
+@pytest.mark.parametrize("C", [1, 2, 3, 5, 16])
+def test_tree_split_reproduces_numpy_sum(n, C):
+    """The cluster split of the pairwise tree (local subtrees + exported
+    roots + shared top program) gives np.sum's bits for any leaf split."""
+    from paper_2305_07030_b200.plan import evaluate_split, reduction_plan, tree_split
+    flat = reduction_plan(n)
+    L = int(flat[0])
+    if C > L:
+        pytest.skip("more ranks than leaves")
+    rng = np.random.default_rng(n * 31 + C)
+    cuts = sorted(rng.choice(np.arange(1, L), C - 1, replace=False).tolist()) if C > 1 else []
+    b = [0] + cuts + [L]
+    ranges = list(zip(b[:-1], b[1:]))
+    blocks = tree_split(flat, ranges)
+    for _ in range(3):
+        a = rng.standard_normal(n) * np.exp(rng.uniform(-30, 30, n))
+        assert evaluate_split(flat, blocks, ranges, a) == np.sum(a)
+    assert len({int(bk[1]) for bk in blocks}) == 1 and len({int(bk[0]) for bk in blocks}) == 1
 
 
 def test_pack_offsets_groups_and_dedup():
@@ -138,8 +168,7 @@ def test_pack_offsets_groups_and_dedup():
     assert sorted(b.arrays["order"].tolist()) == list(range(5))
     assert b.arrays["order"][-1] == 4                                # largest first
     g = b.groups[0]
-    assert g["smem_bytes"] == max(rank_smem_bytes(r, p.topo.n_leaves)
-                                  for p in b.problems for r in p.topo.partition(1).ranks)
+    assert g["smem_bytes"] == max(partition_smem_bytes(p.topo.partition(1)) for p in b.problems)
 
 
 def test_mixed_sizes_form_cluster_groups():
