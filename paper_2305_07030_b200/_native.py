@@ -13,9 +13,9 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libfrb200.so")
+LIB_PATH = os.environ.get("FRB_LIB") or os.path.join(HERE, "lib", "libfrb200.so")
 
-ABI_VERSION = 4
+ABI_VERSION = 5
 MAX_CLUSTER = 16
 FRB_OK, FRB_E_INVALID, FRB_E_TOO_LARGE, FRB_E_CUDA, FRB_E_UNSUPPORTED = 0, -1, -2, -3, -4
 STATUS_CONVERGED, STATUS_MAX_ITERS, STATUS_SINGULAR = 0, 1, 2
@@ -33,7 +33,7 @@ class FrbConfig(C.Structure):
                 ("energy_check_interval", C.c_int32), ("bc_ramp_iters", C.c_int32)]
 
 
-BATCH_POINTERS = ("groups", "problems", "parts", "order", "X", "dof_mass", "inc_node", "inc",
+BATCH_POINTERS = ("groups", "problems", "parts", "order", "X", "node_mass", "inc_node", "inc",
                   "elem_ab", "elem_L", "elem_EA", "plans", "ell", "act_ab", "act_L",
                   "act_EA", "halo_g", "send", "fix_g", "trees", "u", "f", "work", "results", "queue",
                   "phase_cycles")

@@ -338,7 +338,7 @@ def _pack(networks, bcs, probs, cluster: int | None = None) -> Batch:
                 trees.append(rt.tree)
                 n_tree += len(rt.tree)
                 ell.append(rt.ell.reshape(-1))
-                act_ab.append(rt.act_ab)
+                act_ab.append(rt.act_ab[:, 0].astype(np.uint32) | (rt.act_ab[:, 1].astype(np.uint32) << 16))
                 halo_g.append(rt.halo_g)
                 send.append(rt.send)
                 fix_g.append(rt.fix_g)
@@ -390,7 +390,7 @@ def _pack(networks, bcs, probs, cluster: int | None = None) -> Batch:
         actv_base += off
         node_base[i + 1] = node_base[i] + p.n_nodes
         X.append(p.X.reshape(-1))
-        mass.append(np.repeat(p.node_mass, 3))
+        mass.append(p.node_mass)
         EL.append(L)
         EA.append(ea)
         inc_node.append(t.inc_node)
@@ -414,12 +414,12 @@ def _pack(networks, bcs, probs, cluster: int | None = None) -> Batch:
         groups.append(g)
         order.extend(ids)
     arrays = dict(
-        X=_cat(X, np.float64), dof_mass=_cat(mass, np.float64),
+        X=_cat(X, np.float64), node_mass=_cat(mass, np.float64),
         inc_node=_cat(inc_node, np.int32, 2), inc=_cat(inc, np.int32, 2),
         elem_ab=_cat(elem_ab, np.int32, 2), elem_L=_cat(EL, np.float64),
         elem_EA=_cat(EA, np.float64), plans=_cat(plans, np.int32),
         ell=_cat(ell, np.uint32).view(np.int32), fix_g=_cat(fix_g, np.int32),
-        act_ab=_cat(act_ab, np.int32, 2), act_L=_cat(act_L, np.float64),
+        act_ab=_cat(act_ab, np.uint32).view(np.int32), act_L=_cat(act_L, np.float64),
         halo_g=_cat(halo_g, np.int32), send=_cat(send, np.int32, MAX_SEND), trees=_cat(trees, np.int32),
         order=np.asarray(order, dtype=np.int32),
         problems=desc.view(np.uint8).copy(), parts=parts.view(np.uint8).copy(),
@@ -509,7 +509,7 @@ class DeviceBatch:
         fb.n_groups = len(groups)
         fb.groups = groups_c.ctypes.data
         t = self.t
-        for k in ("parts", "order", "X", "dof_mass", "inc_node", "inc", "elem_ab", "elem_L", "elem_EA",
+        for k in ("parts", "order", "X", "node_mass", "inc_node", "inc", "elem_ab", "elem_L", "elem_EA",
                   "plans", "ell", "act_ab", "act_L", "act_EA", "halo_g", "send", "fix_g", "trees"):
             setattr(fb, k, t[k].data_ptr() if k in t and t[k].numel() else None)
         fb.problems = desc_t.data_ptr()

@@ -147,7 +147,7 @@ struct Net {
   double dt, hdt, volume, ea;
   double g[9];  // F - I
   const double* X;
-  const double* mass3;  // per DOF
+  const double* mass;   // per node
   const int2* incn;
   const int2* inc;
   const int2* eab;
@@ -167,7 +167,7 @@ struct Rank {
   uint32_t halo_bytes, leaf_bytes;  // transaction bytes this rank receives per phase
   const int* tree;
   const uint32_t* ell;
-  const int2* act_ab;
+  const uint32_t* act_ab;
   const double* act_L;
   const double* act_EA;
   const int* halo_g;
@@ -190,7 +190,7 @@ __device__ void load_views(Net& n, Rank& R, const frb_batch& b, int p, int r) {
     for (int c = 0; c < 3; ++c) n.g[3 * i + c] = dsub(P.F[3 * i + c], i == c ? 1.0 : 0.0);
   n.node_base = P.node_base;
   n.X = b.X + 3 * P.node_base;
-  n.mass3 = b.dof_mass + 3 * P.node_base;
+  n.mass = b.node_mass + P.node_base;
   n.incn = reinterpret_cast<const int2*>(b.inc_node) + P.node_base;
   n.inc = reinterpret_cast<const int2*>(b.inc) + P.inc_base;
   n.eab = reinterpret_cast<const int2*>(b.elem_ab) + P.elem_base;
@@ -231,7 +231,7 @@ __device__ void load_views(Net& n, Rank& R, const frb_batch& b, int p, int r) {
   }
   R.CF = max(R.CF, R.NFO);
   R.ell = b.ell + Q.ell_base;
-  R.act_ab = reinterpret_cast<const int2*>(b.act_ab) + Q.act_base;
+  R.act_ab = b.act_ab + Q.act_base;
   R.act_L = b.act_L + P.actv_base + Q.actv_off;
   R.act_EA = (b.act_EA && !n.ea_uniform) ? b.act_EA + P.actv_base + Q.actv_off : nullptr;
   R.halo_g = b.halo_g + Q.halo_base;
@@ -361,24 +361,59 @@ extern __shared__ __align__(16) double g_smem[];
 // Phase F1: coefficient EA (l - L) / (L l) of every active element of the
 // rank, once per iteration (microsolver.py:196-211).  Elements cut by a rank
 // boundary are evaluated by both ranks from identical operands.
-__device__ __forceinline__ bool element_coefs(int n_act, const int2* __restrict__ act_ab,
+constexpr int kElem = 4;  // elements a thread keeps in flight in F1
+
+__device__ __noinline__ LenCoef exact_elem(int o_pos, uint32_t ab, double L, double EA) {
+  const double* pa = &g_smem[o_pos + 3 * static_cast<int>(ab & 0xffffu)];
+  const double* pb = &g_smem[o_pos + 3 * static_cast<int>(ab >> 16)];
+  return exact_len_coef(dsub(pb[0], pa[0]), dsub(pb[1], pa[1]), dsub(pb[2], pa[2]), L, EA);
+}
+
+__device__ __forceinline__ bool element_coefs(int n_act, const uint32_t* __restrict__ act_ab,
                                               const double* __restrict__ act_L, const double* __restrict__ act_EA,
                                               double ea, int o_pos, int o_cf) {
   bool bad = false;
   const int T = blockDim.x;
-#pragma unroll 2
-  for (int e = threadIdx.x; e < n_act; e += T) {
-    const int2 ab = __ldg(act_ab + e);
-    const double L = __ldg(act_L + e);
-    const double EA = act_EA ? __ldg(act_EA + e) : ea;
-    const double* pa = &g_smem[o_pos + 3 * ab.x];
-    const double* pb = &g_smem[o_pos + 3 * ab.y];
-    const double dx = dsub(pb[0], pa[0]);
-    const double dy = dsub(pb[1], pa[1]);
-    const double dz = dsub(pb[2], pa[2]);
-    const LenCoef lc = len_coef(dx, dy, dz, L, EA);
-    bad |= lc.l < dmul(kCollapse, L);
-    g_smem[o_cf + e] = lc.coef;
+  const int last = n_act - 1;
+  for (int e0 = threadIdx.x; e0 < n_act; e0 += kElem * T) {
+    uint32_t ab[kElem];
+    double L[kElem], EA[kElem], l[kElem], cf[kElem];
+    bool ok[kElem];
+#pragma unroll
+    for (int q = 0; q < kElem; ++q) {  // table loads of the whole group first
+      const int e = min(e0 + q * T, last);
+      ab[q] = __ldg(act_ab + e);
+      L[q] = __ldg(act_L + e);
+      EA[q] = act_EA ? __ldg(act_EA + e) : ea;
+    }
+#pragma unroll
+    for (int q = 0; q < kElem; ++q) {  // independent chains: the scheduler interleaves them
+      const double* pa = &g_smem[o_pos + 3 * static_cast<int>(ab[q] & 0xffffu)];
+      const double* pb = &g_smem[o_pos + 3 * static_cast<int>(ab[q] >> 16)];
+      const double dx = dsub(pb[0], pa[0]);
+      const double dy = dsub(pb[1], pa[1]);
+      const double dz = dsub(pb[2], pa[2]);
+      bool ok1, ok2;
+      l[q] = frb_arith::sqrt_fast(len2(dx, dy, dz), ok1);
+      cf[q] = frb_arith::div_fast(dmul(EA[q], dsub(l[q], L[q])), dmul(L[q], l[q]), ok2);
+      ok[q] = ok1 && ok2;
+    }
+#pragma unroll
+    for (int q = 0; q < kElem; ++q) {
+      if (!ok[q]) {
+        const LenCoef r = exact_elem(o_pos, ab[q], L[q], EA[q]);
+        l[q] = r.l;
+        cf[q] = r.coef;
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < kElem; ++q) {
+      const int e = e0 + q * T;
+      if (e < n_act) {
+        bad |= l[q] < dmul(kCollapse, L[q]);
+        g_smem[o_cf + e] = cf[q];
+      }
+    }
   }
   return bad;
 }
@@ -421,18 +456,28 @@ __device__ __forceinline__ void gather_role(const uint32_t* __restrict__ ell_i, 
   }
 }
 
-// f of every own node into g_smem[o_out + 3 i + axis]
+// f of every own node into g_smem[o_out + 3 i + axis]; a thread gathers two
+// of its nodes together so their load latencies overlap
+__device__ __forceinline__ void node_force(const uint32_t* __restrict__ ell, int S, int SA, int SB, int o_pos,
+                                           int o_cf, int o_out, int i) {
+  const double px = g_smem[o_pos + 3 * i], py = g_smem[o_pos + 3 * i + 1], pz = g_smem[o_pos + 3 * i + 2];
+  double ax = 0.0, ay = 0.0, az = 0.0, bx = 0.0, by = 0.0, bz = 0.0;
+  gather_role<true>(ell + i, S, SA, i, o_pos, o_cf, px, py, pz, ax, ay, az);
+  gather_role<false>(ell + SA * S + i, S, SB, i, o_pos, o_cf, px, py, pz, bx, by, bz);
+  g_smem[o_out + 3 * i] = dadd(ax, bx);
+  g_smem[o_out + 3 * i + 1] = dadd(ay, by);
+  g_smem[o_out + 3 * i + 2] = dadd(az, bz);
+}
+
 __device__ __forceinline__ void node_forces(int n_own, const uint32_t* __restrict__ ell, int S, int SA, int SB,
                                             int o_pos, int o_cf, int o_out) {
-  for (int i = threadIdx.x; i < n_own; i += blockDim.x) {
-    const double px = g_smem[o_pos + 3 * i], py = g_smem[o_pos + 3 * i + 1], pz = g_smem[o_pos + 3 * i + 2];
-    double ax = 0.0, ay = 0.0, az = 0.0, bx = 0.0, by = 0.0, bz = 0.0;
-    gather_role<true>(ell + i, S, SA, i, o_pos, o_cf, px, py, pz, ax, ay, az);
-    gather_role<false>(ell + SA * S + i, S, SB, i, o_pos, o_cf, px, py, pz, bx, by, bz);
-    g_smem[o_out + 3 * i] = dadd(ax, bx);
-    g_smem[o_out + 3 * i + 1] = dadd(ay, by);
-    g_smem[o_out + 3 * i + 2] = dadd(az, bz);
+  const int T = blockDim.x;
+  int i = threadIdx.x;
+  for (; i + T < n_own; i += 2 * T) {
+    node_force(ell, S, SA, SB, o_pos, o_cf, o_out, i);
+    node_force(ell, S, SA, SB, o_pos, o_cf, o_out, i + T);
   }
+  if (i < n_own) node_force(ell, S, SA, SB, o_pos, o_cf, o_out, i);
 }
 
 // ------------------------------------------------------------------ block helpers
@@ -664,25 +709,25 @@ __device__ __forceinline__ Layout layout(const Rank& R) {
   return o;
 }
 
-// Replay one combine program (plan.py _program layout) on slot array
-// g_smem[o_slot + 3 s + {0,1,2}] with the calling warp; ops of a level are
-// independent, one lane per op.
+// Replay one combine program (plan.py _program: warp rounds of up to 32
+// independent ops, lane-packed) on g_smem[o_slot + 3 s + {0,1,2}] with the
+// calling warp.  The next round's op is fetched while the current one runs.
 __device__ __forceinline__ void run_prog(const int* prog, int o_slot, int lane) {
-  const int nlev = prog[0];
-  const int* off = prog + 1;
-  const int K = off[nlev];
-  const int* dst = prog + nlev + 2;
-  const int* lf = dst + K;
-  const int* rt = lf + K;
-  for (int lev = 0; lev < nlev; ++lev) {
-    const int k1 = off[lev + 1];
-    for (int k = off[lev] + lane; k < k1; k += 32) {
-      const int d = o_slot + 3 * dst[k], a = o_slot + 3 * lf[k], c = o_slot + 3 * rt[k];
-      g_smem[d] = dadd(g_smem[a], g_smem[c]);
-      g_smem[d + 1] = dadd(g_smem[a + 1], g_smem[c + 1]);
-      g_smem[d + 2] = dadd(g_smem[a + 2], g_smem[c + 2]);
+  const int nr = prog[0];
+  const int2* w = reinterpret_cast<const int2*>(prog + 2);  // 8-byte aligned (plan.py _program)
+  int2 cur = nr > 0 ? w[lane] : make_int2(-1, 0);
+  for (int r = 0; r < nr; ++r) {
+    const int2 nxt = r + 1 < nr ? w[(r + 1) * 32 + lane] : make_int2(-1, 0);
+    if (cur.x >= 0) {
+      const int d = o_slot + 3 * cur.x, a = o_slot + 3 * (cur.y & 0xffff), c = o_slot + 3 * (cur.y >> 16);
+      const double a0 = g_smem[a], a1 = g_smem[a + 1], a2 = g_smem[a + 2];
+      const double c0 = g_smem[c], c1 = g_smem[c + 1], c2 = g_smem[c + 2];
+      g_smem[d] = dadd(a0, c0);
+      g_smem[d + 1] = dadd(a1, c1);
+      g_smem[d + 2] = dadd(a2, c2);
     }
     __syncwarp();
+    cur = nxt;
   }
 }
 
@@ -712,13 +757,13 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
   const int C = n.C, L = n.L, n_own = R.n_own, nfo = 3 * n_own;
   const Layout o = layout<kFG>(R);
   const double* __restrict__ Xg = n.X;
-  const double* __restrict__ mass3 = n.mass3;
+  const double* __restrict__ nmass = n.mass + R.node0;  // own nodes' masses
   const int dof0 = 3 * R.node0;
   const int dl_max = nfo > 0 ? nfo - 1 : 0;  // clamp for unconditional per-DOF loads
   // hot per-rank tables and sizes, held in registers
   const uint32_t* __restrict__ ell = R.ell;
   const int S = R.S, SA = R.SA, SB = R.SB, n_act = R.n_act;
-  const int2* __restrict__ act_ab = R.act_ab;
+  const uint32_t* __restrict__ act_ab = R.act_ab;
   const double* __restrict__ act_L = R.act_L;
   const double* __restrict__ act_EA = R.act_EA;
   const double ea = n.ea;
@@ -728,7 +773,16 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
   // f_prev of own DOF dl: SMEM, or the `f` output array for networks too
   // large for the cluster's SMEM (it ends up holding the final f either way)
   double* const fprv_g = b.f + 3 * n.node_base + dof0;
-  auto FPRV = [&](int dl) -> double& { return kFG ? fprv_g[dl] : g_smem[o.fprv + dl]; };
+  // (value getter / setter: a generic reference into shared memory would
+  // hide the address space from the compiler)
+  auto FPRV = [&](int dl) -> double { return kFG ? fprv_g[dl] : g_smem[o.fprv + dl]; };
+  auto SET_FPRV = [&](int dl, double x) {
+    if (kFG) {
+      fprv_g[dl] = x;
+    } else {
+      g_smem[o.fprv + dl] = x;
+    }
+  };
 
   // the rank's tree block (local + top programs, exports) lives in SMEM
   int* const prog = reinterpret_cast<int*>(g_smem) + o.prog;
@@ -765,10 +819,21 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
     nt = lsize - 8 * q;
   }
 
-  // new position of own DOF dl: local slot + the halo copies of peers
-  auto put_pos = [&](int dl, double x) {
+  // reference coordinates of the own DOFs stay in registers; bit k of
+  // sendbits: own DOF k is halo to some peer (its node has a send target)
+  double xr[MAXK];
+  uint32_t sendbits = 0;
+#pragma unroll
+  for (int k = 0; k < MAXK; ++k) {
+    const int dl = min(t + k * T, dl_max);
+    xr[k] = __ldg(Xg + dof0 + dl);
+    if (C > 1 && t + k * T < nfo && __ldg(send + dl / 3).x >= 0) sendbits |= 1u << k;
+  }
+
+  // new position of own DOF k (= dl): local slot + the halo copies of peers
+  auto put_pos = [&](int k, int dl, double x) {
     g_smem[o.pos + dl] = x;
-    if (C > 1) {
+    if (C > 1 && ((sendbits >> k) & 1u)) {
       const int node = dl / 3, axis = dl - 3 * node;
       const int2 tg = __ldg(send + node);
       if (tg.x >= 0) {
@@ -793,13 +858,13 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
 #pragma unroll
       for (int kk = 0; kk < KC; ++kk) {
         const int dl = min(t + (k0 + kk) * T, dl_max);
-        a[kk] = frb_arith::div_fast(-FPRV(dl), __ldg(mass3 + dof0 + dl), ok[kk]);
+        a[kk] = frb_arith::div_fast(-FPRV(dl), __ldg(nmass + dl / 3), ok[kk]);
       }
 #pragma unroll
       for (int kk = 0; kk < KC; ++kk) {
         if (!ok[kk]) {
           const int dl = min(t + (k0 + kk) * T, dl_max);
-          a[kk] = exact_div(-FPRV(dl), __ldg(mass3 + dof0 + dl));
+          a[kk] = exact_div(-FPRV(dl), __ldg(nmass + dl / 3));
         }
       }
 #pragma unroll
@@ -839,14 +904,22 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
   __syncthreads();
   node_forces(n_own, ell, S, SA, SB, o.pos, o.cf, o.fcur);
   __syncthreads();
-  for (int dl = t; dl < nfo; dl += T) FPRV(dl) = g_smem[o.fcur + dl];
+  for (int dl = t; dl < nfo; dl += T) SET_FPRV(dl, g_smem[o.fcur + dl]);
   __syncthreads();
+
   // a = -f/m (:428-430), then iteration 0's kick + drift (:443-448)
   accel([&](int k, int dl, double a) {
     v[k] = dadd(0.0, dmul(hdt, a));
     u[k] = dadd(0.0, dmul(dt, v[k]));
-    put_pos(dl, dadd(__ldg(Xg + dof0 + dl), u[k]));
+    put_pos(k, dl, dadd(xr[k], u[k]));
   });
+#ifdef FRB_DEBUG_PROLOGUE
+  for (int dl = t; dl < nfo; dl += T) b.f[3 * n.node_base + dof0 + dl] = FPRV(dl);
+#pragma unroll
+  for (int k = 0; k < MAXK; ++k)
+    if (t + k * T < nfo) b.u[3 * n.node_base + dof0 + t + k * T] = v[k];
+  return;
+#endif
   if (ramp) {  // iteration 0's ramp step (:449-453)
     alpha = ramp_alpha(1, ramp_n);
     set_local_fixed(n, R, &g_smem[o.pos], alpha, ramp);
@@ -886,7 +959,7 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
         const int dl = min(t + (k0 + kk) * T, dl_max);
         f[kk] = g_smem[o.fcur + dl];
         kh[kk] = FPRV(dl);  // f_prev, until the quotient replaces it
-        m[kk] = __ldg(mass3 + dof0 + dl);
+        m[kk] = __ldg(nmass + dl / 3);
       }
       if (adaptive) {
 #pragma unroll
@@ -918,7 +991,7 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
             g_smem[o.cf + dl] = dmul(dmul(u[k], m[kk]), u[k]);
           }
           g_smem[o.fcur + dl] = dmul(f[kk], f[kk]);
-          FPRV(dl) = f[kk];
+          SET_FPRV(dl, f[kk]);
         }
       }
     }
@@ -1013,46 +1086,50 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
       bool singular = sc.singular != 0;
       for (int qr = 0; qr < C; ++qr) singular |= (qr != rank) && g_smem[o.flag + qr] != 0.0;
       if (!singular) run_prog(tprog, o.tslot, lane);
-      if (t == 0) {
+      // lane 0: damping coefficient; lane 1: residual, threshold, convergence
+      if (lane < 2) {
         if (singular) {
-          sc.singular = 1;
+          if (lane == 0) sc.singular = 1;
         } else {
-          double s_sq = 0.0, s_m = 0.0, s_f = 0.0;
+          double s_a = 0.0, s_b = 0.0;
           if (root_top >= 0) {
-            s_sq = g_smem[o.tslot + 3 * root_top];
-            s_m = g_smem[o.tslot + 3 * root_top + 1];
-            s_f = g_smem[o.tslot + 3 * root_top + 2];
+            s_a = g_smem[o.tslot + 3 * root_top + (lane == 0 ? 0 : 2)];
+            s_b = g_smem[o.tslot + 3 * root_top + 1];
           }
           // np.sum adds the pairwise result to the identity 0.0
-          s_sq = dadd(0.0, s_sq);
-          s_m = dadd(0.0, s_m);
-          s_f = dadd(0.0, s_f);
-          double c = cfg.damping_c;
-          if (adaptive) {
-            if (s_m > 0.0) {
-              const double lam = ddiv(s_sq, s_m);
-              c = lam > 0.0 ? dmul(2.0, dsqrt(lam)) : 0.0;
-            } else {
-              c = 0.0;
+          s_a = dadd(0.0, s_a);
+          if (lane == 0) {
+            const double s_m = dadd(0.0, s_b);
+            double c = cfg.damping_c;
+            if (adaptive) {
+              if (s_m > 0.0) {
+                const double lam = ddiv(s_a, s_m);
+                c = lam > 0.0 ? dmul(2.0, dsqrt(lam)) : 0.0;
+              } else {
+                c = 0.0;
+              }
             }
+            sc.c = c;
+          } else {
+            const double res = dsqrt(s_a);
+            double thr = sc.threshold;
+            if (it == full_bc_iter) {
+              sc.r_ref = res;
+              const double th = dmul(cfg.tol_rel, res);
+              thr = th > cfg.tol_abs ? th : cfg.tol_abs;  // max(tol_abs, .)
+              sc.threshold = thr;
+            }
+            int done = 0, conv = 0;
+            if (it >= full_bc_iter && res <= thr) {
+              done = 1;
+              conv = 1;
+            } else if (it + 1 >= cfg.max_iters) {
+              done = 1;
+            }
+            sc.residual = res;
+            sc.done = done;
+            sc.converged = conv;
           }
-          const double res = dsqrt(s_f);
-          if (it == full_bc_iter) {
-            sc.r_ref = res;
-            const double th = dmul(cfg.tol_rel, res);
-            sc.threshold = th > cfg.tol_abs ? th : cfg.tol_abs;  // max(tol_abs, .)
-          }
-          int done = 0, conv = 0;
-          if (it >= full_bc_iter && res <= sc.threshold) {
-            done = 1;
-            conv = 1;
-          } else if (it + 1 >= cfg.max_iters) {
-            done = 1;
-          }
-          sc.c = c;
-          sc.residual = res;
-          sc.done = done;
-          sc.converged = conv;
         }
       }
     }
@@ -1065,7 +1142,7 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
       // elements (each rank redundantly; rank 0 reports)
 #pragma unroll
       for (int k = 0; k < MAXK; ++k)
-        if (t + k * T < nfo) n.posg[dof0 + t + k * T] = dadd(__ldg(Xg + dof0 + t + k * T), u[k]);
+        if (t + k * T < nfo) n.posg[dof0 + t + k * T] = dadd(xr[k], u[k]);
       set_fixed_positions(n, rank, alpha, ramp);
       csync(C);
       const int badi = singular_argmin(n, PosGlobalAll{n.posg}, sc);
@@ -1083,7 +1160,7 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
       if (!done) {
         v[k] = dadd(v[k], dmul(hdt, a));
         u[k] = dadd(u[k], dmul(dt, v[k]));
-        put_pos(dl, dadd(__ldg(Xg + dof0 + dl), u[k]));
+        put_pos(k, dl, dadd(xr[k], u[k]));
       }
     });
     if (!done && ramp && alpha < 1.0) {
@@ -1107,7 +1184,7 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
       const int d = dof0 + dl;
       uo[d] = u[k];
       if (!kFG) fo[d] = g_smem[o.fprv + dl];
-      n.posg[d] = dadd(__ldg(Xg + d), u[k]);  // x = X + u, all free nodes
+      n.posg[d] = dadd(xr[k], u[k]);  // x = X + u, all free nodes
     }
   }
   set_fixed_positions(n, rank, alpha, ramp);
@@ -1286,7 +1363,6 @@ int dispatch_k(const frb_batch* batch, const frb_config* cfg, const frb_group& g
     return set_err(FRB_E_INVALID, "fprv_global groups need 513..1024 threads per CTA");
   }
   if (k <= 1) return launch_group<1, MAXT, false>(batch, cfg, g, queue, s);
-  if (k <= 2) return launch_group<2, MAXT, false>(batch, cfg, g, queue, s);
   if (k <= 4) return launch_group<4, MAXT, false>(batch, cfg, g, queue, s);
   if (k <= 6) return launch_group<6, MAXT, false>(batch, cfg, g, queue, s);
   if (k <= 8) return launch_group<8, MAXT, false>(batch, cfg, g, queue, s);

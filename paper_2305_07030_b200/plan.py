@@ -143,18 +143,38 @@ def evaluate(flat: np.ndarray, a) -> float:
 TREE_HEADER = 10
 
 
+PROG_LANES = 32
+
+
 def _program(ops: list[tuple[int, int, int, int]]) -> np.ndarray:
-    """Flat [n_levels, level_off[n_levels + 1], dst[K], left[K], right[K]]
-    from (height, dst, left, right); ops of one height are independent."""
+    """Combine program as warp rounds: [n_rounds, 0, n_rounds x 32 x 2 words]
+    (the pad keeps the word pairs 8-byte aligned on the device).
+    Ops (height, dst, left, right) of one height are independent; each round
+    holds up to 32 of them, one per lane, as the pair (dst, left | right << 16)
+    (dst -1: idle lane).  Rounds run in order with a __syncwarp between them."""
     ops = sorted(ops, key=lambda o: o[0])
-    heights = sorted({o[0] for o in ops})
-    level_off = [0]
-    for h in heights:
-        level_off.append(level_off[-1] + sum(1 for o in ops if o[0] == h))
-    return np.concatenate([
-        np.array([len(heights)], dtype=np.int32), np.array(level_off, dtype=np.int32),
-        np.array([o[1] for o in ops], dtype=np.int32), np.array([o[2] for o in ops], dtype=np.int32),
-        np.array([o[3] for o in ops], dtype=np.int32)])
+    rounds = []
+    for h in sorted({o[0] for o in ops}):
+        level = [o for o in ops if o[0] == h]
+        for i in range(0, len(level), PROG_LANES):
+            words = [-1, 0] * PROG_LANES
+            for lane, (_, d, a, b) in enumerate(level[i:i + PROG_LANES]):
+                assert max(d, a, b) < (1 << 15), "tree slot index exceeds 15 bits"
+                words[2 * lane] = d
+                words[2 * lane + 1] = a | (b << 16)
+            rounds.append(words)
+    return np.array([len(rounds), 0] + [w for r in rounds for w in r], dtype=np.int32)
+
+
+def run_program(prog: np.ndarray, slots: list) -> None:
+    """Host replay of a _program (test helper)."""
+    n = int(prog[0])
+    for r in range(n):
+        words = prog[2 + 2 * PROG_LANES * r:2 + 2 * PROG_LANES * (r + 1)]
+        for lane in range(PROG_LANES):
+            d, w = int(words[2 * lane]), int(words[2 * lane + 1])
+            if d >= 0:
+                slots[d] = slots[w & 0xffff] + slots[w >> 16]
 
 
 def tree_split(flat: np.ndarray, ranges: list[tuple[int, int]]) -> list[np.ndarray]:
@@ -179,8 +199,8 @@ def tree_split(flat: np.ndarray, ranges: list[tuple[int, int]]) -> list[np.ndarr
     if L == 0:
         blocks = []
         for _ in range(C):
-            blocks.append(np.array([0, 0, TREE_HEADER, TREE_HEADER, TREE_HEADER + 2, TREE_HEADER + 4, 0, -1, 0, 0,
-                                    0, 0, 0, 0], dtype=np.int32))
+            blocks.append(np.array([0, 0, TREE_HEADER + 4, TREE_HEADER, TREE_HEADER + 2, TREE_HEADER + 4, 0, -1, 0,
+                                    0, 0, 0, 0, 0], dtype=np.int32))
         return blocks
     n_slots = 2 * L - 1
     lo = np.zeros(n_slots, dtype=np.int64)
@@ -278,15 +298,7 @@ def evaluate_split(flat: np.ndarray, blocks: list[np.ndarray], ranges, a) -> flo
             s += a[t]
         leaf.append(s)
 
-    def run(prog, slots):
-        nlev = int(prog[0])
-        off = prog[1:nlev + 2]
-        K = int(off[-1]) if nlev else 0
-        dst = prog[nlev + 2:nlev + 2 + K]
-        lef = prog[nlev + 2 + K:nlev + 2 + 2 * K]
-        rig = prog[nlev + 2 + 2 * K:nlev + 2 + 3 * K]
-        for k in range(K):
-            slots[int(dst[k])] = slots[int(lef[k])] + slots[int(rig[k])]
+    run = run_program
 
     TS = int(blocks[0][1])
     top = [0.0] * TS

@@ -155,3 +155,18 @@ def test_cluster_paths_vs_oracle(cuda_device, n, iters):
     r = frb.solve_batch(batch, config=cfg)[0]
     o = orc.solve(net, F, cfg)
     assert_matches(r, o.u, o.iters, o.converged, o.residual, o.r_ref, o.sigma, label=f"{n}^3")
+
+
+@pytest.mark.parametrize("name", ["c1_7x7x8_uniax", "lat8_seed5", "random60", "lat6_general_F"])
+def test_every_cta_size_matches_reference(cuda_device, name):
+    """Each CTA size selects a different kernel instantiation (register-held
+    DOFs per thread x thread bound); all of them must reproduce the
+    reference bit for bit (guards against a miscompiled instantiation)."""
+    case = gc.load(name)
+    batch = frb.pack_batch([case.network], [frb.AffineBC(case.F)])
+    nf = 3 * batch.problems[0].n_free_nodes
+    for T in (64, 96, 128, 224, 256, 320, 416, 512, 544, 640, 768, 1024):
+        if nf > fb.dofs_per_thread_cap(T) * T:
+            continue
+        r = fb.results_to_solve_results(batch, batch.to_device().solve(case.cfg, frb.TeamBatched(team_size=T)))[0]
+        assert_matches(r, *golden_expect(case), label=f"{name} T={T}")
