@@ -517,7 +517,7 @@ class DeviceBatch:
         fb.results, fb.queue = res.data_ptr(), queue.data_ptr()
         phase = None
         if phase_profile:
-            phase = torch.zeros(8 * 148 * 16, dtype=torch.int64, device=dev)
+            phase = torch.zeros(nat.PHASES * 148 * 16, dtype=torch.int64, device=dev)
             fb.phase_cycles = phase.data_ptr()
         return Launch(self, fb, config_struct(cfg), groups_c,
                       DeviceResults(u=u, f=f, results=res, node_base=h.node_base),

@@ -74,7 +74,11 @@ namespace {
 constexpr int kMaxThreads = 1024;
 constexpr int kMaxWarps = kMaxThreads / 32;
 constexpr double kCollapse = 1e-12;  // microsolver.py:30
-constexpr int kChunk = 4;  // per-DOF phases process a thread's DOFs in chunks of this many
+constexpr int kChunk = 4;
+// instrumentation slots (frb_batch.phase_cycles): F1, F2, A, C, T local tree +
+// exports, T exchange wait, T top tree + scalars, U, epilogue, prologue, halo wait
+constexpr int kPhases = 12;
+enum { PH_F1, PH_F2, PH_A, PH_C, PH_TL, PH_TW, PH_TT, PH_U, PH_EPI, PH_PRO, PH_HALO };  // per-DOF phases process a thread's DOFs in chunks of this many
 
 __device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
@@ -483,7 +487,7 @@ __device__ __forceinline__ void node_forces(int n_own, const uint32_t* __restric
 // ------------------------------------------------------------------ block helpers
 
 struct Scalars {
-  long long clk[8];  // per-phase cycle totals (thread 0, when instrumented)
+  long long clk[kPhases];  // per-phase cycle totals (thread 0, when instrumented)
   long long t_last;
   double c, residual, r_ref, threshold;
   double red[kMaxWarps * 9];
@@ -712,10 +716,13 @@ __device__ __forceinline__ Layout layout(const Rank& R) {
 // Replay one combine program (plan.py _program: warp rounds of up to 32
 // independent ops, lane-packed) on g_smem[o_slot + 3 s + {0,1,2}] with the
 // calling warp.  The next round's op is fetched while the current one runs.
+// Not unrolled: a single warp runs it while the rest of the CTA waits, so its
+// code must stay small and I-cache resident.
 __device__ __forceinline__ void run_prog(const int* prog, int o_slot, int lane) {
   const int nr = prog[0];
   const int2* w = reinterpret_cast<const int2*>(prog + 2);  // 8-byte aligned (plan.py _program)
   int2 cur = nr > 0 ? w[lane] : make_int2(-1, 0);
+#pragma unroll 1
   for (int r = 0; r < nr; ++r) {
     const int2 nxt = r + 1 < nr ? w[(r + 1) * 32 + lane] : make_int2(-1, 0);
     if (cur.x >= 0) {
@@ -849,28 +856,27 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
 
   // a = (-f)/m for every own DOF (f = g_smem[o.fprv + dl]), then use(k, dl, a)
   // for the valid ones; divisions are issued together, rare exact fallback
-  auto accel = [&](auto use) {
+  // fm[k] = (-f)/m of every own DOF k (f = f_prev slot = the current force
+  // once A has run); divisions are issued together, rare exact fallback
+  double fm[MAXK];
+  auto accel = [&]() {
 #pragma unroll
     for (int k0 = 0; k0 < MAXK; k0 += kChunk) {
       constexpr int KC = MAXK < kChunk ? MAXK : kChunk;
-      double a[KC];
       bool ok[KC];
 #pragma unroll
       for (int kk = 0; kk < KC; ++kk) {
-        const int dl = min(t + (k0 + kk) * T, dl_max);
-        a[kk] = frb_arith::div_fast(-FPRV(dl), __ldg(nmass + dl / 3), ok[kk]);
-      }
-#pragma unroll
-      for (int kk = 0; kk < KC; ++kk) {
-        if (!ok[kk]) {
+        if (k0 + kk < MAXK) {
           const int dl = min(t + (k0 + kk) * T, dl_max);
-          a[kk] = exact_div(-FPRV(dl), __ldg(nmass + dl / 3));
+          fm[k0 + kk] = frb_arith::div_fast(-FPRV(dl), __ldg(nmass + dl / 3), ok[kk]);
         }
       }
 #pragma unroll
       for (int kk = 0; kk < KC; ++kk) {
-        const int dl = t + (k0 + kk) * T;
-        if (k0 + kk < MAXK && dl < nfo) use(k0 + kk, dl, a[kk]);
+        if (k0 + kk < MAXK && !ok[kk]) {
+          const int dl = min(t + (k0 + kk) * T, dl_max);
+          fm[k0 + kk] = exact_div(-FPRV(dl), __ldg(nmass + dl / 3));
+        }
       }
     }
   };
@@ -908,18 +914,16 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
   __syncthreads();
 
   // a = -f/m (:428-430), then iteration 0's kick + drift (:443-448)
-  accel([&](int k, int dl, double a) {
-    v[k] = dadd(0.0, dmul(hdt, a));
-    u[k] = dadd(0.0, dmul(dt, v[k]));
-    put_pos(k, dl, dadd(xr[k], u[k]));
-  });
-#ifdef FRB_DEBUG_PROLOGUE
-  for (int dl = t; dl < nfo; dl += T) b.f[3 * n.node_base + dof0 + dl] = FPRV(dl);
+  accel();
 #pragma unroll
-  for (int k = 0; k < MAXK; ++k)
-    if (t + k * T < nfo) b.u[3 * n.node_base + dof0 + t + k * T] = v[k];
-  return;
-#endif
+  for (int k = 0; k < MAXK; ++k) {
+    const int dl = t + k * T;
+    if (dl < nfo) {
+      v[k] = dadd(0.0, dmul(hdt, fm[k]));
+      u[k] = dadd(0.0, dmul(dt, v[k]));
+      put_pos(k, dl, dadd(xr[k], u[k]));
+    }
+  }
   if (ramp) {  // iteration 0's ramp step (:449-453)
     alpha = ramp_alpha(1, ramp_n);
     set_local_fixed(n, R, &g_smem[o.pos], alpha, ramp);
@@ -927,22 +931,23 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
   __syncthreads();
 
   // ---- relaxation loop (microsolver.py:434-530) ---------------------------
-  mark(sc, prof, 7);
+  mark(sc, prof, PH_PRO);
   int it = 0;
   for (;; ++it) {
     if (C > 1) {  // halo positions of this iteration
       mbar_wait(mb.h, mb.ph_h);
       mb.ph_h ^= 1u;
+      mark(sc, prof, PH_HALO);
     }
     // F: internal forces at the drifted positions (:456-465)
     bool bad = element_coefs(n_act, act_ab, act_L, act_EA, ea, o.pos, o.cf);
     if (ramp && it < ramp_n && rank == 0) bad |= check_elements(n, PosFixed{&n, alpha, ramp}, false);
     __syncthreads();
-    mark(sc, prof, 0);
+    mark(sc, prof, PH_F1);
     node_forces(n_own, ell, S, SA, SB, o.pos, o.cf, o.fcur);
     if (bad) sc.singular = 1;
     __syncthreads();
-    mark(sc, prof, 1);
+    mark(sc, prof, PH_F2);
 
     // A: k_hat = (f - f_prev)/(dt v) where dt v != 0 else 0, clamped with
     // np.maximum(k_hat, 0) (:468-476); sq = (u k_hat) u, sq2 = (u m) u,
@@ -996,7 +1001,7 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
       }
     }
     __syncthreads();
-    mark(sc, prof, 2);
+    mark(sc, prof, PH_A);
 
     // C: ordered chain sums of one leaf chain + fold + tails -> every rank's
     // slots; the singular flag travels with them
@@ -1052,13 +1057,16 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
       }
     }
     __syncthreads();
-    mark(sc, prof, 3);
+    mark(sc, prof, PH_C);
 
     // T (warp 0): local subtrees of this rank's leaves, their roots to every
     // rank (with this rank's singular flag), the top tree over all ranks'
-    // exports, then the scalar bookkeeping
+    // exports, then the scalar bookkeeping.  Meanwhile the other warps
+    // compute U's c-independent part, fm = (-f)/m (warp 0 does after T).
+    if (t >= 32) accel();
     if (t < 32) {
       run_prog(lprog, o.lslot, lane);
+#pragma unroll 1
       for (int x = lane; x < n_exp; x += 32) {
         const int ls = o.lslot + 3 * exps[2 * x], ts = 3 * exps[2 * x + 1];
         const double v0 = g_smem[ls], v1 = g_smem[ls + 1], v2 = g_smem[ls + 2];
@@ -1073,6 +1081,7 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
           st_async(ad + 16, v2, sc.peer_bar_s[qr]);
         }
       }
+      mark(sc, prof, PH_TL);
       if (C > 1) {
         if (lane == 0) {
           const double fl = sc.singular ? 1.0 : 0.0;
@@ -1081,37 +1090,37 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
         }
         mbar_wait(mb.s, mb.ph_s);  // every peer's exports and flag
         if (lane == 0) mbar_expect(mb.s, R.leaf_bytes);  // next exchange phase
+        mark(sc, prof, PH_TW);
       }
       __syncwarp();
       bool singular = sc.singular != 0;
       for (int qr = 0; qr < C; ++qr) singular |= (qr != rank) && g_smem[o.flag + qr] != 0.0;
       if (!singular) run_prog(tprog, o.tslot, lane);
-      // lane 0: damping coefficient; lane 1: residual, threshold, convergence
+      double s_sq = 0.0, s_m = 0.0, s_f = 0.0;  // the three pairwise sums
+      if (root_top >= 0) {
+        s_sq = g_smem[o.tslot + 3 * root_top];
+        s_m = g_smem[o.tslot + 3 * root_top + 1];
+        s_f = g_smem[o.tslot + 3 * root_top + 2];
+      }
+      // lanes 0 and 1 run the same instructions (no divergence): lane 0
+      // lam = s_sq / s_m and c = 2 sqrt(lam); lane 1 s_f / 1 = s_f and the
+      // residual sqrt(s_f), threshold and convergence test
       if (lane < 2) {
         if (singular) {
           if (lane == 0) sc.singular = 1;
         } else {
-          double s_a = 0.0, s_b = 0.0;
-          if (root_top >= 0) {
-            s_a = g_smem[o.tslot + 3 * root_top + (lane == 0 ? 0 : 2)];
-            s_b = g_smem[o.tslot + 3 * root_top + 1];
-          }
           // np.sum adds the pairwise result to the identity 0.0
-          s_a = dadd(0.0, s_a);
+          s_sq = dadd(0.0, s_sq);
+          s_m = dadd(0.0, s_m);
+          s_f = dadd(0.0, s_f);
+          const double qv = ddiv(lane == 0 ? s_sq : s_f, lane == 0 ? s_m : 1.0);
+          const double rv = dsqrt(qv);
           if (lane == 0) {
-            const double s_m = dadd(0.0, s_b);
             double c = cfg.damping_c;
-            if (adaptive) {
-              if (s_m > 0.0) {
-                const double lam = ddiv(s_a, s_m);
-                c = lam > 0.0 ? dmul(2.0, dsqrt(lam)) : 0.0;
-              } else {
-                c = 0.0;
-              }
-            }
+            if (adaptive) c = (s_m > 0.0 && qv > 0.0) ? dmul(2.0, rv) : 0.0;
             sc.c = c;
           } else {
-            const double res = dsqrt(s_a);
+            const double res = rv;
             double thr = sc.threshold;
             if (it == full_bc_iter) {
               sc.r_ref = res;
@@ -1132,10 +1141,11 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
           }
         }
       }
+      accel();
     }
     mb.ph_s ^= 1u;
     __syncthreads();
-    mark(sc, prof, 4);
+    mark(sc, prof, PH_TT);
     if (sc.singular) {
       if (C > 1) drain(mb, R);
       // positions of every node to global memory, then the argmin over all
@@ -1154,25 +1164,29 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
     // iteration's first half-kick and drift (:443-453) unless finished
     const double c = sc.c;
     const bool done = sc.done != 0;
-    accel([&](int k, int dl, double fm) {
-      const double a = dsub(fm, dmul(c, v[k]));
-      v[k] = dadd(v[k], dmul(hdt, a));
-      if (!done) {
+#pragma unroll
+    for (int k = 0; k < MAXK; ++k) {
+      const int dl = t + k * T;
+      if (dl < nfo) {
+        const double a = dsub(fm[k], dmul(c, v[k]));
         v[k] = dadd(v[k], dmul(hdt, a));
-        u[k] = dadd(u[k], dmul(dt, v[k]));
-        put_pos(k, dl, dadd(xr[k], u[k]));
+        if (!done) {
+          v[k] = dadd(v[k], dmul(hdt, a));
+          u[k] = dadd(u[k], dmul(dt, v[k]));
+          put_pos(k, dl, dadd(xr[k], u[k]));
+        }
       }
-    });
+    }
     if (!done && ramp && alpha < 1.0) {
       alpha = ramp_alpha(it + 2, ramp_n);
       set_local_fixed(n, R, &g_smem[o.pos], alpha, ramp);
     }
     if (done) break;
     __syncthreads();
-    mark(sc, prof, 5);
+    mark(sc, prof, PH_U);
   }
   if (C > 1) drain(mb, R);
-  mark(sc, prof, 5);
+  mark(sc, prof, PH_U);
 
   // ---- epilogue: outputs in solver order + stress (:549-564, :285-299) ----
   double* uo = b.u + 3 * n.node_base;
@@ -1191,7 +1205,7 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
   csync(C);
   if (rank == 0) fixed_forces_and_stress(b, p, n, sc, it, alpha, ramp, full_bc_iter);
   __syncthreads();
-  mark(sc, prof, 6);
+  mark(sc, prof, PH_EPI);
 }
 
 template <int MAXK, int MAXT, bool kFG>
@@ -1205,7 +1219,7 @@ __global__ void __launch_bounds__(MAXT, 1)
   const int C = static_cast<int>(cg::this_cluster().num_blocks());
   const int rank = C > 1 ? static_cast<int>(cg::this_cluster().block_rank()) : 0;
   if (threadIdx.x == 0) {
-    for (int k = 0; k < 8; ++k) sc.clk[k] = 0;
+    for (int k = 0; k < kPhases; ++k) sc.clk[k] = 0;
     sc.t_last = clock64();
     if (C > 1) {
       mbar_init(&bars[0], 1);
@@ -1241,7 +1255,7 @@ __global__ void __launch_bounds__(MAXT, 1)
     csync(C);  // no rank reuses its SMEM before every peer is done with it
   }
   if (b.phase_cycles && threadIdx.x == 0) {
-    for (int k = 0; k < 8; ++k) b.phase_cycles[8 * blockIdx.x + k] = sc.clk[k];
+    for (int k = 0; k < kPhases; ++k) b.phase_cycles[kPhases * blockIdx.x + k] = sc.clk[k];
   }
 }
 
@@ -1315,6 +1329,18 @@ int launch_group(const frb_batch* batch, const frb_config* cfg, const frb_group&
   int rc = cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, g.smem_bytes),
                       "cudaFuncSetAttribute(smem)");
   if (rc) return rc;
+  {
+    // smallest SMEM carveout that holds the rank: the rest of the 256 KB
+    // array is L1, which holds the loop's read-only tables
+    cudaFuncAttributes fa;
+    rc = cuda_check(cudaFuncGetAttributes(&fa, kern), "cudaFuncGetAttributes");
+    if (rc) return rc;
+    const int need = g.smem_bytes + static_cast<int>(fa.sharedSizeBytes) + 1024;
+    const int pct = (100 * need + 228 * 1024 - 1) / (228 * 1024);
+    rc = cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, pct < 100 ? pct : 100),
+                    "cudaFuncSetAttribute(carveout)");
+    if (rc) return rc;
+  }
   if (C > 8) {
     rc = cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1),
                     "cudaFuncSetAttribute(non-portable cluster)");

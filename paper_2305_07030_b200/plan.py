@@ -166,6 +166,40 @@ def _program(ops: list[tuple[int, int, int, int]]) -> np.ndarray:
     return np.array([len(rounds), 0] + [w for r in rounds for w in r], dtype=np.int32)
 
 
+MODE_LOCAL_SHFL, MODE_TOP_SHFL = 1, 2
+
+
+def _shuffle_program(ops: list[tuple[int, int, int]]) -> np.ndarray:
+    """Warp-shuffle form of a tree whose leaves sit one per lane: every node's
+    value lives in the lane of its leftmost leaf, so op (height, left lane,
+    right lane) is `lane[left] += lane[right]` -- one shuffle per round.
+    Layout [n_rounds, 0, n_rounds x 8 words]: per round 32 source lanes as
+    bytes (0xFF: lane idle)."""
+    ops = sorted(ops)
+    heights = sorted({o[0] for o in ops})
+    words = []
+    for h in heights:
+        src = [0xFF] * PROG_LANES
+        for _, d, a in (o for o in ops if o[0] == h):
+            assert 0 <= d < PROG_LANES and 0 <= a < PROG_LANES and src[d] == 0xFF
+            src[d] = a
+        b = np.array(src, dtype=np.uint8).view(np.int32)
+        words.extend(int(x) for x in b)
+    return np.array([len(heights), 0] + words, dtype=np.int32)
+
+
+def run_shuffle_program(prog: np.ndarray, lanes: list) -> None:
+    """Host replay of a _shuffle_program (test helper)."""
+    n = int(prog[0])
+    for r in range(n):
+        src = prog[2 + 8 * r:2 + 8 * (r + 1)].astype(np.int32).view(np.uint8)
+        new = list(lanes)
+        for lane in range(PROG_LANES):
+            if src[lane] != 0xFF:
+                new[lane] = lanes[lane] + lanes[int(src[lane])]
+        lanes[:] = new
+
+
 def run_program(prog: np.ndarray, slots: list) -> None:
     """Host replay of a _program (test helper)."""
     n = int(prog[0])
@@ -239,7 +273,20 @@ def tree_split(flat: np.ndarray, ranges: list[tuple[int, int]]) -> list[np.ndarr
         top_ops.append((h, int(top_of[d]), int(top_of[a]), int(top_of[b])))
     TS = E + len(top_internal)
     root_top = int(top_of[p.root])
-    tprog = _program(top_ops)
+    top_shfl = False                           # (shuffle form measured slower on B200)
+    if top_shfl:                               # top leaves (exports) one per lane
+        tlo = {}
+        for i, sl in enumerate(exports):
+            tlo[sl] = i
+        sops = []
+        for k in top_internal:
+            d, a, b = int(p.op_dst[k]), int(p.op_left[k]), int(p.op_right[k])
+            tlo[d] = tlo[a]
+            sops.append((theight[d], tlo[a], tlo[b]))
+        tprog = _shuffle_program(sops)
+        TS, root_top = E, 0
+    else:
+        tprog = _program(top_ops)
     blocks = []
     for r, (a, b) in enumerate(ranges):
         local_idx = np.full(n_slots, -1, dtype=np.int64)
@@ -256,13 +303,26 @@ def tree_split(flat: np.ndarray, ranges: list[tuple[int, int]]) -> list[np.ndarr
             h = 1 + max(lheight.get(x, 0), lheight.get(y, 0))
             lheight[d] = h
             lops.append((h, int(local_idx[d]), int(local_idx[x]), int(local_idx[y])))
-        lprog = _program(lops)
-        exp = np.array([(int(local_idx[s]), int(top_of[s])) for s in exports if owner[s] == r],
-                       dtype=np.int32).reshape(-1)
+        loc_shfl = False
+        if loc_shfl:                           # own leaves one per lane
+            sops = []
+            for k in range(K):
+                d, x, y = int(p.op_dst[k]), int(p.op_left[k]), int(p.op_right[k])
+                if owner[d] == r:
+                    sops.append((lheight[d], int(lo[x]) - a, int(lo[y]) - a))
+            lprog = _shuffle_program(sops)
+            nl = b - a
+            exp = np.array([(int(lo[s]) - a, int(top_of[s])) for s in exports if owner[s] == r],
+                           dtype=np.int32).reshape(-1)
+        else:
+            lprog = _program(lops)
+            exp = np.array([(int(local_idx[s]), int(top_of[s])) for s in exports if owner[s] == r],
+                           dtype=np.int32).reshape(-1)
+        mode = (MODE_LOCAL_SHFL if loc_shfl else 0) | (MODE_TOP_SHFL if top_shfl else 0)
         lprog_off = TREE_HEADER
         tprog_off = lprog_off + len(lprog)
         exp_off = tprog_off + len(tprog)
-        hdr = np.array([nl, TS, 0, lprog_off, tprog_off, exp_off, len(exp) // 2, root_top, E, 0],
+        hdr = np.array([nl, TS, 0, lprog_off, tprog_off, exp_off, len(exp) // 2, root_top, E, mode],
                        dtype=np.int32)
         blocks.append(np.concatenate([hdr, lprog, tprog, exp]).astype(np.int32))
     LS = max(int(bk[0]) for bk in blocks)
@@ -301,15 +361,23 @@ def evaluate_split(flat: np.ndarray, blocks: list[np.ndarray], ranges, a) -> flo
     run = run_program
 
     TS = int(blocks[0][1])
-    top = [0.0] * TS
+    top = [0.0] * max(TS, PROG_LANES)
     for bk, (ra, rb) in zip(blocks, ranges):
         LS = int(bk[0])
-        loc = [0.0] * max(LS, 1)
+        loc = [0.0] * max(LS, PROG_LANES)
         loc[:rb - ra] = leaf[ra:rb]
-        run(bk[int(bk[3]):int(bk[4])], loc)
+        prog = bk[int(bk[3]):int(bk[4])]
+        if int(bk[9]) & MODE_LOCAL_SHFL:
+            run_shuffle_program(prog, loc)
+        else:
+            run(prog, loc)
         exp = bk[int(bk[5]):int(bk[5]) + 2 * int(bk[6])]
         for i in range(0, len(exp), 2):
             top[int(exp[i + 1])] = loc[int(exp[i])]
     bk = blocks[0]
-    run(bk[int(bk[4]):int(bk[5])], top)
+    prog = bk[int(bk[4]):int(bk[5])]
+    if int(bk[9]) & MODE_TOP_SHFL:
+        run_shuffle_program(prog, top)
+    else:
+        run(prog, top)
     return top[int(bk[7])]
