@@ -646,7 +646,8 @@ __device__ __forceinline__ T* peer(T* p, int q) {
 // 285-299; deterministic order, tolerance-only vs the reference's BLAS) and
 // the result record.
 __device__ __noinline__ void fixed_forces_and_stress(const frb_batch& b, int p, const Net& n, Scalars& sc,
-                                                     int it, double alpha, bool ramp, int full_bc_iter) {
+                                                     int it, double alpha, bool ramp, int full_bc_iter,
+                                                     bool energy, const double* w) {
   const int T = blockDim.x, t = threadIdx.x;
   double* uo = b.u + 3 * n.node_base;
   double* fo = b.f + 3 * n.node_base;
@@ -677,8 +678,55 @@ __device__ __noinline__ void fixed_forces_and_stress(const frb_batch& b, int p, 
     r.bad_element = -1;
     r.final_residual = sc.residual;
     r.r_ref = (full_bc_iter <= it) ? sc.r_ref : qnan();
+    // energy_balance (microsolver.py:274-282): w = {w_kin, w_int, w_damp, w_ext}
     r.energy_residual = qnan();
-    for (int e = 0; e < 4; ++e) r.energy[e] = 0.0;
+    for (int e = 0; e < 4; ++e) r.energy[e] = energy ? w[e] : 0.0;
+    if (energy) {
+      const double defect = fabs(dsub(dsub(dsub(w[3], w[1]), w[0]), w[2]));
+      double den = fabs(w[3]);
+      if (fabs(w[1]) > den) den = fabs(w[1]);
+      if (w[0] > den) den = w[0];
+      if (1e-30 > den) den = 1e-30;  // ENERGY_FLOOR, microsolver.py:29
+      r.energy_residual = ddiv(defect, den);
+    }
+  }
+}
+
+// Work ledger terms at the fixed nodes (rank 0, every thread; positions of
+// all nodes in posg): the reactions f_fix from the incidence lists, then
+//   mode 0: sum f_fix . u_presc                        (initial BC step)
+//   mode 1: store f_fix as the previous reactions       (ramp, iteration -1)
+//   mode 2: sum f_fix . du and sum f_prev_fix . du with du = d_alpha u_presc,
+//           then store f_fix                            (ramp iterations)
+// f_prev_fix lives in the fixed-DOF part of the u output (written only by
+// the epilogue).  Returns {sum1, sum2} in thread 0 (any order: the
+// reference's np.dot is BLAS-ordered, the ledger is tolerance-only).
+__device__ __noinline__ void energy_fixed(const frb_batch& b, const Net& n, Scalars& sc, int mode, double d_alpha,
+                                          double* out) {
+  double s9[9];
+#pragma unroll
+  for (int r = 0; r < 9; ++r) s9[r] = 0.0;
+  double* fprev_fix = b.u + 3 * n.node_base;
+  const PosGlobalAll G{n.posg};
+  for (int i = n.NF + threadIdx.x; i < n.N; i += blockDim.x) {
+    double f3[3];
+    node_force_csr(n, G, i, f3[0], f3[1], f3[2]);
+    for (int j = 0; j < 3; ++j) {
+      const double up = presc(n, i, j);
+      if (mode == 0) {
+        s9[0] = dadd(s9[0], dmul(f3[j], up));
+      } else if (mode == 2) {
+        const double du = dmul(d_alpha, up);
+        s9[0] = dadd(s9[0], dmul(f3[j], du));
+        s9[1] = dadd(s9[1], dmul(fprev_fix[3 * i + j], du));
+      }
+      fprev_fix[3 * i + j] = f3[j];
+    }
+  }
+  block_sum9(s9, sc);
+  if (threadIdx.x == 0) {
+    out[0] = s9[0];
+    out[1] = s9[1];
   }
 }
 
@@ -709,7 +757,7 @@ __device__ __forceinline__ Layout layout(const Rank& R) {
   o.lslot = o.cf + R.CF;
   o.tslot = o.lslot + 3 * R.LS;
   o.flag = o.tslot + 3 * R.TS;
-  o.prog = 2 * (o.flag + 16);
+  o.prog = 2 * (o.flag + 64);  // flags[16], energy partials [16][3]
   return o;
 }
 
@@ -746,10 +794,10 @@ struct Mbar {
 
 // Complete the two phases posted for an iteration that will not run, so the
 // barriers are idle for the next problem (see the header comment).
-__device__ __forceinline__ void drain(Mbar& mb, const Rank& R) {
+__device__ __forceinline__ void drain(Mbar& mb, uint32_t halo_bytes, uint32_t leaf_bytes) {
   if (threadIdx.x == 0) {
-    mbar_complete(mb.h, R.halo_bytes);
-    mbar_complete(mb.s, R.leaf_bytes);
+    mbar_complete(mb.h, halo_bytes);
+    mbar_complete(mb.s, leaf_bytes);
   }
   mbar_wait(mb.h, mb.ph_h);
   mbar_wait(mb.s, mb.ph_s);
@@ -806,6 +854,15 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
   const double dt = n.dt, hdt = n.hdt;
   double alpha = ramp ? -1.0 : 1.0;  // -1: fixed nodes still at their zero init
   const bool prof = b.phase_cycles != nullptr;
+  // work ledger (energy_check_interval > 0, used as a flag like the
+  // reference, microsolver.py:395, 510): rank 0's thread 0 keeps
+  // w = {w_kin, w_int, w_damp, w_ext}; the other ranks send it their
+  // per-iteration partial dots with the exchange
+  const bool energy = cfg.energy_check_interval > 0;
+  const bool eramp = energy && ramp;  // reactions at the ramped fixed nodes each ramp step
+  const uint32_t leaf_bytes = R.leaf_bytes + ((energy && rank == 0) ? 24u * static_cast<uint32_t>(C - 1) : 0u);
+  double w[4] = {0.0, 0.0, 0.0, 0.0};
+  double alpha_prev = 0.0;  // alpha of the previous step (d_alpha, microsolver.py:451)
 
   // own DOF dl = t + k*T (local DOF; global DOF dof0 + dl)
   double u[MAXK], v[MAXK];
@@ -840,6 +897,7 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
   // new position of own DOF k (= dl): local slot + the halo copies of peers
   auto put_pos = [&](int k, int dl, double x) {
     g_smem[o.pos + dl] = x;
+    if (eramp && alpha < 1.0) n.posg[dof0 + dl] = x;  // ramp reactions read every position
     if (C > 1 && ((sendbits >> k) & 1u)) {
       const int node = dl / 3, axis = dl - 3 * node;
       const int2 tg = __ldg(send + node);
@@ -885,7 +943,7 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
   // post the first halo and leaf-sum phases before any peer may send
   if (C > 1 && t == 0) {
     mbar_expect(mb.h, R.halo_bytes);
-    mbar_expect(mb.s, R.leaf_bytes);
+    mbar_expect(mb.s, leaf_bytes);
   }
   for (int l = t; l < R.n_local; l += T) {
     const int g = l < n_own ? R.node0 + l : R.halo_g[l - n_own];
@@ -900,7 +958,7 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
   if (check_elements(n, PosGlobalAll{n.posg}, true)) sc.singular = 1;
   __syncthreads();
   if (sc.singular) {
-    if (C > 1) drain(mb, R);
+    if (C > 1) drain(mb, R.halo_bytes, leaf_bytes);
     const int bad = singular_argmin(n, PosGlobalAll{n.posg}, sc);
     if (rank == 0 && t == 0) write_singular(b, p, bad, 0);
     return;
@@ -912,6 +970,16 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
   __syncthreads();
   for (int dl = t; dl < nfo; dl += T) SET_FPRV(dl, g_smem[o.fcur + dl]);
   __syncthreads();
+  if (energy && rank == 0) {  // initial BC step work (:421-425), or the reactions before the ramp
+    double e2[2];
+    energy_fixed(b, n, sc, ramp ? 1 : 0, 0.0, e2);
+    if (t == 0 && !ramp) {
+      const double step = dmul(0.5, e2[0]);
+      w[3] = dadd(w[3], step);
+      w[1] = dadd(w[1], step);
+    }
+  }
+  if (eramp) csync(C);  // rank 0 has read the initial positions before any rank drifts
 
   // a = -f/m (:428-430), then iteration 0's kick + drift (:443-448)
   accel();
@@ -927,6 +995,7 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
   if (ramp) {  // iteration 0's ramp step (:449-453)
     alpha = ramp_alpha(1, ramp_n);
     set_local_fixed(n, R, &g_smem[o.pos], alpha, ramp);
+    if (energy) set_fixed_positions(n, rank, alpha, ramp);
   }
   __syncthreads();
 
@@ -938,6 +1007,16 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
       mbar_wait(mb.h, mb.ph_h);
       mb.ph_h ^= 1u;
       mark(sc, prof, PH_HALO);
+    }
+    double wfix = 0.0;  // ramp work at the fixed nodes this step (rank 0, thread 0)
+    if (eramp && it < ramp_n) {
+      csync(C);  // every rank's positions of this step are in posg
+      if (rank == 0) {
+        double e2[2];
+        energy_fixed(b, n, sc, 2, dsub(alpha, alpha_prev), e2);
+        if (t == 0) wfix = dmul(0.5, dadd(e2[0], e2[1]));
+      }
+      alpha_prev = alpha;
     }
     // F: internal forces at the drifted positions (:456-465)
     bool bad = element_coefs(n_act, act_ab, act_L, act_EA, ea, o.pos, o.cf);
@@ -954,6 +1033,7 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
     // ff = f f (:489).  Outputs: sq -> own position slot, sq2 -> cf,
     // ff -> fcur, f -> fprv.
     if (C > 1 && t == 0) mbar_expect(mb.h, R.halo_bytes);  // next halo phase
+    double es[3] = {0.0, 0.0, 0.0};
 #pragma unroll
     for (int k0 = 0; k0 < MAXK; k0 += kChunk) {
       constexpr int KC = MAXK < kChunk ? MAXK : kChunk;
@@ -996,8 +1076,22 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
             g_smem[o.cf + dl] = dmul(dmul(u[k], m[kk]), u[k]);
           }
           g_smem[o.fcur + dl] = dmul(f[kk], f[kk]);
+          if (energy) {  // f . v_half, f_prev . v_half, (m v_half) . v_half (:538-544)
+            const double vh = v[k];
+            es[0] = dadd(es[0], dmul(f[kk], vh));
+            es[1] = dadd(es[1], dmul(FPRV(dl), vh));
+            es[2] = dadd(es[2], dmul(dmul(m[kk], vh), vh));
+          }
           SET_FPRV(dl, f[kk]);
         }
+      }
+    }
+    if (energy) {  // warp partials of the ledger dots -> sc.red
+#pragma unroll
+      for (int e = 0; e < 3; ++e) {
+        double x = es[e];
+        for (int sh = 16; sh > 0; sh >>= 1) x = dadd(x, __shfl_down_sync(0xffffffffu, x, sh));
+        if (lane == 0) sc.red[(t >> 5) * 9 + e] = x;
       }
     }
     __syncthreads();
@@ -1082,6 +1176,15 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
         }
       }
       mark(sc, prof, PH_TL);
+      if (energy && lane == 0) {  // this rank's ledger dots: own slot, and rank 0's
+        double e3[3] = {0.0, 0.0, 0.0};
+        for (int wp = 0; wp < (T + 31) / 32; ++wp)
+          for (int e = 0; e < 3; ++e) e3[e] = dadd(e3[e], sc.red[wp * 9 + e]);
+        for (int e = 0; e < 3; ++e) g_smem[o.flag + 16 + 3 * rank + e] = e3[e];
+        if (rank != 0)
+          for (int e = 0; e < 3; ++e)
+            st_async(sc.peer_smem[0] + peer_flag + 8u * (16 + 3 * rank + e), e3[e], sc.peer_bar_s[0]);
+      }
       if (C > 1) {
         if (lane == 0) {
           const double fl = sc.singular ? 1.0 : 0.0;
@@ -1089,7 +1192,7 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
             if (qr != rank) st_async(sc.peer_smem[qr] + peer_flag + 8u * rank, fl, sc.peer_bar_s[qr]);
         }
         mbar_wait(mb.s, mb.ph_s);  // every peer's exports and flag
-        if (lane == 0) mbar_expect(mb.s, R.leaf_bytes);  // next exchange phase
+        if (lane == 0) mbar_expect(mb.s, leaf_bytes);  // next exchange phase
         mark(sc, prof, PH_TW);
       }
       __syncwarp();
@@ -1119,6 +1222,17 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
             double c = cfg.damping_c;
             if (adaptive) c = (s_m > 0.0 && qv > 0.0) ? dmul(2.0, rv) : 0.0;
             sc.c = c;
+            if (energy && rank == 0) {  // _accumulate_energy (microsolver.py:533-546), ranks in order
+              double d[3] = {0.0, 0.0, 0.0};
+              for (int qr = 0; qr < C; ++qr)
+                for (int e = 0; e < 3; ++e) d[e] = dadd(d[e], g_smem[o.flag + 16 + 3 * qr + e]);
+              w[1] = dadd(w[1], dmul(0.5, dmul(dt, dadd(d[0], d[1]))));
+              if (wfix != 0.0 || (ramp && it < ramp_n)) {
+                w[1] = dadd(w[1], wfix);
+                w[3] = dadd(w[3], wfix);
+              }
+              w[2] = dadd(w[2], dmul(dmul(c, dt), d[2]));
+            }
           } else {
             const double res = rv;
             double thr = sc.threshold;
@@ -1147,7 +1261,7 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
     __syncthreads();
     mark(sc, prof, PH_TT);
     if (sc.singular) {
-      if (C > 1) drain(mb, R);
+      if (C > 1) drain(mb, R.halo_bytes, leaf_bytes);
       // positions of every node to global memory, then the argmin over all
       // elements (each rank redundantly; rank 0 reports)
 #pragma unroll
@@ -1180,12 +1294,13 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
     if (!done && ramp && alpha < 1.0) {
       alpha = ramp_alpha(it + 2, ramp_n);
       set_local_fixed(n, R, &g_smem[o.pos], alpha, ramp);
+      if (energy) set_fixed_positions(n, rank, alpha, ramp);
     }
     if (done) break;
     __syncthreads();
     mark(sc, prof, PH_U);
   }
-  if (C > 1) drain(mb, R);
+  if (C > 1) drain(mb, R.halo_bytes, leaf_bytes);
   mark(sc, prof, PH_U);
 
   // ---- epilogue: outputs in solver order + stress (:549-564, :285-299) ----
@@ -1202,8 +1317,28 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
     }
   }
   set_fixed_positions(n, rank, alpha, ramp);
+  if (energy) {  // w_kin = 0.5 (m v) . v (:546): rank partials into rank 0's slots
+    double ek = 0.0;
+#pragma unroll
+    for (int k = 0; k < MAXK; ++k)
+      if (t + k * T < nfo) ek = dadd(ek, dmul(dmul(__ldg(nmass + (t + k * T) / 3), v[k]), v[k]));
+    for (int sh = 16; sh > 0; sh >>= 1) ek = dadd(ek, __shfl_down_sync(0xffffffffu, ek, sh));
+    if (lane == 0) sc.red[(t >> 5) * 9] = ek;
+    __syncthreads();
+    if (t == 0) {
+      double e = 0.0;
+      for (int wp = 0; wp < (T + 31) / 32; ++wp) e = dadd(e, sc.red[wp * 9]);
+      double* dst = &g_smem[o.flag + 16 + 3 * rank];
+      *(C > 1 ? peer(dst, 0) : dst) = e;
+    }
+  }
   csync(C);
-  if (rank == 0) fixed_forces_and_stress(b, p, n, sc, it, alpha, ramp, full_bc_iter);
+  if (rank == 0 && energy && t == 0) {
+    double e = 0.0;
+    for (int qr = 0; qr < C; ++qr) e = dadd(e, g_smem[o.flag + 16 + 3 * qr]);
+    w[0] = dmul(0.5, e);
+  }
+  if (rank == 0) fixed_forces_and_stress(b, p, n, sc, it, alpha, ramp, full_bc_iter, energy, w);
   __syncthreads();
   mark(sc, prof, PH_EPI);
 }
@@ -1426,7 +1561,7 @@ int64_t frb_rank_smem_bytes(int32_t n_pos, int32_t n_own, int32_t n_act, int32_t
                             int32_t fprv_global) {
   const int64_t nf = 3 * static_cast<int64_t>(n_own);
   return 8 * (3 * static_cast<int64_t>(n_pos) + (fprv_global ? 1 : 2) * nf + (nf > n_act ? nf : n_act) +
-              3 * static_cast<int64_t>(n_slots) + 16) +
+              3 * static_cast<int64_t>(n_slots) + 64) +
          4 * ((static_cast<int64_t>(n_prog) + 1) & ~1LL);
 }
 
@@ -1437,7 +1572,6 @@ int frb_solve_batch(const frb_batch* batch, const frb_config* cfg, void* stream)
   if (batch->n_problems < 0 || batch->n_groups < 0) return set_err(FRB_E_INVALID, "negative counts");
   if (batch->n_problems == 0) return FRB_OK;
   if (!batch->groups || !batch->queue || !batch->work) return set_err(FRB_E_INVALID, "groups/queue/work missing");
-  if (cfg->energy_check_interval > 0) return set_err(FRB_E_UNSUPPORTED, "energy ledger not in this build");
   if (cfg->max_iters <= 0) return set_err(FRB_E_INVALID, "max_iters must be > 0");
   int dev = 0, optin = 0;
   int rc = cuda_check(cudaGetDevice(&dev), "cudaGetDevice");

@@ -170,3 +170,17 @@ def test_every_cta_size_matches_reference(cuda_device, name):
             continue
         r = fb.results_to_solve_results(batch, batch.to_device().solve(case.cfg, frb.TeamBatched(team_size=T)))[0]
         assert_matches(r, *golden_expect(case), label=f"{name} T={T}")
+
+
+@pytest.mark.parametrize("n,ramp", [(6, 0), (6, 4), (14, 0), (14, 6)])
+def test_energy_ledger_vs_oracle(cuda_device, n, ramp):
+    """Work ledger on one CTA and on a 2-CTA cluster, with and without the BC
+    ramp: same iterate bit for bit (the ledger never feeds back), energy
+    residual within 1e-10 (the reference's np.dot is BLAS-ordered)."""
+    net = frb.generate_lattice(n, n, n, 0.3, 2)
+    F = np.diag([1.1, 1.0, 1.05])
+    cfg = frb.SolverConfig(energy_check_interval=1, bc_ramp_iters=ramp, max_iters=400)
+    r = frb.dynamic_relaxation_solve(net, frb.AffineBC(F), cfg)
+    o = orc.solve(net, F, cfg)
+    assert_matches(r, o.u, o.iters, o.converged, o.residual, o.r_ref, o.sigma, label=f"{n}/{ramp}")
+    assert abs(r.energy_residual - o.energy_residual) <= 1e-10 * abs(o.energy_residual)
