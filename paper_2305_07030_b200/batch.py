@@ -292,12 +292,13 @@ def _cat(parts, dtype, width=None):
 
 def _group_threads(max_own_dofs: int, max_rank_leaves: int, n_problems: int, cluster: int,
                    fprv_global: bool = False) -> int:
-    """Threads per CTA for a group: 8 per pairwise leaf at least, few enough
-    DOFs per thread for the register budget; more threads when there are too
-    few problems to fill the GPU (latency), fewer when many small problems
-    can share an SM."""
+    """Threads per CTA for a group: 8 per pairwise leaf of a rank (one per
+    accumulator chain) and at most 16 register-held DOFs per thread; more
+    threads when too few problems fill the GPU (latency matters more than
+    throughput then).  Measured on c2 (15^3, 2 ranks): 256 threads beat 512
+    (82.9 vs 84.9 ms; tools/sweep_c2.py)."""
     need = max(64, 8 * max_rank_leaves, math.ceil(max_own_dofs / 16))
-    if max_own_dofs > 1024 or n_problems * cluster < 148:
+    if n_problems * cluster < 148:
         need = max(need, min(512, 32 * math.ceil(max_own_dofs / 32)))
     if fprv_global:  # the global-f_prev kernels exist for 768 and 1024 threads
         need = max(need, 768)

@@ -805,7 +805,7 @@ __device__ __forceinline__ void drain(Mbar& mb, uint32_t halo_bytes, uint32_t le
   mb.ph_s ^= 1u;
 }
 
-template <int MAXK, bool kFG>
+template <int MAXK, bool kFG, bool kEnergy>
 __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, int rank, Scalars& sc, Mbar& mb,
                               const Net& n, const Rank& R) {
   const int T = blockDim.x, t = threadIdx.x, lane = t & 31;
@@ -858,7 +858,7 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
   // reference, microsolver.py:395, 510): rank 0's thread 0 keeps
   // w = {w_kin, w_int, w_damp, w_ext}; the other ranks send it their
   // per-iteration partial dots with the exchange
-  const bool energy = cfg.energy_check_interval > 0;
+  constexpr bool energy = kEnergy;  // == (cfg.energy_check_interval > 0), dispatched per kernel
   const bool eramp = energy && ramp;  // reactions at the ramped fixed nodes each ramp step
   const uint32_t leaf_bytes = R.leaf_bytes + ((energy && rank == 0) ? 24u * static_cast<uint32_t>(C - 1) : 0u);
   double w[4] = {0.0, 0.0, 0.0, 0.0};
@@ -1343,7 +1343,7 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
   mark(sc, prof, PH_EPI);
 }
 
-template <int MAXK, int MAXT, bool kFG>
+template <int MAXK, int MAXT, bool kFG, bool kEnergy>
 __global__ void __launch_bounds__(MAXT, 1)
     frb_relax_kernel(const __grid_constant__ frb_batch b, const __grid_constant__ frb_config cfg, int first,
                      int count, int32_t* queue) {
@@ -1386,7 +1386,7 @@ __global__ void __launch_bounds__(MAXT, 1)
       sc.threshold = __longlong_as_double(0x7ff0000000000000ULL);  // +inf until set
     }
     __syncthreads();
-    solve_problem<MAXK, kFG>(b, cfg, p, rank, sc, mb, net, rk);
+    solve_problem<MAXK, kFG, kEnergy>(b, cfg, p, rank, sc, mb, net, rk);
     csync(C);  // no rank reuses its SMEM before every peer is done with it
   }
   if (b.phase_cycles && threadIdx.x == 0) {
@@ -1456,10 +1456,10 @@ int cuda_check(cudaError_t e, const char* where) {
 
 int dofs_cap(int threads) { return threads > 768 ? 8 : threads > 512 ? 12 : 16; }
 
-template <int MAXK, int MAXT, bool kFG>
+template <int MAXK, int MAXT, bool kFG, bool kEnergy = false>
 int launch_group(const frb_batch* batch, const frb_config* cfg, const frb_group& g, int32_t* queue,
-                 cudaStream_t s) {
-  auto kern = frb_relax_kernel<MAXK, MAXT, kFG>;
+                 cudaStream_t s, int threads = 0) {
+  auto kern = frb_relax_kernel<MAXK, MAXT, kFG, kEnergy>;
   const int C = g.cluster;
   int rc = cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, g.smem_bytes),
                       "cudaFuncSetAttribute(smem)");
@@ -1487,7 +1487,7 @@ int launch_group(const frb_batch* batch, const frb_config* cfg, const frb_group&
   attr[0].val.clusterDim.x = C;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
-  lc.blockDim = dim3(g.block_threads);
+  lc.blockDim = dim3(threads > 0 ? threads : g.block_threads);
   lc.dynamicSmemBytes = g.smem_bytes;
   lc.stream = s;
   lc.attrs = attr;
@@ -1587,6 +1587,25 @@ int frb_solve_batch(const frb_batch* batch, const frb_config* cfg, void* stream)
     if (g.block_threads < 32 || g.block_threads > kMaxThreads || g.block_threads % 32)
       return set_err(FRB_E_INVALID, "block_threads must be a multiple of 32 in [32, 1024]");
     if (g.smem_bytes > optin) return set_err(FRB_E_TOO_LARGE, "a rank exceeds shared memory per CTA");
+    if (cfg->energy_check_interval > 0) {
+      // work-ledger kernels (a diagnostic, kept out of the production
+      // kernels' code): CTAs of at most 512 threads, up to 16 DOFs each
+      const int T = g.block_threads < 512 ? g.block_threads : 512;
+      const int ke = (g.max_own_dofs + T - 1) / T;
+      if (ke > 16) return set_err(FRB_E_TOO_LARGE, "too many free DOFs per thread for the ledger kernels");
+      int32_t* q = batch->queue + gi;
+      if (g.fprv_global) {
+        rc = ke <= 4   ? launch_group<4, 512, true, true>(batch, cfg, g, q, s, T)
+             : ke <= 8 ? launch_group<8, 512, true, true>(batch, cfg, g, q, s, T)
+                       : launch_group<16, 512, true, true>(batch, cfg, g, q, s, T);
+      } else {
+        rc = ke <= 4   ? launch_group<4, 512, false, true>(batch, cfg, g, q, s, T)
+             : ke <= 8 ? launch_group<8, 512, false, true>(batch, cfg, g, q, s, T)
+                       : launch_group<16, 512, false, true>(batch, cfg, g, q, s, T);
+      }
+      if (rc) return rc;
+      continue;
+    }
     const int k = (g.max_own_dofs + g.block_threads - 1) / g.block_threads;
     if (k > dofs_cap(g.block_threads)) return set_err(FRB_E_TOO_LARGE, "too many free DOFs per thread");
     if (g.block_threads <= 256) rc = dispatch_k<256>(batch, cfg, g, batch->queue + gi, s, k);
