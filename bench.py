@@ -46,20 +46,54 @@ SHEAR = np.eye(3) + 0.2 * np.outer([1, 0, 0], [0, 1, 0])
 L2_FLUSH_BYTES = 256 << 20
 
 
-def config_networks(name: str, rank: int, world: int):
+C5_TOTAL = 16384
+
+
+def shard_indices(name: str, rank: int, world: int) -> list[int]:
+    """Network indices a rank solves: c2 is weak-scaled (256 per
+    GPU), c3/c4 are strided (iteration counts vary by size/load), c5 is split
+    into contiguous shards of the FE2 macro-step's 16,384 networks."""
+    if name == "c1":
+        return [0]
+    if name == "c2":
+        return list(range(rank * 256, (rank + 1) * 256))
+    if name == "c3":
+        return list(range(rank, 1024, world))
+    if name == "c4":
+        return list(range(rank, 1024, world))
+    if name == "c5":
+        per = -(-C5_TOTAL // world)
+        return list(range(rank * per, min(C5_TOTAL, (rank + 1) * per)))
+    raise SystemExit(f"unknown --config {name}")
+
+
+def c5_gradient(i: int) -> np.ndarray:
+    """Random macro deformation gradient of FE2 network i."""
+    rng = np.random.default_rng(10 ** 6 + i)
+    diag = rng.uniform(0.0, 0.1, 3)
+    off = rng.uniform(-0.05, 0.05, (3, 3))
+    np.fill_diagonal(off, 0.0)
+    return np.eye(3) + np.diag(diag) + off
+
+
+def config_networks(name: str, rank: int, world: int, limit: int | None = None):
     """(workload description, networks, deformation gradients) for one rank."""
     import paper_2305_07030_b200 as frb
+    idx = shard_indices(name, rank, world)
+    if limit is not None:
+        idx = idx[:limit]
     if name == "c1":
         return ("c1: 1 x generate_lattice(7,7,8,0.3,seed=0), uniaxial F=diag(1.1,1,1)",
                 [frb.generate_lattice(7, 7, 8, 0.3, 0)], [UNIAX])
     if name == "c2":
-        P = 256
-        seeds = range(rank * P, (rank + 1) * P)
-        return (f"c2: {P} x generate_lattice(15,15,15,0.3,seed=s) per GPU (10,125 DOF, 9,450 fibers), "
+        return (f"c2: {len(idx)} x generate_lattice(15,15,15,0.3,seed=s) per GPU (10,125 DOF, 9,450 fibers), "
                 "uniaxial F=diag(1.1,1,1)",
-                [frb.generate_lattice(15, 15, 15, 0.3, s) for s in seeds], [UNIAX] * P)
+                [frb.generate_lattice(15, 15, 15, 0.3, s) for s in idx], [UNIAX] * len(idx))
+    if name == "c3":
+        return (f"c3: 1024 x generate_lattice(32,32,32,0.3,seed=s) (98,304 DOF, 95,232 fibers), uniaxial, "
+                f"strided shards ({len(idx)} on this GPU)",
+                [frb.generate_lattice(32, 32, 32, 0.3, s) for s in idx], [UNIAX] * len(idx))
     if name == "c4":
-        idx = range(rank, 1024, world)
         nets, Fs = [], []
         for i in idx:
             n = 7 + (i % 26)
@@ -67,20 +101,27 @@ def config_networks(name: str, rank: int, world: int):
             Fs.append([UNIAX, BIAX, SHEAR][i % 3])
         return ("c4: 1024 heterogeneous lattices n=7+(i mod 26) (1k-100k DOF), "
                 "loads uniax/biax/shear by i mod 3, strided shards", nets, Fs)
-    if name == "c5":
-        total = 16384
-        per = total // world
-        idx = range(rank * per, (rank + 1) * per)
-        nets, Fs = [], []
-        for i in idx:
-            nets.append(frb.generate_lattice(15, 15, 15, 0.3, i))
-            rng = np.random.default_rng(10 ** 6 + i)
-            diag = rng.uniform(0.0, 0.1, 3)
-            off = rng.uniform(-0.05, 0.05, (3, 3))
-            np.fill_diagonal(off, 0.0)
-            Fs.append(np.eye(3) + np.diag(diag) + off)
-        return (f"c5: FE2 macro-step, {total} x 15^3 networks, random F, contiguous shards", nets, Fs)
-    raise SystemExit(f"unknown --config {name}")
+    return (f"c5: FE2 macro-step, {C5_TOTAL} x 15^3 networks, random F, contiguous shards",
+            [frb.generate_lattice(15, 15, 15, 0.3, i) for i in idx], [c5_gradient(i) for i in idx])
+
+
+def gather_stresses(sig, world: int, dist):
+    """Final homogenized-stress gather of the macro step: every rank's
+    [P, 9] float64 block to every rank (NCCL on the GPU box, gloo in tests)."""
+    import torch
+    P = sig.shape[0]
+    counts = torch.tensor([P], dtype=torch.int64, device=sig.device)
+    all_counts = [torch.zeros_like(counts) for _ in range(world)]
+    dist.all_gather(all_counts, counts)
+    Pmax = int(max(c.item() for c in all_counts))
+    pad = torch.zeros((Pmax, 9), dtype=sig.dtype, device=sig.device)
+    pad[:P] = sig
+    out = torch.empty((world, Pmax, 9), dtype=sig.dtype, device=sig.device)
+    if sig.is_cuda:
+        dist.all_gather_into_tensor(out.view(world * Pmax, 9), pad)
+    else:  # gloo has no all_gather_into_tensor
+        dist.all_gather(list(out.unbind(0)), pad)
+    return torch.cat([out[r, :int(all_counts[r].item())] for r in range(world)])
 
 
 def b_iter(N: int, nf: int, M: int) -> int:
@@ -141,28 +182,44 @@ class ClockSampler:
 # --------------------------------------------------------------------- CPU arm
 
 def _oracle_solve(args):
-    n, seed, F = args
+    cfgname, i = args
     sys.path.insert(0, ROOT)
     os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
     import paper_2305_07030_b200 as frb
     from oracle import frb_oracle as orc
-    net = frb.generate_lattice(*n, 0.3, seed)
+    if cfgname == "warm":
+        net, F = frb.generate_lattice(3, 3, 3, 0.3, 0), UNIAX
+    else:
+        _, nets, Fs = config_networks(cfgname, 0, 1, limit=None) if cfgname == "c1" else \
+            _one_network(cfgname, i)
+        net, F = nets[0], Fs[0]
     t0 = time.perf_counter()
     r = orc.solve(net, F, frb.SolverConfig())
     return time.perf_counter() - t0, r.iters, net.n_nodes
 
 
+def _one_network(cfgname: str, i: int):
+    """Network i of a workload (the CPU sample takes the first ones)."""
+    import paper_2305_07030_b200 as frb
+    if cfgname == "c2":
+        return "", [frb.generate_lattice(15, 15, 15, 0.3, i)], [UNIAX]
+    if cfgname == "c3":
+        return "", [frb.generate_lattice(32, 32, 32, 0.3, i)], [UNIAX]
+    if cfgname == "c4":
+        n = 7 + (i % 26)
+        return "", [frb.generate_lattice(n, n, n, 0.3, i)], [[UNIAX, BIAX, SHEAR][i % 3]]
+    return "", [frb.generate_lattice(15, 15, 15, 0.3, i)], [c5_gradient(i)]
+
+
 def cpu_sample(config: str, cores: int, per_core: int = 1):
     """Time the oracle port on `cores` worker processes over a bounded sample
-    of the workload (networks/s over the sample; generation excluded)."""
+    of the workload: its first cores * per_core networks (networks/s over the
+    sample; generation excluded)."""
     import multiprocessing as mp
-    if config == "c1":
-        jobs = [((7, 7, 8), 0, UNIAX)] * (cores * per_core)
-    else:
-        jobs = [((15, 15, 15), s, UNIAX) for s in range(cores * per_core)]
+    jobs = [(config, i) for i in range(cores * per_core)]
     ctx = mp.get_context("fork")
     with ctx.Pool(cores) as pool:
-        pool.map(_oracle_solve, [((3, 3, 3), 0, UNIAX)] * cores)  # warm the workers (imports)
+        pool.map(_oracle_solve, [("warm", 0)] * cores)  # warm the workers (imports)
         t0 = time.perf_counter()
         out = pool.map(_oracle_solve, jobs)
         wall = time.perf_counter() - t0
@@ -188,7 +245,7 @@ def run_reference_arm(args, rank: int):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (reference generate_lattice inputs)",
-        "config": {"workload": config_networks(args.config, 0, 1)[0] if args.config != "c4" else args.config,
+        "config": {"workload": config_networks(args.config, 0, 1, limit=0)[0],
                    "arm": "oracle/frb_oracle.py (numpy restatement of fibrelax, bit-exact)"},
         "node_updates_per_s": statistics.mean(s["node_updates_per_s"] for s in samples),
         "cpu_baseline": {"value": value, "unit": "networks/s", "cores": cores, "kind": "port",
@@ -205,7 +262,8 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c4", "c5"])
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--limit", type=int, default=None, help="networks per rank (c3/c4/c5 samples)")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--team-size", type=int, default=None, help="CTA size override (TeamBatched)")
@@ -231,7 +289,7 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
 
-    workload, nets, Fs = config_networks(args.config, rank, world)
+    workload, nets, Fs = config_networks(args.config, rank, world, args.limit)
     cfg = frb.SolverConfig()
     t0 = time.perf_counter()
     batch = frb.pack_batch(nets, [frb.AffineBC(F) for F in Fs])
@@ -242,7 +300,6 @@ def main():
     launch = dbatch.prepare(cfg, strategy)
     flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
     P = batch.n_problems
-    gathered = torch.empty(world * P * 9, dtype=torch.float64, device=dev)
     stream = torch.cuda.current_stream(dev)
 
     def step(ev=None):
@@ -253,8 +310,8 @@ def main():
         if ev is not None:
             ev[1].record(stream)
         if world > 1:  # final homogenized-stress gather (C1 result gather)
-            sig = launch.out.results.view(torch.float64).view(P, -1)[:, 5:14].contiguous().view(-1)
-            dist.all_gather_into_tensor(gathered, sig)
+            sig = launch.out.results.view(torch.float64).view(P, -1)[:, 5:14]
+            gather_stresses(sig, world, dist)
 
     for _ in range(args.warmup):
         step()
