@@ -394,7 +394,7 @@ def main():
         "iters_mean": float(iters.mean()),
         "e2e": {"value": world * P / e2e_s, "unit": "networks/s", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h)},
-        "gpu_launches": args.steps,
+        "gpu_launches": args.steps * int((launch.groups["count"] > 0).sum()),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                      "kernel": "frb_relax_cta_kernel", "kernel_ms": 1e3 * kern_mean,

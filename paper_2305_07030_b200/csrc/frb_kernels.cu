@@ -1567,6 +1567,47 @@ int64_t frb_rank_smem_bytes(int32_t n_pos, int32_t n_own, int32_t n_act, int32_t
 
 int frb_max_dofs_per_thread(int block_threads) { return dofs_cap(block_threads); }
 
+}  // extern "C"
+
+namespace {
+
+// One launch group on stream s (validated, dispatched to its instantiation).
+int launch_one(const frb_batch* batch, const frb_config* cfg, int gi, int optin, cudaStream_t s) {
+  const frb_group& g = batch->groups[gi];
+  int rc = FRB_OK;
+  if (g.cluster < 1 || g.cluster > FRB_MAX_CLUSTER) return set_err(FRB_E_INVALID, "cluster size out of range");
+  if (g.block_threads < 32 || g.block_threads > kMaxThreads || g.block_threads % 32)
+    return set_err(FRB_E_INVALID, "block_threads must be a multiple of 32 in [32, 1024]");
+  if (g.smem_bytes > optin) return set_err(FRB_E_TOO_LARGE, "a rank exceeds shared memory per CTA");
+  int32_t* q = batch->queue + gi;
+  if (cfg->energy_check_interval > 0) {
+    // work-ledger kernels (a diagnostic, kept out of the production
+    // kernels' code): CTAs of at most 512 threads, up to 16 DOFs each
+    const int T = g.block_threads < 512 ? g.block_threads : 512;
+    const int ke = (g.max_own_dofs + T - 1) / T;
+    if (ke > 16) return set_err(FRB_E_TOO_LARGE, "too many free DOFs per thread for the ledger kernels");
+    if (g.fprv_global) {
+      return ke <= 4   ? launch_group<4, 512, true, true>(batch, cfg, g, q, s, T)
+             : ke <= 8 ? launch_group<8, 512, true, true>(batch, cfg, g, q, s, T)
+                       : launch_group<16, 512, true, true>(batch, cfg, g, q, s, T);
+    }
+    return ke <= 4   ? launch_group<4, 512, false, true>(batch, cfg, g, q, s, T)
+           : ke <= 8 ? launch_group<8, 512, false, true>(batch, cfg, g, q, s, T)
+                     : launch_group<16, 512, false, true>(batch, cfg, g, q, s, T);
+  }
+  const int k = (g.max_own_dofs + g.block_threads - 1) / g.block_threads;
+  if (k > dofs_cap(g.block_threads)) return set_err(FRB_E_TOO_LARGE, "too many free DOFs per thread");
+  if (g.block_threads <= 256) rc = dispatch_k<256>(batch, cfg, g, q, s, k);
+  else if (g.block_threads <= 512) rc = dispatch_k<512>(batch, cfg, g, q, s, k);
+  else if (g.block_threads <= 768) rc = dispatch_k<768>(batch, cfg, g, q, s, k);
+  else rc = dispatch_k<1024>(batch, cfg, g, q, s, k);
+  return rc;
+}
+
+}  // namespace
+
+extern "C" {
+
 int frb_solve_batch(const frb_batch* batch, const frb_config* cfg, void* stream) {
   if (!batch || !cfg) return set_err(FRB_E_INVALID, "null batch or config");
   if (batch->n_problems < 0 || batch->n_groups < 0) return set_err(FRB_E_INVALID, "negative counts");
@@ -1580,41 +1621,38 @@ int frb_solve_batch(const frb_batch* batch, const frb_config* cfg, void* stream)
                   "cudaDeviceGetAttribute");
   if (rc) return rc;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  for (int gi = 0; gi < batch->n_groups; ++gi) {
-    const frb_group& g = batch->groups[gi];
-    if (g.count == 0) continue;
-    if (g.cluster < 1 || g.cluster > FRB_MAX_CLUSTER) return set_err(FRB_E_INVALID, "cluster size out of range");
-    if (g.block_threads < 32 || g.block_threads > kMaxThreads || g.block_threads % 32)
-      return set_err(FRB_E_INVALID, "block_threads must be a multiple of 32 in [32, 1024]");
-    if (g.smem_bytes > optin) return set_err(FRB_E_TOO_LARGE, "a rank exceeds shared memory per CTA");
-    if (cfg->energy_check_interval > 0) {
-      // work-ledger kernels (a diagnostic, kept out of the production
-      // kernels' code): CTAs of at most 512 threads, up to 16 DOFs each
-      const int T = g.block_threads < 512 ? g.block_threads : 512;
-      const int ke = (g.max_own_dofs + T - 1) / T;
-      if (ke > 16) return set_err(FRB_E_TOO_LARGE, "too many free DOFs per thread for the ledger kernels");
-      int32_t* q = batch->queue + gi;
-      if (g.fprv_global) {
-        rc = ke <= 4   ? launch_group<4, 512, true, true>(batch, cfg, g, q, s, T)
-             : ke <= 8 ? launch_group<8, 512, true, true>(batch, cfg, g, q, s, T)
-                       : launch_group<16, 512, true, true>(batch, cfg, g, q, s, T);
-      } else {
-        rc = ke <= 4   ? launch_group<4, 512, false, true>(batch, cfg, g, q, s, T)
-             : ke <= 8 ? launch_group<8, 512, false, true>(batch, cfg, g, q, s, T)
-                       : launch_group<16, 512, false, true>(batch, cfg, g, q, s, T);
-      }
-      if (rc) return rc;
-      continue;
-    }
-    const int k = (g.max_own_dofs + g.block_threads - 1) / g.block_threads;
-    if (k > dofs_cap(g.block_threads)) return set_err(FRB_E_TOO_LARGE, "too many free DOFs per thread");
-    if (g.block_threads <= 256) rc = dispatch_k<256>(batch, cfg, g, batch->queue + gi, s, k);
-    else if (g.block_threads <= 512) rc = dispatch_k<512>(batch, cfg, g, batch->queue + gi, s, k);
-    else if (g.block_threads <= 768) rc = dispatch_k<768>(batch, cfg, g, batch->queue + gi, s, k);
-    else rc = dispatch_k<1024>(batch, cfg, g, batch->queue + gi, s, k);
-    if (rc) return rc;
+  int n_live = 0;
+  for (int gi = 0; gi < batch->n_groups; ++gi) n_live += batch->groups[gi].count > 0;
+  if (n_live <= 1) {
+    for (int gi = 0; gi < batch->n_groups; ++gi)
+      if (batch->groups[gi].count > 0 && (rc = launch_one(batch, cfg, gi, optin, s))) return rc;
+    return FRB_OK;
   }
-  return FRB_OK;
+  // Several cluster sizes (heterogeneous batch): the groups run concurrently
+  // on forked streams, largest clusters launched first, joined back into s,
+  // so small networks fill the SMs the large clusters leave free.
+  cudaEvent_t fork;
+  rc = cuda_check(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming), "cudaEventCreate");
+  if (rc) return rc;
+  rc = cuda_check(cudaEventRecord(fork, s), "cudaEventRecord");
+  for (int gi = batch->n_groups - 1; gi >= 0 && !rc; --gi) {
+    if (batch->groups[gi].count == 0) continue;
+    cudaStream_t gs;
+    cudaEvent_t join;
+    rc = cuda_check(cudaStreamCreateWithFlags(&gs, cudaStreamNonBlocking), "cudaStreamCreate");
+    if (rc) break;
+    rc = cuda_check(cudaStreamWaitEvent(gs, fork, 0), "cudaStreamWaitEvent");
+    if (!rc) rc = launch_one(batch, cfg, gi, optin, gs);
+    if (!rc) rc = cuda_check(cudaEventCreateWithFlags(&join, cudaEventDisableTiming), "cudaEventCreate");
+    if (!rc) {
+      rc = cuda_check(cudaEventRecord(join, gs), "cudaEventRecord");
+      if (!rc) rc = cuda_check(cudaStreamWaitEvent(s, join, 0), "cudaStreamWaitEvent");
+      cudaEventDestroy(join);  // released once recorded work completes
+    }
+    cudaStreamDestroy(gs);     // likewise: pending work still runs
+  }
+  cudaEventDestroy(fork);
+  return rc;
 }
 
 int frb_selftest_arith(const double* a, const double* b, int n, double* out, void* stream) {
