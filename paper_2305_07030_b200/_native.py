@@ -23,7 +23,7 @@ DAMPING_ADAPTIVE, DAMPING_FIXED = 0, 1
 PF_EA_UNIFORM = 1
 PHASES = 12             # phase_cycles slots per CTA (frb200.h)
 PHASE_NAMES = ("F1 coefs", "F2 gather", "A per-DOF", "C chains", "T local+exp", "T exch wait",
-               "T top+scal", "U update", "epilogue", "prologue", "halo wait", "-")
+               "T top+scal", "U update", "epilogue", "prologue", "halo wait", "T local tree")
 
 EXPORTS = ("frb_abi_version", "frb_last_error", "frb_device_info", "frb_rank_smem_bytes",
            "frb_max_dofs_per_thread", "frb_solve_batch", "frb_internal_forces",

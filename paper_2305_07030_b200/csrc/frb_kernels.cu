@@ -78,7 +78,7 @@ constexpr int kChunk = 4;
 // instrumentation slots (frb_batch.phase_cycles): F1, F2, A, C, T local tree +
 // exports, T exchange wait, T top tree + scalars, U, epilogue, prologue, halo wait
 constexpr int kPhases = 12;
-enum { PH_F1, PH_F2, PH_A, PH_C, PH_TL, PH_TW, PH_TT, PH_U, PH_EPI, PH_PRO, PH_HALO };  // per-DOF phases process a thread's DOFs in chunks of this many
+enum { PH_F1, PH_F2, PH_A, PH_C, PH_TL, PH_TW, PH_TT, PH_U, PH_EPI, PH_PRO, PH_HALO, PH_TLP };  // per-DOF phases process a thread's DOFs in chunks of this many
 
 __device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
@@ -1160,6 +1160,7 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
     if (t >= 32) accel();
     if (t < 32) {
       run_prog(lprog, o.lslot, lane);
+      mark(sc, prof, PH_TLP);
 #pragma unroll 1
       for (int x = lane; x < n_exp; x += 32) {
         const int ls = o.lslot + 3 * exps[2 * x], ts = 3 * exps[2 * x + 1];

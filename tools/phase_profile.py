@@ -25,5 +25,5 @@ for T in [int(x) for x in a.teams.split(",")]:
     C = int(batch.groups["cluster"].max())
     tot = cyc.sum(axis=0)
     print(f"T={T}: {ms:.2f} ms, {iters} network-iterations, cluster {C}, grid {int((cyc.sum(axis=1) > 0).sum())} CTAs")
-    for k in range(nat.PHASES - 1):
+    for k in range(nat.PHASES):
         print(f"   {nat.PHASE_NAMES[k]:12s} {tot[k] / iters / C:9.0f} cycles per rank-iteration ({100 * tot[k] / tot.sum():5.1f}%)")
