@@ -397,7 +397,7 @@ def main():
         "gpu_launches": args.steps * int((launch.groups["count"] > 0).sum()),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                     "kernel": "frb_relax_cta_kernel", "kernel_ms": 1e3 * kern_mean,
+                     "kernel": "frb_relax_kernel", "kernel_ms": 1e3 * kern_mean,
                      "alg_bytes_per_launch": alg_bytes},
         "clocks": clocks.summary(),
         "kernel_ms_per_step": [round(1e3 * k, 3) for k in kern],
