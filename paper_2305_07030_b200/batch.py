@@ -52,9 +52,12 @@ MAX_CTA_THREADS = 1024
 CLUSTER_SIZES = (1, 2, 4, 8, 16)
 # per-CTA dynamic SMEM budget (227 KB opt-in minus the kernel's static SMEM)
 SMEM_BUDGET = 227 * 1024 - 4 * 1024
-# target free DOFs per cluster rank: keeps u, v register-resident and leaves
-# L1 room for the read-only tables (C2's 10k-DOF networks -> 2 ranks)
-DOFS_PER_RANK = int(os.environ.get("FRB_DOFS_PER_RANK", "3400"))
+# most free DOFs per cluster rank before a larger cluster is considered; the
+# SMEM budget usually decides first (15^3 networks need 2 ranks).  Fewer,
+# fuller ranks win on heterogeneous batches: c4 156 -> 217 networks/s going
+# from 3400 to 8000 (profiles/r01_configs.md), because large clusters cost
+# SMs (a 16-CTA cluster fills a GPC) and exchange latency.
+DOFS_PER_RANK = int(os.environ.get("FRB_DOFS_PER_RANK", "8000"))
 
 
 def dofs_per_thread_cap(threads: int) -> int:

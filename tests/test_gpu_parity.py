@@ -140,18 +140,19 @@ def test_identity_deformation_converges_in_one(cuda_device):
     assert not r.u.any() and not r.avg_stress.any()
 
 
-@pytest.mark.parametrize("n,iters", [(14, 20000), (20, 60), (32, 40)])
+@pytest.mark.parametrize("n,iters", [(15, 20000), (16, 20000), (24, 60), (32, 40)])
 def test_cluster_paths_vs_oracle(cuda_device, n, iters):
-    """Networks split over 2 / 8 / 16-CTA clusters (the 32^3 one with f_prev
-    in global memory, config 3's path), bit-equal to the oracle.  The larger
-    ones stop at max_iters so the CPU oracle stays fast; u, f, residual and
-    the stress are compared at that iterate."""
+    """Networks on one CTA with f_prev in global memory (15^3, config 2) and
+    split over 2 / 8 / 16-CTA clusters (32^3: config 3's path, f_prev in
+    global memory), bit-equal to the oracle.  The larger ones stop at
+    max_iters so the CPU oracle stays fast; u, f, residual and the stress are
+    compared at that iterate."""
     net = frb.generate_lattice(n, n, n, 0.3, 3)
     F = np.eye(3) + 0.2 * np.outer([1, 0, 0], [0, 1, 0])
     cfg = frb.SolverConfig(max_iters=iters)
     batch = frb.pack_batch([net], [frb.AffineBC(F)])
-    assert int(batch.desc[0]["cluster"]) == {14: 2, 20: 8, 32: 16}[n]
-    assert bool(batch.groups[0]["fprv_global"]) == (n == 32)
+    assert int(batch.desc[0]["cluster"]) == {15: 1, 16: 2, 24: 8, 32: 16}[n]
+    assert bool(batch.groups[0]["fprv_global"]) == (n in (15, 32))
     r = frb.solve_batch(batch, config=cfg)[0]
     o = orc.solve(net, F, cfg)
     assert_matches(r, o.u, o.iters, o.converged, o.residual, o.r_ref, o.sigma, label=f"{n}^3")
@@ -172,7 +173,7 @@ def test_every_cta_size_matches_reference(cuda_device, name):
         assert_matches(r, *golden_expect(case), label=f"{name} T={T}")
 
 
-@pytest.mark.parametrize("n,ramp", [(6, 0), (6, 4), (14, 0), (14, 6)])
+@pytest.mark.parametrize("n,ramp", [(6, 0), (6, 4), (16, 0), (16, 6)])
 def test_energy_ledger_vs_oracle(cuda_device, n, ramp):
     """Work ledger on one CTA and on a 2-CTA cluster, with and without the BC
     ramp: same iterate bit for bit (the ledger never feeds back), energy
