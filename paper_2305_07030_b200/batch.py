@@ -303,8 +303,8 @@ def _group_threads(max_own_dofs: int, max_rank_leaves: int, n_problems: int, clu
     need = max(64, 8 * max_rank_leaves, math.ceil(max_own_dofs / 16))
     if n_problems * cluster < 148:
         need = max(need, min(512, 32 * math.ceil(max_own_dofs / 32)))
-    if fprv_global:  # the global-f_prev kernels exist for 768 and 1024 threads
-        need = max(need, 768)
+    if fprv_global:  # global-f_prev kernels exist for 512..1024 threads; c2 (one 15^3
+        need = max(need, 768)  # network per CTA): 768 -> 82.3 ms, 512 -> 83.3 ms
     threads = min(MAX_CTA_THREADS, 32 * math.ceil(need / 32))
     while max_own_dofs > dofs_per_thread_cap(threads) * threads and threads < MAX_CTA_THREADS:
         threads += 32

@@ -912,8 +912,6 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
     }
   };
 
-  // a = (-f)/m for every own DOF (f = g_smem[o.fprv + dl]), then use(k, dl, a)
-  // for the valid ones; divisions are issued together, rare exact fallback
   // fm[k] = (-f)/m of every own DOF k (f = f_prev slot = the current force
   // once A has run); divisions are issued together, rare exact fallback
   double fm[MAXK];
@@ -938,6 +936,7 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
       }
     }
   };
+
 
   // ---- prologue: BCs, initial positions (microsolver.py:400-411) ---------
   // post the first halo and leaf-sum phases before any peer may send
@@ -1512,7 +1511,13 @@ int launch_group(const frb_batch* batch, const frb_config* cfg, const frb_group&
 template <int MAXT>
 int dispatch_k(const frb_batch* batch, const frb_config* cfg, const frb_group& g, int32_t* queue,
                cudaStream_t s, int k) {
-  if (g.fprv_global) {  // large networks: CTAs of 768 / 1024 threads, >= 4 DOFs per thread
+  if (g.fprv_global) {  // large networks: CTAs of 512 / 768 / 1024 threads, >= 4 DOFs per thread
+    if constexpr (MAXT == 512) {
+      if (k <= 8) return launch_group<8, MAXT, true>(batch, cfg, g, queue, s);
+      if (k <= 12) return launch_group<12, MAXT, true>(batch, cfg, g, queue, s);
+      if (k <= 14) return launch_group<14, MAXT, true>(batch, cfg, g, queue, s);
+      if (k <= 16) return launch_group<16, MAXT, true>(batch, cfg, g, queue, s);
+    }
     if constexpr (MAXT >= 768) {
       if (k <= 4) return launch_group<4, MAXT, true>(batch, cfg, g, queue, s);
       if (k <= 6) return launch_group<6, MAXT, true>(batch, cfg, g, queue, s);
@@ -1522,7 +1527,7 @@ int dispatch_k(const frb_batch* batch, const frb_config* cfg, const frb_group& g
         if (k <= 12) return launch_group<12, MAXT, true>(batch, cfg, g, queue, s);
       }
     }
-    return set_err(FRB_E_INVALID, "fprv_global groups need 513..1024 threads per CTA");
+    return set_err(FRB_E_INVALID, "fprv_global groups need 257..1024 threads per CTA");
   }
   if (k <= 1) return launch_group<1, MAXT, false>(batch, cfg, g, queue, s);
   if (k <= 4) return launch_group<4, MAXT, false>(batch, cfg, g, queue, s);
