@@ -126,15 +126,16 @@ class Topology:
 
     def choose_cluster(self) -> tuple[Partition, bool]:
         """Smallest cluster with at most DOFS_PER_RANK free DOFs per rank whose
-        ranks fit the SMEM budget (more ranks if SMEM demands it), and whether
-        f_prev must live in global memory instead of SMEM to fit."""
+        ranks fit the SMEM budget (more ranks if SMEM demands it), keeping
+        f_prev in SMEM whenever some cluster size allows it; otherwise the
+        smallest cluster that fits with f_prev in global memory (32^3)."""
         nf = 3 * self.n_free_nodes
         want = max(1, math.ceil(nf / DOFS_PER_RANK))
-        for C in CLUSTER_SIZES:
-            if C < want and C != CLUSTER_SIZES[-1]:
-                continue
-            part = self.partition(C)
-            for fprv_global in (False, True):
+        for fprv_global in (False, True):  # on-chip f_prev at any cluster size first
+            for C in CLUSTER_SIZES:
+                if C < want and C != CLUSTER_SIZES[-1]:
+                    continue
+                part = self.partition(C)
                 if partition_smem_bytes(part, fprv_global) <= SMEM_BUDGET:
                     return part, fprv_global
         raise nat.NativeError(nat.FRB_E_TOO_LARGE,

@@ -119,13 +119,13 @@ def test_rank_smem_mirror_matches_library():
         assert nat.lib().frb_rank_smem_bytes(*args) == smem_bytes(*args[:5], bool(args[5]))
 
 
-def test_c2_networks_fit_one_cta_with_global_fprev():
-    """15^3 networks (config 2): one CTA whose f_prev lives in global memory
-    (SMEM would need 262 KB with it, 209 KB without)."""
+def test_c2_networks_use_two_ranks_on_chip():
+    """15^3 networks (config 2): a 2-CTA cluster keeps every array on chip
+    (one CTA would need f_prev in global memory)."""
     t = fb.build_problem(frb.generate_lattice(15, 15, 15, 0.3, 0), frb.AffineBC(np.eye(3))).topo
     part, fglob = t.choose_cluster()
-    assert part.C == 1 and fglob
-    assert partition_smem_bytes(part, True) <= fb.SMEM_BUDGET < partition_smem_bytes(part, False)
+    assert part.C == 2 and not fglob
+    assert partition_smem_bytes(part, False) <= fb.SMEM_BUDGET < partition_smem_bytes(t.partition(1), False)
 
 
 def test_c3_networks_fit_a_16_cluster_with_global_fprev():
@@ -174,11 +174,11 @@ def test_pack_offsets_groups_and_dedup():
 
 def test_mixed_sizes_form_cluster_groups():
     nets = [frb.generate_lattice(16, 16, 16, 0.3, 0), frb.generate_lattice(6, 6, 6, 0.3, 0),
-            frb.generate_lattice(15, 15, 15, 0.3, 0)]
+            frb.generate_lattice(32, 32, 32, 0.3, 0)]
     b = frb.pack_batch(nets, [frb.AffineBC(np.eye(3))] * 3)
-    # groups: (cluster, f_prev in global memory); 15^3 fits one CTA only without f_prev in SMEM
-    assert [(int(g["cluster"]), int(g["fprv_global"])) for g in b.groups] == [(1, 0), (1, 1), (2, 0)]
-    assert [int(d["cluster"]) for d in b.desc] == [2, 1, 1]
+    # groups: (cluster, f_prev in global memory); 32^3 needs both 16 ranks and global f_prev
+    assert [(int(g["cluster"]), int(g["fprv_global"])) for g in b.groups] == [(1, 0), (2, 0), (16, 1)]
+    assert [int(d["cluster"]) for d in b.desc] == [2, 1, 16]
 
 
 def test_mixed_materials_carry_element_ea():
