@@ -152,6 +152,9 @@ def test_cluster_paths_vs_oracle(cuda_device, n, iters):
     batch = frb.pack_batch([net], [frb.AffineBC(F)])
     assert int(batch.desc[0]["cluster"]) == {16: 2, 24: 8, 32: 16}[n]
     assert bool(batch.groups[0]["fprv_global"]) == (n == 32)
+    r = frb.solve_batch(batch, config=cfg)[0]
+    o = orc.solve(net, F, cfg)
+    assert_matches(r, o.u, o.iters, o.converged, o.residual, o.r_ref, o.sigma, label=f"{n}^3")
 
 
 def test_single_cta_global_fprev_vs_oracle(cuda_device):
@@ -169,9 +172,6 @@ def test_single_cta_global_fprev_vs_oracle(cuda_device):
     r = fb.results_to_solve_results(batch, batch.to_device().solve(cfg))[0]
     o = orc.solve(net, F, cfg)
     assert_matches(r, o.u, o.iters, o.converged, o.residual, o.r_ref, o.sigma, label="15^3 one CTA")
-    r = frb.solve_batch(batch, config=cfg)[0]
-    o = orc.solve(net, F, cfg)
-    assert_matches(r, o.u, o.iters, o.converged, o.residual, o.r_ref, o.sigma, label=f"{n}^3")
 
 
 @pytest.mark.parametrize("name", ["c1_7x7x8_uniax", "lat8_seed5", "random60", "lat6_general_F"])
