@@ -477,6 +477,21 @@ class DeviceBatch:
             t[k] = src.to(device, non_blocking=True)
         return cls(host=batch, device=device, t=t)
 
+    def set_deformation(self, Fs) -> None:
+        """FE2 macro step: new deformation gradients for every network, the
+        packed geometry and topology stay resident (only the per-problem
+        descriptor changes; the prescribed displacements are formed on the
+        device from F, microsolver.py:320-322).  Takes effect at the next
+        prepare()/solve()."""
+        h = self.host
+        bcs = [b if isinstance(b, AffineBC) else AffineBC(np.asarray(b, dtype=np.float64)) for b in Fs]
+        if len(bcs) != h.n_problems:
+            raise ValueError(f"expected {h.n_problems} deformation gradients, got {len(bcs)}")
+        for i, bc in enumerate(bcs):
+            h.desc[i]["F"] = np.asarray(bc.deformation_gradient, dtype=np.float64).reshape(9)
+            h.problems[i].F = np.asarray(bc.deformation_gradient, dtype=np.float64)
+        h.bcs = bcs
+
     def prepare(self, cfg: SolverConfig, strategy=None, phase_profile: bool = False) -> "Launch":
         """Allocate outputs and build the launch arguments once; the
         returned Launch can be replayed (bench) or run once (solve)."""

@@ -201,3 +201,19 @@ def test_energy_ledger_vs_oracle(cuda_device, n, ramp):
     o = orc.solve(net, F, cfg)
     assert_matches(r, o.u, o.iters, o.converged, o.residual, o.r_ref, o.sigma, label=f"{n}/{ramp}")
     assert abs(r.energy_residual - o.energy_residual) <= 1e-10 * abs(o.energy_residual)
+
+
+def test_fe2_macro_step_reuses_the_packed_batch(cuda_device):
+    """DeviceBatch.set_deformation: a new F per network on the resident batch
+    gives the same bits as packing afresh (the FE2 macro-step loop)."""
+    nets = [frb.generate_lattice(6, 6, 7, 0.3, s) for s in range(4)]
+    F0 = [np.diag([1.1, 1.0, 1.0])] * 4
+    F1 = [np.eye(3) + 0.02 * (k + 1) * np.outer([1, 0, 0], [0, 1, 0]) for k in range(4)]
+    batch = frb.pack_batch(nets, [frb.AffineBC(F) for F in F0])
+    dev = batch.to_device()
+    fb.results_to_solve_results(batch, dev.solve(frb.SolverConfig()))
+    dev.set_deformation(F1)
+    got = fb.results_to_solve_results(batch, dev.solve(frb.SolverConfig()))
+    fresh = frb.solve_batch(frb.pack_batch(nets, [frb.AffineBC(F) for F in F1]))
+    for a, b in zip(got, fresh):
+        assert a.iters == b.iters and np.array_equal(a.u, b.u) and np.array_equal(a.avg_stress, b.avg_stress)
