@@ -373,11 +373,10 @@ __device__ __noinline__ LenCoef exact_elem(int o_pos, uint32_t ab, double L, dou
   return exact_len_coef(dsub(pb[0], pa[0]), dsub(pb[1], pa[1]), dsub(pb[2], pa[2]), L, EA);
 }
 
-__device__ __forceinline__ bool element_coefs(int n_act, const uint32_t* __restrict__ act_ab,
+__device__ __forceinline__ bool element_coefs(int T, int n_act, const uint32_t* __restrict__ act_ab,
                                               const double* __restrict__ act_L, const double* __restrict__ act_EA,
                                               double ea, int o_pos, int o_cf) {
   bool bad = false;
-  const int T = blockDim.x;
   const int last = n_act - 1;
   for (int e0 = threadIdx.x; e0 < n_act; e0 += kElem * T) {
     uint32_t ab[kElem];
@@ -473,9 +472,8 @@ __device__ __forceinline__ void node_force(const uint32_t* __restrict__ ell, int
   g_smem[o_out + 3 * i + 2] = dadd(az, bz);
 }
 
-__device__ __forceinline__ void node_forces(int n_own, const uint32_t* __restrict__ ell, int S, int SA, int SB,
+__device__ __forceinline__ void node_forces(int T, int n_own, const uint32_t* __restrict__ ell, int S, int SA, int SB,
                                             int o_pos, int o_cf, int o_out) {
-  const int T = blockDim.x;
   int i = threadIdx.x;
   for (; i + T < n_own; i += 2 * T) {
     node_force(ell, S, SA, SB, o_pos, o_cf, o_out, i);
@@ -805,10 +803,13 @@ __device__ __forceinline__ void drain(Mbar& mb, uint32_t halo_bytes, uint32_t le
   mb.ph_s ^= 1u;
 }
 
-template <int MAXK, bool kFG, bool kEnergy>
+template <int MAXK, bool kFG, bool kEnergy, int kT>
 __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, int rank, Scalars& sc, Mbar& mb,
                               const Net& n, const Rank& R) {
-  const int T = blockDim.x, t = threadIdx.x, lane = t & 31;
+  // kT > 0: the kernel is launched with exactly kT threads, so every
+  // DOF-strided index t + k T folds its stride into immediate offsets
+  const int T = kT > 0 ? kT : static_cast<int>(blockDim.x);
+  const int t = threadIdx.x, lane = t & 31;
   const int C = n.C, L = n.L, n_own = R.n_own, nfo = 3 * n_own;
   const Layout o = layout<kFG>(R);
   const double* __restrict__ Xg = n.X;
@@ -963,9 +964,9 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
     return;
   }
   // initial internal forces on own nodes (:413-420), kept as f_prev
-  element_coefs(n_act, act_ab, act_L, act_EA, ea, o.pos, o.cf);
+  element_coefs(T, n_act, act_ab, act_L, act_EA, ea, o.pos, o.cf);
   __syncthreads();
-  node_forces(n_own, ell, S, SA, SB, o.pos, o.cf, o.fcur);
+  node_forces(T, n_own, ell, S, SA, SB, o.pos, o.cf, o.fcur);
   __syncthreads();
   for (int dl = t; dl < nfo; dl += T) SET_FPRV(dl, g_smem[o.fcur + dl]);
   __syncthreads();
@@ -1018,11 +1019,11 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
       alpha_prev = alpha;
     }
     // F: internal forces at the drifted positions (:456-465)
-    bool bad = element_coefs(n_act, act_ab, act_L, act_EA, ea, o.pos, o.cf);
+    bool bad = element_coefs(T, n_act, act_ab, act_L, act_EA, ea, o.pos, o.cf);
     if (ramp && it < ramp_n && rank == 0) bad |= check_elements(n, PosFixed{&n, alpha, ramp}, false);
     __syncthreads();
     mark(sc, prof, PH_F1);
-    node_forces(n_own, ell, S, SA, SB, o.pos, o.cf, o.fcur);
+    node_forces(T, n_own, ell, S, SA, SB, o.pos, o.cf, o.fcur);
     if (bad) sc.singular = 1;
     __syncthreads();
     mark(sc, prof, PH_F2);
@@ -1386,7 +1387,7 @@ __global__ void __launch_bounds__(MAXT, 1)
       sc.threshold = __longlong_as_double(0x7ff0000000000000ULL);  // +inf until set
     }
     __syncthreads();
-    solve_problem<MAXK, kFG, kEnergy>(b, cfg, p, rank, sc, mb, net, rk);
+    solve_problem<MAXK, kFG, kEnergy, kEnergy ? 0 : MAXT>(b, cfg, p, rank, sc, mb, net, rk);
     csync(C);  // no rank reuses its SMEM before every peer is done with it
   }
   if (b.phase_cycles && threadIdx.x == 0) {
@@ -1487,7 +1488,7 @@ int launch_group(const frb_batch* batch, const frb_config* cfg, const frb_group&
   attr[0].val.clusterDim.x = C;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
-  lc.blockDim = dim3(threads > 0 ? threads : g.block_threads);
+  lc.blockDim = dim3(threads > 0 ? threads : (kEnergy ? g.block_threads : MAXT));
   lc.dynamicSmemBytes = g.smem_bytes;
   lc.stream = s;
   lc.attrs = attr;
@@ -1601,7 +1602,10 @@ int launch_one(const frb_batch* batch, const frb_config* cfg, int gi, int optin,
            : ke <= 8 ? launch_group<8, 512, false, true>(batch, cfg, g, q, s, T)
                      : launch_group<16, 512, false, true>(batch, cfg, g, q, s, T);
   }
-  const int k = (g.max_own_dofs + g.block_threads - 1) / g.block_threads;
+  // production kernels run with exactly MAXT threads (the template's CTA
+  // size, >= block_threads): DOFs per thread follow from that
+  const int tpl = g.block_threads <= 256 ? 256 : g.block_threads <= 512 ? 512 : g.block_threads <= 768 ? 768 : 1024;
+  const int k = (g.max_own_dofs + tpl - 1) / tpl;
   if (k > dofs_cap(g.block_threads)) return set_err(FRB_E_TOO_LARGE, "too many free DOFs per thread");
   if (g.block_threads <= 256) rc = dispatch_k<256>(batch, cfg, g, q, s, k);
   else if (g.block_threads <= 512) rc = dispatch_k<512>(batch, cfg, g, q, s, k);
