@@ -431,11 +431,13 @@ __device__ __forceinline__ bool element_coefs(int T, int n_act, const uint32_t* 
 // so their latencies overlap.
 constexpr int kSlots = 3;
 
-template <bool kRoleA>
+// kOne: at most kSlots slots per role (lattices: 3 + 3), a single unrolled group
+template <bool kRoleA, bool kOne>
 __device__ __forceinline__ void gather_role(const uint32_t* __restrict__ ell_i, int S, int n_slots, int i,
                                             int o_pos, int o_cf, double px, double py, double pz, double& sx,
                                             double& sy, double& sz) {
-  for (int k0 = 0; k0 < n_slots; k0 += kSlots) {
+  for (int k0 = 0; k0 < (kOne ? 1 : n_slots); k0 += kSlots) {
+    if (kOne && n_slots == 0) break;
     uint32_t w[kSlots];
     w[0] = __ldg(ell_i + k0 * S);
     // slots past the end become self-padding of node i (a +-0 contribution)
@@ -461,25 +463,36 @@ __device__ __forceinline__ void gather_role(const uint32_t* __restrict__ ell_i, 
 
 // f of every own node into g_smem[o_out + 3 i + axis]; a thread gathers two
 // of its nodes together so their load latencies overlap
+template <bool kOne>
 __device__ __forceinline__ void node_force(const uint32_t* __restrict__ ell, int S, int SA, int SB, int o_pos,
                                            int o_cf, int o_out, int i) {
   const double px = g_smem[o_pos + 3 * i], py = g_smem[o_pos + 3 * i + 1], pz = g_smem[o_pos + 3 * i + 2];
   double ax = 0.0, ay = 0.0, az = 0.0, bx = 0.0, by = 0.0, bz = 0.0;
-  gather_role<true>(ell + i, S, SA, i, o_pos, o_cf, px, py, pz, ax, ay, az);
-  gather_role<false>(ell + SA * S + i, S, SB, i, o_pos, o_cf, px, py, pz, bx, by, bz);
+  gather_role<true, kOne>(ell + i, S, SA, i, o_pos, o_cf, px, py, pz, ax, ay, az);
+  gather_role<false, kOne>(ell + SA * S + i, S, SB, i, o_pos, o_cf, px, py, pz, bx, by, bz);
   g_smem[o_out + 3 * i] = dadd(ax, bx);
   g_smem[o_out + 3 * i + 1] = dadd(ay, by);
   g_smem[o_out + 3 * i + 2] = dadd(az, bz);
 }
 
-__device__ __forceinline__ void node_forces(int T, int n_own, const uint32_t* __restrict__ ell, int S, int SA, int SB,
-                                            int o_pos, int o_cf, int o_out) {
+template <bool kOne>
+__device__ __forceinline__ void node_forces_t(int T, int n_own, const uint32_t* __restrict__ ell, int S, int SA,
+                                              int SB, int o_pos, int o_cf, int o_out) {
   int i = threadIdx.x;
   for (; i + T < n_own; i += 2 * T) {
-    node_force(ell, S, SA, SB, o_pos, o_cf, o_out, i);
-    node_force(ell, S, SA, SB, o_pos, o_cf, o_out, i + T);
+    node_force<kOne>(ell, S, SA, SB, o_pos, o_cf, o_out, i);
+    node_force<kOne>(ell, S, SA, SB, o_pos, o_cf, o_out, i + T);
   }
-  if (i < n_own) node_force(ell, S, SA, SB, o_pos, o_cf, o_out, i);
+  if (i < n_own) node_force<kOne>(ell, S, SA, SB, o_pos, o_cf, o_out, i);
+}
+
+__device__ __forceinline__ void node_forces(int T, int n_own, const uint32_t* __restrict__ ell, int S, int SA, int SB,
+                                            int o_pos, int o_cf, int o_out) {
+  if (SA <= kSlots && SB <= kSlots) {  // uniform: a lattice's 3 + 3 incidences
+    node_forces_t<true>(T, n_own, ell, S, SA, SB, o_pos, o_cf, o_out);
+  } else {
+    node_forces_t<false>(T, n_own, ell, S, SA, SB, o_pos, o_cf, o_out);
+  }
 }
 
 // ------------------------------------------------------------------ block helpers
