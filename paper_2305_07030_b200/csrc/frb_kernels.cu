@@ -926,31 +926,29 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
     }
   };
 
-  // fm[k] = (-f)/m of every own DOF k (f = f_prev slot = the current force
-  // once A has run); divisions are issued together, rare exact fallback
-  double fm[MAXK];
-  auto accel = [&]() {
+  // (-f)/m of every own DOF into its f slot of SMEM (free once C has
+  // consumed f f): threads first .. first + n - 1 cover all DOFs, four per
+  // step so the divisions overlap; rare exact fallback.  In the loop the
+  // warps other than warp 0 do it while warp 0 runs the tree phase.
+  auto accel = [&](int first, int nthr) {
+    for (int d0 = t - first; d0 < nfo; d0 += kChunk * nthr) {
+      double q[kChunk];
+      bool ok[kChunk];
 #pragma unroll
-    for (int k0 = 0; k0 < MAXK; k0 += kChunk) {
-      constexpr int KC = MAXK < kChunk ? MAXK : kChunk;
-      bool ok[KC];
-#pragma unroll
-      for (int kk = 0; kk < KC; ++kk) {
-        if (k0 + kk < MAXK) {
-          const int dl = min(t + (k0 + kk) * T, dl_max);
-          fm[k0 + kk] = frb_arith::div_fast(-FPRV(dl), __ldg(nmass + dl / 3), ok[kk]);
-        }
+      for (int kk = 0; kk < kChunk; ++kk) {
+        const int dl = min(d0 + kk * nthr, dl_max);
+        q[kk] = frb_arith::div_fast(-FPRV(dl), __ldg(nmass + dl / 3), ok[kk]);
       }
 #pragma unroll
-      for (int kk = 0; kk < KC; ++kk) {
-        if (k0 + kk < MAXK && !ok[kk]) {
-          const int dl = min(t + (k0 + kk) * T, dl_max);
-          fm[k0 + kk] = exact_div(-FPRV(dl), __ldg(nmass + dl / 3));
+      for (int kk = 0; kk < kChunk; ++kk) {
+        const int dl = d0 + kk * nthr;
+        if (dl < nfo) {
+          if (!ok[kk]) q[kk] = exact_div(-FPRV(dl), __ldg(nmass + dl / 3));
+          g_smem[o.fcur + dl] = q[kk];
         }
       }
     }
   };
-
 
   // ---- prologue: BCs, initial positions (microsolver.py:400-411) ---------
   // post the first halo and leaf-sum phases before any peer may send
@@ -995,12 +993,13 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
   if (eramp) csync(C);  // rank 0 has read the initial positions before any rank drifts
 
   // a = -f/m (:428-430), then iteration 0's kick + drift (:443-448)
-  accel();
+  accel(0, T);
+  __syncthreads();
 #pragma unroll
   for (int k = 0; k < MAXK; ++k) {
     const int dl = t + k * T;
     if (dl < nfo) {
-      v[k] = dadd(0.0, dmul(hdt, fm[k]));
+      v[k] = dadd(0.0, dmul(hdt, g_smem[o.fcur + dl]));
       u[k] = dadd(0.0, dmul(dt, v[k]));
       put_pos(k, dl, dadd(xr[k], u[k]));
     }
@@ -1170,7 +1169,7 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
     // rank (with this rank's singular flag), the top tree over all ranks'
     // exports, then the scalar bookkeeping.  Meanwhile the other warps
     // compute U's c-independent part, fm = (-f)/m (warp 0 does after T).
-    if (t >= 32) accel();
+    if (T > 32 && t >= 32) accel(32, T - 32);
     if (t < 32) {
       run_prog(lprog, o.lslot, lane);
       mark(sc, prof, PH_TLP);
@@ -1269,7 +1268,7 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
           }
         }
       }
-      accel();
+      if (T <= 32) accel(0, T);
     }
     mb.ph_s ^= 1u;
     __syncthreads();
@@ -1296,7 +1295,7 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
     for (int k = 0; k < MAXK; ++k) {
       const int dl = t + k * T;
       if (dl < nfo) {
-        const double a = dsub(fm[k], dmul(c, v[k]));
+        const double a = dsub(g_smem[o.fcur + dl], dmul(c, v[k]));
         v[k] = dadd(v[k], dmul(hdt, a));
         if (!done) {
           v[k] = dadd(v[k], dmul(hdt, a));
