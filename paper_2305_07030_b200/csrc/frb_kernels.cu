@@ -860,6 +860,7 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
   const int* const tprog = prog + R.tree[4];
   const int* const exps = prog + R.tree[5];
   const int n_exp = R.n_exp, root_top = R.root_top;
+  const bool quad_mode = (R.tree[9] & 4) != 0;  // plan.py MODE_QUAD
 
   const bool adaptive = cfg.damping == FRB_DAMPING_ADAPTIVE;
   const int ramp_n = cfg.bc_ramp_iters;
@@ -1155,7 +1156,25 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
           r2 = dadd(r2, a2);
         }
       }
-      if (chain && j == 0) {
+      if (quad_mode) {  // lanes 0, 8, 16, 24 hold leaves 4w .. 4w+3: ((l0 + l1) + (l2 + l3))
+        const double p0 = __shfl_down_sync(0xffffffffu, r0, 8);
+        const double p1 = __shfl_down_sync(0xffffffffu, r1, 8);
+        const double p2 = __shfl_down_sync(0xffffffffu, r2, 8);
+        if ((lane & 15) == 0) {
+          r0 = dadd(r0, p0);
+          r1 = dadd(r1, p1);
+          r2 = dadd(r2, p2);
+        }
+        const double q0 = __shfl_down_sync(0xffffffffu, r0, 16);
+        const double q1 = __shfl_down_sync(0xffffffffu, r1, 16);
+        const double q2 = __shfl_down_sync(0xffffffffu, r2, 16);
+        if (lane == 0) {
+          const int sl = o.lslot + 3 * (t >> 5);  // local slot = the warp's quad
+          g_smem[sl] = dadd(r0, q0);
+          g_smem[sl + 1] = dadd(r1, q1);
+          g_smem[sl + 2] = dadd(r2, q2);
+        }
+      } else if (chain && j == 0) {
         const int sl = o.lslot + 3 * lloc;  // local leaf lloc
         g_smem[sl] = r0;
         g_smem[sl + 1] = r1;

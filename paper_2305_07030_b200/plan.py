@@ -166,38 +166,7 @@ def _program(ops: list[tuple[int, int, int, int]]) -> np.ndarray:
     return np.array([len(rounds), 0] + [w for r in rounds for w in r], dtype=np.int32)
 
 
-MODE_LOCAL_SHFL, MODE_TOP_SHFL = 1, 2
-
-
-def _shuffle_program(ops: list[tuple[int, int, int]]) -> np.ndarray:
-    """Warp-shuffle form of a tree whose leaves sit one per lane: every node's
-    value lives in the lane of its leftmost leaf, so op (height, left lane,
-    right lane) is `lane[left] += lane[right]` -- one shuffle per round.
-    Layout [n_rounds, 0, n_rounds x 8 words]: per round 32 source lanes as
-    bytes (0xFF: lane idle)."""
-    ops = sorted(ops)
-    heights = sorted({o[0] for o in ops})
-    words = []
-    for h in heights:
-        src = [0xFF] * PROG_LANES
-        for _, d, a in (o for o in ops if o[0] == h):
-            assert 0 <= d < PROG_LANES and 0 <= a < PROG_LANES and src[d] == 0xFF
-            src[d] = a
-        b = np.array(src, dtype=np.uint8).view(np.int32)
-        words.extend(int(x) for x in b)
-    return np.array([len(heights), 0] + words, dtype=np.int32)
-
-
-def run_shuffle_program(prog: np.ndarray, lanes: list) -> None:
-    """Host replay of a _shuffle_program (test helper)."""
-    n = int(prog[0])
-    for r in range(n):
-        src = prog[2 + 8 * r:2 + 8 * (r + 1)].astype(np.int32).view(np.uint8)
-        new = list(lanes)
-        for lane in range(PROG_LANES):
-            if src[lane] != 0xFF:
-                new[lane] = lanes[lane] + lanes[int(src[lane])]
-        lanes[:] = new
+MODE_QUAD = 4   # the rank's leaves fold in aligned quads inside the chain warps
 
 
 def run_program(prog: np.ndarray, slots: list) -> None:
@@ -273,52 +242,54 @@ def tree_split(flat: np.ndarray, ranges: list[tuple[int, int]]) -> list[np.ndarr
         top_ops.append((h, int(top_of[d]), int(top_of[a]), int(top_of[b])))
     TS = E + len(top_internal)
     root_top = int(top_of[p.root])
-    top_shfl = False                           # (shuffle form measured slower on B200)
-    if top_shfl:                               # top leaves (exports) one per lane
-        tlo = {}
-        for i, sl in enumerate(exports):
-            tlo[sl] = i
-        sops = []
-        for k in top_internal:
-            d, a, b = int(p.op_dst[k]), int(p.op_left[k]), int(p.op_right[k])
-            tlo[d] = tlo[a]
-            sops.append((theight[d], tlo[a], tlo[b]))
-        tprog = _shuffle_program(sops)
-        TS, root_top = E, 0
-    else:
-        tprog = _program(top_ops)
+    tprog = _program(top_ops)
     blocks = []
+    children = {int(p.op_dst[k]): (int(p.op_left[k]), int(p.op_right[k])) for k in range(K)}
     for r, (a, b) in enumerate(ranges):
+        nleaf = b - a
+        # quad mode: every aligned group of 4 own leaves is the complete
+        # subtree ((l0 + l1) + (l2 + l3)); the chain warps (4 leaves each)
+        # fold it with shuffles and the local program starts at the quads
+        quad_nodes, quad_roots = set(), []
+        quad = nleaf > 0 and nleaf % 4 == 0
+        if quad:
+            for g in range(nleaf // 4):
+                l0 = a + 4 * g
+                p01, p23 = int(parent[l0]), int(parent[l0 + 2])
+                q = int(parent[p01]) if p01 >= 0 else -1
+                if (p01 < 0 or p23 < 0 or q < 0 or children.get(p01) != (l0, l0 + 1)
+                        or children.get(p23) != (l0 + 2, l0 + 3) or children.get(q) != (p01, p23)
+                        or owner[q] != r):
+                    quad = False
+                    break
+                quad_nodes.update((l0, l0 + 1, l0 + 2, l0 + 3, p01, p23))
+                quad_roots.append(q)
+        if quad and any(owner[sl] == r and sl in quad_nodes for sl in exports):
+            quad = False
         local_idx = np.full(n_slots, -1, dtype=np.int64)
-        local_idx[a:b] = np.arange(b - a)
-        nl = b - a
+        if quad:
+            for g, q in enumerate(quad_roots):
+                local_idx[q] = g
+            nl = len(quad_roots)
+        else:
+            local_idx[a:b] = np.arange(nleaf)
+            nl = nleaf
+        below = set(quad_roots) | quad_nodes if quad else set()
         lheight = {}
         lops = []
         for k in range(K):
             d, x, y = int(p.op_dst[k]), int(p.op_left[k]), int(p.op_right[k])
-            if owner[d] != r:
+            if owner[d] != r or d in below:
                 continue
             local_idx[d] = nl
             nl += 1
             h = 1 + max(lheight.get(x, 0), lheight.get(y, 0))
             lheight[d] = h
             lops.append((h, int(local_idx[d]), int(local_idx[x]), int(local_idx[y])))
-        loc_shfl = False
-        if loc_shfl:                           # own leaves one per lane
-            sops = []
-            for k in range(K):
-                d, x, y = int(p.op_dst[k]), int(p.op_left[k]), int(p.op_right[k])
-                if owner[d] == r:
-                    sops.append((lheight[d], int(lo[x]) - a, int(lo[y]) - a))
-            lprog = _shuffle_program(sops)
-            nl = b - a
-            exp = np.array([(int(lo[s]) - a, int(top_of[s])) for s in exports if owner[s] == r],
-                           dtype=np.int32).reshape(-1)
-        else:
-            lprog = _program(lops)
-            exp = np.array([(int(local_idx[s]), int(top_of[s])) for s in exports if owner[s] == r],
-                           dtype=np.int32).reshape(-1)
-        mode = (MODE_LOCAL_SHFL if loc_shfl else 0) | (MODE_TOP_SHFL if top_shfl else 0)
+        lprog = _program(lops)
+        exp = np.array([(int(local_idx[sl]), int(top_of[sl])) for sl in exports if owner[sl] == r],
+                       dtype=np.int32).reshape(-1)
+        mode = MODE_QUAD if quad else 0
         lprog_off = TREE_HEADER
         tprog_off = lprog_off + len(lprog)
         exp_off = tprog_off + len(tprog)
@@ -361,23 +332,20 @@ def evaluate_split(flat: np.ndarray, blocks: list[np.ndarray], ranges, a) -> flo
     run = run_program
 
     TS = int(blocks[0][1])
-    top = [0.0] * max(TS, PROG_LANES)
+    top = [0.0] * max(TS, 1)
     for bk, (ra, rb) in zip(blocks, ranges):
         LS = int(bk[0])
-        loc = [0.0] * max(LS, PROG_LANES)
-        loc[:rb - ra] = leaf[ra:rb]
-        prog = bk[int(bk[3]):int(bk[4])]
-        if int(bk[9]) & MODE_LOCAL_SHFL:
-            run_shuffle_program(prog, loc)
+        loc = [0.0] * max(LS, 1)
+        if int(bk[9]) & MODE_QUAD:
+            for g in range((rb - ra) // 4):
+                l0 = ra + 4 * g
+                loc[g] = (leaf[l0] + leaf[l0 + 1]) + (leaf[l0 + 2] + leaf[l0 + 3])
         else:
-            run(prog, loc)
+            loc[:rb - ra] = leaf[ra:rb]
+        run(bk[int(bk[3]):int(bk[4])], loc)
         exp = bk[int(bk[5]):int(bk[5]) + 2 * int(bk[6])]
         for i in range(0, len(exp), 2):
             top[int(exp[i + 1])] = loc[int(exp[i])]
     bk = blocks[0]
-    prog = bk[int(bk[4]):int(bk[5])]
-    if int(bk[9]) & MODE_TOP_SHFL:
-        run_shuffle_program(prog, top)
-    else:
-        run(prog, top)
+    run(bk[int(bk[4]):int(bk[5])], top)
     return top[int(bk[7])]
