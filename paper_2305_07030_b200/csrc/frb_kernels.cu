@@ -773,25 +773,28 @@ __device__ __forceinline__ Layout layout(const Rank& R) {
 }
 
 // Replay one combine program (plan.py _program: warp rounds of up to 32
-// independent ops, lane-packed) on g_smem[o_slot + 3 s + {0,1,2}] with the
-// calling warp.  The next round's op is fetched while the current one runs.
-// Not unrolled: a single warp runs it while the rest of the CTA waits, so its
-// code must stay small and I-cache resident.
+// independent ops, lane-packed, slot indices premultiplied by 3, idle lanes
+// folding a scratch slot, one idle pad round) on g_smem[o_slot + ...] with
+// the calling warp: no branch in the loop, the next round's op is fetched
+// while the current one runs.  Not unrolled: a single warp runs it while
+// the rest of the CTA waits, so its code must stay small.
 __device__ __forceinline__ void run_prog(const int* prog, int o_slot, int lane) {
   const int nr = prog[0];
-  const int2* w = reinterpret_cast<const int2*>(prog + 2);  // 8-byte aligned (plan.py _program)
-  int2 cur = nr > 0 ? w[lane] : make_int2(-1, 0);
+  const int2* w = reinterpret_cast<const int2*>(prog + 2) + lane;  // 8-byte aligned (plan.py _program)
+  double* const sl = &g_smem[o_slot];
+  int2 cur = w[0];
 #pragma unroll 1
   for (int r = 0; r < nr; ++r) {
-    const int2 nxt = r + 1 < nr ? w[(r + 1) * 32 + lane] : make_int2(-1, 0);
-    if (cur.x >= 0) {
-      const int d = o_slot + 3 * cur.x, a = o_slot + 3 * (cur.y & 0xffff), c = o_slot + 3 * (cur.y >> 16);
-      const double a0 = g_smem[a], a1 = g_smem[a + 1], a2 = g_smem[a + 2];
-      const double c0 = g_smem[c], c1 = g_smem[c + 1], c2 = g_smem[c + 2];
-      g_smem[d] = dadd(a0, c0);
-      g_smem[d + 1] = dadd(a1, c1);
-      g_smem[d + 2] = dadd(a2, c2);
-    }
+    w += 32;
+    const int2 nxt = w[0];
+    const double* pa = sl + (cur.y & 0xffff);
+    const double* pb = sl + (cur.y >> 16);
+    const double a0 = pa[0], a1 = pa[1], a2 = pa[2];
+    const double b0 = pb[0], b1 = pb[1], b2 = pb[2];
+    double* pd = sl + cur.x;
+    pd[0] = dadd(a0, b0);
+    pd[1] = dadd(a1, b1);
+    pd[2] = dadd(a2, b2);
     __syncwarp();
     cur = nxt;
   }

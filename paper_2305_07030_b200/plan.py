@@ -146,24 +146,29 @@ TREE_HEADER = 10
 PROG_LANES = 32
 
 
-def _program(ops: list[tuple[int, int, int, int]]) -> np.ndarray:
-    """Combine program as warp rounds: [n_rounds, 0, n_rounds x 32 x 2 words]
-    (the pad keeps the word pairs 8-byte aligned on the device).
+def _program(ops: list[tuple[int, int, int, int]], scratch: int) -> np.ndarray:
+    """Combine program as warp rounds: [n_rounds, 0, (n_rounds + 1) x 32 x 2
+    words] (the pad keeps the word pairs 8-byte aligned on the device; the
+    extra idle round lets the device prefetch the next round unconditionally).
     Ops (height, dst, left, right) of one height are independent; each round
-    holds up to 32 of them, one per lane, as the pair (dst, left | right << 16)
-    (dst -1: idle lane).  Rounds run in order with a __syncwarp between them."""
+    holds up to 32 of them, one per lane, as the pair (3 dst, 3 left |
+    3 right << 16) -- slot indices premultiplied by the 3 components.  Idle
+    lanes combine the scratch slot into itself, so the device loop has no
+    branch.  Rounds run in order with a __syncwarp between them."""
     ops = sorted(ops, key=lambda o: o[0])
+    idle = [3 * scratch, 3 * scratch | (3 * scratch << 16)]
     rounds = []
     for h in sorted({o[0] for o in ops}):
         level = [o for o in ops if o[0] == h]
         for i in range(0, len(level), PROG_LANES):
-            words = [-1, 0] * PROG_LANES
+            words = idle * PROG_LANES
             for lane, (_, d, a, b) in enumerate(level[i:i + PROG_LANES]):
-                assert max(d, a, b) < (1 << 15), "tree slot index exceeds 15 bits"
-                words[2 * lane] = d
-                words[2 * lane + 1] = a | (b << 16)
+                assert 3 * max(d, a, b, scratch) < (1 << 16), "tree slot index exceeds 16 bits / 3"
+                words[2 * lane] = 3 * d
+                words[2 * lane + 1] = 3 * a | (3 * b << 16)
             rounds.append(words)
-    return np.array([len(rounds), 0] + [w for r in rounds for w in r], dtype=np.int32)
+    rounds.append(idle * PROG_LANES)
+    return np.array([len(rounds) - 1, 0] + [w for r in rounds for w in r], dtype=np.int32)
 
 
 MODE_QUAD = 4   # the rank's leaves fold in aligned quads inside the chain warps
@@ -174,10 +179,12 @@ def run_program(prog: np.ndarray, slots: list) -> None:
     n = int(prog[0])
     for r in range(n):
         words = prog[2 + 2 * PROG_LANES * r:2 + 2 * PROG_LANES * (r + 1)]
+        new = {}
         for lane in range(PROG_LANES):
             d, w = int(words[2 * lane]), int(words[2 * lane + 1])
-            if d >= 0:
-                slots[d] = slots[w & 0xffff] + slots[w >> 16]
+            new[d // 3] = slots[(w & 0xffff) // 3] + slots[(w >> 16) // 3]
+        for d, v in new.items():
+            slots[d] = v
 
 
 def tree_split(flat: np.ndarray, ranges: list[tuple[int, int]]) -> list[np.ndarray]:
@@ -202,8 +209,10 @@ def tree_split(flat: np.ndarray, ranges: list[tuple[int, int]]) -> list[np.ndarr
     if L == 0:
         blocks = []
         for _ in range(C):
-            blocks.append(np.array([0, 0, TREE_HEADER + 4, TREE_HEADER, TREE_HEADER + 2, TREE_HEADER + 4, 0, -1, 0,
-                                    0, 0, 0, 0, 0], dtype=np.int32))
+            empty = _program([], 0)
+            blocks.append(np.concatenate([
+                np.array([1, 1, TREE_HEADER + 2 * len(empty), TREE_HEADER, TREE_HEADER + len(empty),
+                          TREE_HEADER + 2 * len(empty), 0, -1, 0, 0], dtype=np.int32), empty, empty]))
         return blocks
     n_slots = 2 * L - 1
     lo = np.zeros(n_slots, dtype=np.int64)
@@ -240,11 +249,12 @@ def tree_split(flat: np.ndarray, ranges: list[tuple[int, int]]) -> list[np.ndarr
         h = 1 + max(theight.get(a, 0), theight.get(b, 0))
         theight[d] = h
         top_ops.append((h, int(top_of[d]), int(top_of[a]), int(top_of[b])))
-    TS = E + len(top_internal)
+    TS = E + len(top_internal) + 1            # + a scratch slot for idle lanes
     root_top = int(top_of[p.root])
-    tprog = _program(top_ops)
+    tprog = _program(top_ops, TS - 1)
     blocks = []
     children = {int(p.op_dst[k]): (int(p.op_left[k]), int(p.op_right[k])) for k in range(K)}
+    pending = []
     for r, (a, b) in enumerate(ranges):
         nleaf = b - a
         # quad mode: every aligned group of 4 own leaves is the complete
@@ -286,17 +296,19 @@ def tree_split(flat: np.ndarray, ranges: list[tuple[int, int]]) -> list[np.ndarr
             h = 1 + max(lheight.get(x, 0), lheight.get(y, 0))
             lheight[d] = h
             lops.append((h, int(local_idx[d]), int(local_idx[x]), int(local_idx[y])))
-        lprog = _program(lops)
         exp = np.array([(int(local_idx[sl]), int(top_of[sl])) for sl in exports if owner[sl] == r],
                        dtype=np.int32).reshape(-1)
         mode = MODE_QUAD if quad else 0
+        pending.append((nl, lops, exp, mode))
+    LS = max(nl for nl, _, _, _ in pending) + 1   # + a scratch slot for idle lanes
+    for nl, lops, exp, mode in pending:
+        lprog = _program(lops, LS - 1)
         lprog_off = TREE_HEADER
         tprog_off = lprog_off + len(lprog)
         exp_off = tprog_off + len(tprog)
         hdr = np.array([nl, TS, 0, lprog_off, tprog_off, exp_off, len(exp) // 2, root_top, E, mode],
                        dtype=np.int32)
         blocks.append(np.concatenate([hdr, lprog, tprog, exp]).astype(np.int32))
-    LS = max(int(bk[0]) for bk in blocks)
     PI = max(len(bk) for bk in blocks)
     for bk in blocks:
         bk[0] = LS
