@@ -21,41 +21,49 @@
 //     8*leaf + j sums the stride-8 chain j of its leaf in order, the 8
 //     chains of a leaf sit in 8 consecutive lanes and fold with xor shuffles
 //     1, 2, 4 (= ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7))), tails are added in
-//     order; every rank receives every leaf sum and replays the combine tree
-//     identically, so all ranks take the same decisions.
+//     order; aligned 4-leaf subtrees fold in the same warp (quad mode); the
+//     rank evaluates the subtrees of its own leaves (local program), exports
+//     their roots to every rank, and every rank replays the same top program
+//     over all exports (plan.tree_split), so all ranks take the same
+//     decisions.
 //
 // Work per iteration on each rank (T threads; own DOF d owned by thread d%T):
 //   F1 coefs   per active element (>= 1 own endpoint): EA (l-L)/(L l)
 //   F2 gather  per own node: f = A + B from the coefficients
 //   A  per DOF k_hat, sq = (u k_hat) u, sq2 = (u m) u, ff = f f
-//   C  chains  per (own leaf, chain): ordered sums -> all ranks' tree slots
-//   T  tree    warp 0: pairwise combine, c, residual, convergence
-//   U  per DOF a = -f/m - c v, two half kicks, drift, positions (+ halo push)
+//   C  chains  per (own leaf, chain): ordered sums, folds -> local tree slots
+//   T  tree    warp 0: local program, exports (+ flags, ledger partials) to the
+//              peers, wait, top program, c / residual / convergence; warps
+//              1.. meanwhile form (-f)/m of every own DOF
+//   U  per DOF a = (-f)/m - c v, two half kicks, drift, positions (+ halo push)
 //
-// Cluster exchange (C > 1).  Halo positions (U -> next F) and leaf sums
-// (C -> T) travel as st.async stores into the peers' shared memory, each
+// Cluster exchange (C > 1).  Halo positions (U -> next F) and tree exports
+// (T) travel as st.async stores into the peers' shared memory, each
 // completing a transaction on the receiver's mbarrier; a rank waits on its
 // own mbarriers only.  There is no cluster-wide barrier inside the loop: a
 // cluster barrier's acquire invalidates L1 (CCTL.IVALL), which evicted the
 // read-only tables the loop streams through L1 (profiles/r01_v4_ncu_c2.md).
 // Each rank posts the byte count it expects for a phase (arrive.expect_tx)
 // before any peer can send into that phase: the next halo phase is posted in
-// A (peers send halos only after receiving this rank's leaf sums of C), the
-// next leaf-sum phase right after the current one completes (peers send leaf
-// sums only after this rank's halo push of U).  When a problem ends, the two
-// phases posted for an iteration that will not happen are completed locally
-// (mbarrier.complete_tx) so the barriers are idle for the next problem.
+// A (peers send halos only after receiving this rank's exports of T), the
+// next export phase right after the current one completes (peers send
+// exports only after this rank's halo push of U).  When a problem ends, the
+// two phases posted for an iteration that will not happen are completed
+// locally (mbarrier.complete_tx) so the barriers are idle for the next
+// problem.
 //
 // Shared memory per rank (offsets identical on every rank of a problem so a
-// peer's buffer is addressed by the same offset):
-//   pos  [PN][3]  positions (AoS) of own, halo and fixed local nodes; an own
-//                 DOF's slot holds its sq between A and U.
-//   fcur [NFO]    f from F2; after A it holds ff
-//   fprv [NFO]    f of the previous iteration; after A the current f
-//   cf   [CF]     F1 element coefficients, then sq2
-//   slot [2L-1][3] pairwise-tree slots;  flag[16]: peers' singular flags
-//   prog          the tree's combine program
-// u and v of a thread's own DOFs live in registers.
+// peer's buffer is addressed by the same offset; Layout):
+//   pos   [PN][3]  positions (AoS) of own, halo and fixed local nodes; an own
+//                  DOF's slot holds its sq between A and C.
+//   fcur  [NFO]    f from F2; ff after A; (-f)/m after T
+//   fprv  [NFO]    f of the previous iteration; the current f after A (in
+//                  global memory instead for networks too large for it)
+//   cf    [CF]     F1 element coefficients, then sq2
+//   lslot [LS][3], tslot [TS][3]  local / top tree slots; flag[16] peers'
+//                  singular flags; [16][3] work-ledger partials
+//   prog           the rank's tree block (programs, exports)
+// u, v and the reference coordinates of a thread's own DOFs live in registers.
 
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
@@ -300,16 +308,6 @@ __device__ __noinline__ LenCoef exact_len_coef(double dx, double dy, double dz, 
   return r;
 }
 __device__ __noinline__ double exact_div(double a, double b) { return ddiv(a, b); }
-
-// Length and force coefficient of one element through the fast paths.
-__device__ __forceinline__ LenCoef len_coef(double dx, double dy, double dz, double L, double EA) {
-  bool ok1, ok2;
-  LenCoef r;
-  r.l = frb_arith::sqrt_fast(len2(dx, dy, dz), ok1);
-  r.coef = frb_arith::div_fast(dmul(EA, dsub(r.l, L)), dmul(L, r.l), ok2);
-  if (!(ok1 && ok2)) r = exact_len_coef(dx, dy, dz, L, EA);
-  return r;
-}
 
 // One element's end-force vector nd = d*coef with d = P[b] - P[a] (exact
 // intrinsics; used off the hot path).  Returns true when it collapsed.
