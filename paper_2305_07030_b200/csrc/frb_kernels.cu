@@ -829,7 +829,11 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
   const double* __restrict__ Xg = n.X;
   const double* __restrict__ nmass = n.mass + R.node0;  // own nodes' masses
   const int dof0 = 3 * R.node0;
-  const int dl_max = nfo > 0 ? nfo - 1 : 0;  // clamp for unconditional per-DOF loads
+  // clamp for unconditional per-DOF loads of read-only data (X, masses);
+  // data other threads write (f, f_prev) is only read for owned DOFs
+  const int dl_max = nfo > 0 ? nfo - 1 : 0;
+  const int nk = t < nfo ? (nfo - 1 - t) / T + 1 : 0;  // DOFs this thread owns
+  const int dl_last = t + (nk > 0 ? nk - 1 : 0) * T;
   // hot per-rank tables and sizes, held in registers
   const uint32_t* __restrict__ ell = R.ell;
   const int S = R.S, SA = R.SA, SB = R.SB, n_act = R.n_act;
@@ -939,7 +943,7 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
 #pragma unroll
       for (int kk = 0; kk < kChunk; ++kk) {
         const int dl = min(d0 + kk * nthr, dl_max);
-        q[kk] = frb_arith::div_fast(-FPRV(dl), __ldg(nmass + dl / 3), ok[kk]);
+        q[kk] = frb_arith::div_fast(-FPRV(dl), __ldg(nmass + dl / 3), ok[kk]);  // f_prev is read-only in T
       }
 #pragma unroll
       for (int kk = 0; kk < kChunk; ++kk) {
@@ -1048,6 +1052,7 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
     // ff -> fcur, f -> fprv.
     if (C > 1 && t == 0) mbar_expect(mb.h, R.halo_bytes);  // next halo phase
     double es[3] = {0.0, 0.0, 0.0};
+    if (nk > 0)
 #pragma unroll
     for (int k0 = 0; k0 < MAXK; k0 += kChunk) {
       constexpr int KC = MAXK < kChunk ? MAXK : kChunk;
@@ -1055,7 +1060,9 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
       bool ok[KC];
 #pragma unroll
       for (int kk = 0; kk < KC; ++kk) {
-        const int dl = min(t + (k0 + kk) * T, dl_max);
+        // unowned slots re-read the thread's own last DOF (written only by
+        // this thread, later in program order): no other thread's data
+        const int dl = k0 + kk < nk ? t + (k0 + kk) * T : dl_last;
         f[kk] = g_smem[o.fcur + dl];
         kh[kk] = FPRV(dl);  // f_prev, until the quotient replaces it
         m[kk] = __ldg(nmass + dl / 3);
@@ -1074,10 +1081,8 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
         }
 #pragma unroll
         for (int kk = 0; kk < KC; ++kk) {
-          if (!ok[kk]) {
-            const int dl = min(t + (k0 + kk) * T, dl_max);
-            kh[kk] = exact_div(dsub(f[kk], FPRV(dl)), dmul(dt, v[k0 + kk]));
-          }
+          const int dl = t + (k0 + kk) * T;
+          if (!ok[kk] && dl < nfo) kh[kk] = exact_div(dsub(f[kk], FPRV(dl)), dmul(dt, v[k0 + kk]));
         }
       }
 #pragma unroll
