@@ -63,6 +63,8 @@
 //   cf    [CF]     F1 element coefficients, then sq2
 //   lslot [LS][3], tslot [TS][3]  local / top tree slots; flag[16] peers'
 //                  singular flags; [16][3] work-ledger partials
+//   rm    [NFO/3]  refined reciprocal (div_fast's r2) of each own node's
+//                  mass: (-f)/m then costs 3 FP64 ops instead of 9 + MUFU
 //   prog           the rank's tree block (programs, exports)
 // u, v and the reference coordinates of a thread's own DOFs live in registers.
 
@@ -765,7 +767,7 @@ __device__ __forceinline__ void write_singular(const frb_batch& b, int p, int ba
 // SMEM layout of a problem, in doubles from g_smem (identical on every
 // rank of the problem, so a peer's buffer is addressed by the same offset).
 struct Layout {
-  int pos, fcur, fprv, cf, lslot, tslot, flag, prog;  // prog: int32 index
+  int pos, fcur, fprv, cf, lslot, tslot, flag, rm, prog;  // prog: int32 index
 };
 
 template <bool kFG>
@@ -778,7 +780,8 @@ __device__ __forceinline__ Layout layout(const Rank& R) {
   o.lslot = o.cf + R.CF;
   o.tslot = o.lslot + 3 * R.LS;
   o.flag = o.tslot + 3 * R.TS;
-  o.prog = 2 * (o.flag + 64);  // flags[16], energy partials [16][3]
+  o.rm = o.flag + 64;  // flags[16], energy partials [16][3]
+  o.prog = 2 * (o.rm + R.NFO / 3);  // refined reciprocal masses of the own nodes
   return o;
 }
 
@@ -873,6 +876,7 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
   // the rank's tree block (local + top programs, exports) lives in SMEM
   int* const prog = reinterpret_cast<int*>(g_smem) + o.prog;
   for (int k = t; k < R.tree_len; k += T) prog[k] = __ldg(R.tree + k);
+  for (int i = t; i < n_own; i += T) g_smem[o.rm + i] = frb_arith::rcp_refined(__ldg(nmass + i));
   const int* const lprog = prog + R.tree[3];
   const int* const tprog = prog + R.tree[4];
   const int* const exps = prog + R.tree[5];
@@ -955,7 +959,8 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
 #pragma unroll
       for (int kk = 0; kk < kChunk; ++kk) {
         const int dl = min(d0 + kk * nthr, dl_max);
-        q[kk] = frb_arith::div_fast(-FPRV(dl), __ldg(nmass + dl / 3), ok[kk]);  // f_prev is read-only in T
+        const int i = dl / 3;  // f_prev is read-only in T
+        q[kk] = frb_arith::div_fast_r(-FPRV(dl), __ldg(nmass + i), g_smem[o.rm + i], ok[kk]);
       }
 #pragma unroll
       for (int kk = 0; kk < kChunk; ++kk) {

@@ -205,7 +205,8 @@ def rank_smem_bytes(rt: RankTables, fprv_global: bool = False) -> int:
     sq entry between the force and update phases), f and -- unless it lives
     in global memory -- f_prev (8 B per own DOF each), coefficients / sq2
     max(own DOFs, n_act), local + top tree slots (3 doubles each), 64 cluster
-    flag words and the int32 tree block (programs + exports)."""
+    flag words, one refined reciprocal mass per own node and the int32 tree
+    block (programs + exports)."""
     return smem_bytes(rt.n_local + rt.n_fix, rt.n_own, rt.n_act, int(rt.tree[0]) + int(rt.tree[1]),
                       int(rt.tree[2]), fprv_global)
 
@@ -222,5 +223,5 @@ def partition_smem_bytes(part: "Partition", fprv_global: bool = False) -> int:
 
 def smem_bytes(n_pos: int, n_own: int, n_act: int, n_slots: int, n_prog: int, fprv_global: bool = False) -> int:
     nf = 3 * n_own
-    return 8 * (3 * n_pos + (1 if fprv_global else 2) * nf + max(nf, n_act) + 3 * n_slots + 64) + \
+    return 8 * (3 * n_pos + (1 if fprv_global else 2) * nf + max(nf, n_act) + n_own + 3 * n_slots + 64) + \
         4 * ((n_prog + 1) & ~1)
