@@ -80,18 +80,20 @@ def config_networks(name: str, rank: int, world: int, limit: int | None = None):
     """(workload description, networks, deformation gradients) for one rank."""
     import paper_2305_07030_b200 as frb
     idx = shard_indices(name, rank, world)
+    n_all = len(idx)  # limit=0: the description only (names the whole shard)
     if limit is not None:
         idx = idx[:limit]
+        n_all = n_all if limit == 0 else len(idx)
     if name == "c1":
         return ("c1: 1 x generate_lattice(7,7,8,0.3,seed=0), uniaxial F=diag(1.1,1,1)",
                 [frb.generate_lattice(7, 7, 8, 0.3, 0)], [UNIAX])
     if name == "c2":
-        return (f"c2: {len(idx)} x generate_lattice(15,15,15,0.3,seed=s) per GPU (10,125 DOF, 9,450 fibers), "
+        return (f"c2: {n_all} x generate_lattice(15,15,15,0.3,seed=s) per GPU (10,125 DOF, 9,450 fibers), "
                 "uniaxial F=diag(1.1,1,1)",
                 [frb.generate_lattice(15, 15, 15, 0.3, s) for s in idx], [UNIAX] * len(idx))
     if name == "c3":
         return (f"c3: 1024 x generate_lattice(32,32,32,0.3,seed=s) (98,304 DOF, 95,232 fibers), uniaxial, "
-                f"strided shards ({len(idx)} on this GPU)",
+                f"strided shards ({n_all} on this GPU)",
                 [frb.generate_lattice(32, 32, 32, 0.3, s) for s in idx], [UNIAX] * len(idx))
     if name == "c4":
         nets, Fs = [], []
