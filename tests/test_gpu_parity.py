@@ -217,3 +217,22 @@ def test_fe2_macro_step_reuses_the_packed_batch(cuda_device):
     fresh = frb.solve_batch(frb.pack_batch(nets, [frb.AffineBC(F) for F in F1]))
     for a, b in zip(got, fresh):
         assert a.iters == b.iters and np.array_equal(a.u, b.u) and np.array_equal(a.avg_stress, b.avg_stress)
+
+
+def test_tangent_matches_oracle_differences(cuda_device):
+    """Homogenized tangent: the 19 solves per network run as one
+    device batch; the result equals the oracle's central differences up to
+    the σ bar propagated through the difference quotient."""
+    from paper_2305_07030_b200.tangent import assemble_tangent, perturbed_gradients
+    nets = [frb.generate_lattice(4, 4, 5, 0.3, s) for s in range(2)]
+    Fs = [np.diag([1.05, 1.0, 1.0]), np.eye(3) + 0.1 * np.outer([1, 0, 0], [0, 1, 0])]
+    h = 1e-5
+    res = frb.homogenized_tangent(nets, Fs, h=h)
+    for net, F, r in zip(nets, Fs, res):
+        sig = [orc.solve(net, Fp, frb.SolverConfig()).sigma for Fp in perturbed_gradients(F, h)]
+        C = assemble_tangent(sig, h)
+        S = max(np.abs(s).max() for s in sig)
+        assert r.converged and r.iters.shape == (19,)
+        assert np.abs(r.sigma - sig[0]).max() <= SIGMA_RTOL * S
+        assert np.abs(r.tangent - C).max() <= SIGMA_RTOL * S / h + 1e-15 * np.abs(C).max()
+        assert np.array_equal(r.tangent, r.tangent.transpose(1, 0, 2, 3))
