@@ -443,8 +443,9 @@ __device__ __forceinline__ bool element_coefs(int T, int n_act, const uint32_t* 
 // so their latencies overlap.
 constexpr int kSlots = 3;
 
-// kOne: at most kSlots slots per role (lattices: 3 + 3), a single unrolled group
-template <bool kRoleA, bool kOne>
+// kOne: at most kSlots slots per role, a single unrolled group; kFull:
+// exactly kSlots per role (lattices: 3 + 3), no padding selects
+template <bool kRoleA, bool kOne, bool kFull>
 __device__ __forceinline__ void gather_role(const uint32_t* __restrict__ ell_i, int S, int n_slots, int i,
                                             int o_pos, int o_cf, double px, double py, double pz, double& sx,
                                             double& sy, double& sz) {
@@ -455,7 +456,7 @@ __device__ __forceinline__ void gather_role(const uint32_t* __restrict__ ell_i, 
     // slots past the end become self-padding of node i (a +-0 contribution)
     const uint32_t self_pad = (static_cast<uint32_t>(i) << 16) | (w[0] & 0xffffu);
 #pragma unroll
-    for (int q = 1; q < kSlots; ++q) w[q] = k0 + q < n_slots ? __ldg(ell_i + (k0 + q) * S) : self_pad;
+    for (int q = 1; q < kSlots; ++q) w[q] = kFull || k0 + q < n_slots ? __ldg(ell_i + (k0 + q) * S) : self_pad;
 #pragma unroll
     for (int q = 0; q < kSlots; ++q) {
       const double* po = &g_smem[o_pos + 3 * static_cast<int>(w[q] >> 16)];
@@ -475,35 +476,37 @@ __device__ __forceinline__ void gather_role(const uint32_t* __restrict__ ell_i, 
 
 // f of every own node into g_smem[o_out + 3 i + axis]; a thread gathers two
 // of its nodes together so their load latencies overlap
-template <bool kOne>
+template <bool kOne, bool kFull>
 __device__ __forceinline__ void node_force(const uint32_t* __restrict__ ell, int S, int SA, int SB, int o_pos,
                                            int o_cf, int o_out, int i) {
   const double px = g_smem[o_pos + 3 * i], py = g_smem[o_pos + 3 * i + 1], pz = g_smem[o_pos + 3 * i + 2];
   double ax = 0.0, ay = 0.0, az = 0.0, bx = 0.0, by = 0.0, bz = 0.0;
-  gather_role<true, kOne>(ell + i, S, SA, i, o_pos, o_cf, px, py, pz, ax, ay, az);
-  gather_role<false, kOne>(ell + SA * S + i, S, SB, i, o_pos, o_cf, px, py, pz, bx, by, bz);
+  gather_role<true, kOne, kFull>(ell + i, S, SA, i, o_pos, o_cf, px, py, pz, ax, ay, az);
+  gather_role<false, kOne, kFull>(ell + SA * S + i, S, SB, i, o_pos, o_cf, px, py, pz, bx, by, bz);
   g_smem[o_out + 3 * i] = dadd(ax, bx);
   g_smem[o_out + 3 * i + 1] = dadd(ay, by);
   g_smem[o_out + 3 * i + 2] = dadd(az, bz);
 }
 
-template <bool kOne>
+template <bool kOne, bool kFull>
 __device__ __forceinline__ void node_forces_t(int T, int n_own, const uint32_t* __restrict__ ell, int S, int SA,
                                               int SB, int o_pos, int o_cf, int o_out) {
   int i = threadIdx.x;
   for (; i + T < n_own; i += 2 * T) {
-    node_force<kOne>(ell, S, SA, SB, o_pos, o_cf, o_out, i);
-    node_force<kOne>(ell, S, SA, SB, o_pos, o_cf, o_out, i + T);
+    node_force<kOne, kFull>(ell, S, SA, SB, o_pos, o_cf, o_out, i);
+    node_force<kOne, kFull>(ell, S, SA, SB, o_pos, o_cf, o_out, i + T);
   }
-  if (i < n_own) node_force<kOne>(ell, S, SA, SB, o_pos, o_cf, o_out, i);
+  if (i < n_own) node_force<kOne, kFull>(ell, S, SA, SB, o_pos, o_cf, o_out, i);
 }
 
 __device__ __forceinline__ void node_forces(int T, int n_own, const uint32_t* __restrict__ ell, int S, int SA, int SB,
                                             int o_pos, int o_cf, int o_out) {
-  if (SA <= kSlots && SB <= kSlots) {  // uniform: a lattice's 3 + 3 incidences
-    node_forces_t<true>(T, n_own, ell, S, SA, SB, o_pos, o_cf, o_out);
+  if (SA == kSlots && SB == kSlots) {  // a lattice's 3 + 3 incidences
+    node_forces_t<true, true>(T, n_own, ell, S, SA, SB, o_pos, o_cf, o_out);
+  } else if (SA <= kSlots && SB <= kSlots) {
+    node_forces_t<true, false>(T, n_own, ell, S, SA, SB, o_pos, o_cf, o_out);
   } else {
-    node_forces_t<false>(T, n_own, ell, S, SA, SB, o_pos, o_cf, o_out);
+    node_forces_t<false, false>(T, n_own, ell, S, SA, SB, o_pos, o_cf, o_out);
   }
 }
 

@@ -236,3 +236,20 @@ def test_tangent_matches_oracle_differences(cuda_device):
         assert np.abs(r.sigma - sig[0]).max() <= SIGMA_RTOL * S
         assert np.abs(r.tangent - C).max() <= SIGMA_RTOL * S / h + 1e-15 * np.abs(C).max()
         assert np.array_equal(r.tangent, r.tangent.transpose(1, 0, 2, 3))
+
+
+def test_two_slot_network_vs_oracle(cuda_device):
+    """A lattice without its z-links has at most 2 slots per role: the
+    padded (<= 3 slots) gather path, 400 iterations bit for bit."""
+    net = frb.generate_lattice(5, 5, 4, 0.3, 0)
+    X, E = net.node_coords, net.elements
+    d = np.abs(X[E[:, 1]] - X[E[:, 0]])
+    net2 = frb.FiberNetwork(X, E[d[:, 2] < 0.5 * np.maximum(d[:, 0], d[:, 1])], net.materials,
+                            net.boundary_nodes, rve_volume=net.volume)
+    part, _ = fb.build_problem(net2, frb.AffineBC(np.eye(3))).topo.choose_cluster()
+    assert (part.slots_a, part.slots_b) == (2, 2)
+    F = np.diag([1.1, 1.0, 1.0])
+    cfg = frb.SolverConfig(max_iters=400)
+    r = frb.dynamic_relaxation_solve(net2, frb.AffineBC(F), cfg)
+    o = orc.solve(net2, F, cfg)
+    assert_matches(r, o.u, o.iters, o.converged, o.residual, o.r_ref, o.sigma, label="2-slot")
