@@ -1099,10 +1099,15 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
             ok[kk] = true;
           }
         }
+        bool all_ok = true;
 #pragma unroll
-        for (int kk = 0; kk < KC; ++kk) {
-          const int dl = t + (k0 + kk) * T;
-          if (!ok[kk] && dl < nfo) kh[kk] = exact_div(dsub(f[kk], FPRV(dl)), dmul(dt, v[k0 + kk]));
+        for (int kk = 0; kk < KC; ++kk) all_ok &= ok[kk];
+        if (!all_ok) {  // one branch per chunk: the rare exact fallbacks
+#pragma unroll
+          for (int kk = 0; kk < KC; ++kk) {
+            const int dl = t + (k0 + kk) * T;
+            if (!ok[kk] && dl < nfo) kh[kk] = exact_div(dsub(f[kk], FPRV(dl)), dmul(dt, v[k0 + kk]));
+          }
         }
       }
 #pragma unroll
