@@ -965,13 +965,20 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
         const int i = dl / 3;  // f_prev is read-only in T
         q[kk] = frb_arith::div_fast_r(-FPRV(dl), __ldg(nmass + i), g_smem[o.rm + i], ok[kk]);
       }
+      bool all_ok = true;
+#pragma unroll
+      for (int kk = 0; kk < kChunk; ++kk) all_ok &= ok[kk];
+      if (!all_ok) {  // one branch per chunk: the rare exact fallbacks
+#pragma unroll
+        for (int kk = 0; kk < kChunk; ++kk) {
+          const int dl = d0 + kk * nthr;
+          if (!ok[kk] && dl < nfo) q[kk] = exact_div(-FPRV(dl), __ldg(nmass + dl / 3));
+        }
+      }
 #pragma unroll
       for (int kk = 0; kk < kChunk; ++kk) {
         const int dl = d0 + kk * nthr;
-        if (dl < nfo) {
-          if (!ok[kk]) q[kk] = exact_div(-FPRV(dl), __ldg(nmass + dl / 3));
-          g_smem[o.fcur + dl] = q[kk];
-        }
+        if (dl < nfo) g_smem[o.fcur + dl] = q[kk];
       }
     }
   };
