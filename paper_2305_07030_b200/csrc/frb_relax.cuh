@@ -934,10 +934,8 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
   }
 
   // new position of own DOF k (= dl): local slot + the halo copies of peers
-  auto put_pos = [&](int k, int dl, double x) {
-    g_smem[o.pos + dl] = x;
-    if (eramp && alpha < 1.0) n.posg[dof0 + dl] = x;  // ramp reactions read every position
-    if (C > 1 && ((sendbits >> k) & 1u)) {
+  auto send_pos = [&](int dl, double x) {
+    {
       const int node = dl / 3, axis = dl - 3 * node;
       const int2 tg = __ldg(send + node);
       if (tg.x >= 0) {
@@ -949,6 +947,14 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
         st_async(sc.peer_smem[qr] + peer_pos + 8u * (3u * (tg.y & 0xffffff) + axis), x, sc.peer_bar_h[qr]);
       }
     }
+  };
+  auto put_local = [&](int dl, double x) {
+    g_smem[o.pos + dl] = x;
+    if (eramp && alpha < 1.0) n.posg[dof0 + dl] = x;  // ramp reactions read every position
+  };
+  auto put_pos = [&](int k, int dl, double x) {
+    put_local(dl, x);
+    if (C > 1 && ((sendbits >> k) & 1u)) send_pos(dl, x);
   };
 
   // (-f)/m of every own DOF into its f slot of SMEM (free once C has
@@ -1357,8 +1363,14 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
         if (!done) {
           v[k] = dadd(v[k], dmul(hdt, a));
           u[k] = dadd(u[k], dmul(dt, v[k]));
-          put_pos(k, dl, dadd(xr[k], u[k]));
+          put_local(dl, dadd(xr[k], u[k]));
         }
+      }
+    }
+    if (C > 1 && !done) {  // halo copies to the peers: only the few DOFs that have one
+      for (uint32_t bits = sendbits; bits; bits &= bits - 1) {
+        const int dl = t + (__ffs(bits) - 1) * T;
+        send_pos(dl, g_smem[o.pos + dl]);
       }
     }
     if (!done && ramp && alpha < 1.0) {
