@@ -75,6 +75,8 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <type_traits>
+
 #include "frb200.h"
 #include "frb_arith.cuh"
 
@@ -1085,63 +1087,72 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
     // ff -> fcur, f -> fprv.
     if (C > 1 && t == 0) mbar_expect(mb.h, R.halo_bytes);  // next halo phase
     double es[3] = {0.0, 0.0, 0.0};
-    if (nk > 0)
+    // damping mode hoisted out of the per-DOF loop (one copy per mode)
+    auto a_phase = [&](auto ad) {
+      constexpr bool kAd = decltype(ad)::value;
+      if (nk > 0)
 #pragma unroll
-    for (int k0 = 0; k0 < MAXK; k0 += kChunk) {
-      constexpr int KC = MAXK < kChunk ? MAXK : kChunk;
-      double f[KC], kh[KC], m[KC];
-      bool ok[KC];
-#pragma unroll
-      for (int kk = 0; kk < KC; ++kk) {
-        // unowned slots re-read the thread's own last DOF (written only by
-        // this thread, later in program order): no other thread's data
-        const int dl = k0 + kk < nk ? t + (k0 + kk) * T : dl_last;
-        f[kk] = g_smem[o.fcur + dl];
-        kh[kk] = FPRV(dl);  // f_prev, until the quotient replaces it
-        m[kk] = __ldg(nmass + dl / 3);
-      }
-      if (adaptive) {
+      for (int k0 = 0; k0 < MAXK; k0 += kChunk) {
+        constexpr int KC = MAXK < kChunk ? MAXK : kChunk;
+        double f[KC], kh[KC], m[KC];
+        bool ok[KC];
 #pragma unroll
         for (int kk = 0; kk < KC; ++kk) {
-          const double vk = k0 + kk < MAXK ? v[k0 + kk] : 0.0;
-          const double den = dmul(dt, vk);
-          const double num = dsub(f[kk], kh[kk]);
-          kh[kk] = frb_arith::div_fast(num, den, ok[kk]);
-          if (den == 0.0) {
-            kh[kk] = 0.0;
-            ok[kk] = true;
-          }
+          // unowned slots re-read the thread's own last DOF (written only by
+          // this thread, later in program order): no other thread's data
+          const int dl = k0 + kk < nk ? t + (k0 + kk) * T : dl_last;
+          f[kk] = g_smem[o.fcur + dl];
+          kh[kk] = FPRV(dl);  // f_prev, until the quotient replaces it
+          m[kk] = __ldg(nmass + dl / 3);
         }
-        bool all_ok = true;
-#pragma unroll
-        for (int kk = 0; kk < KC; ++kk) all_ok &= ok[kk];
-        if (!all_ok) {  // one branch per chunk: the rare exact fallbacks
+        if constexpr (kAd) {
 #pragma unroll
           for (int kk = 0; kk < KC; ++kk) {
-            const int dl = t + (k0 + kk) * T;
-            if (!ok[kk] && dl < nfo) kh[kk] = exact_div(dsub(f[kk], FPRV(dl)), dmul(dt, v[k0 + kk]));
+            const double vk = k0 + kk < MAXK ? v[k0 + kk] : 0.0;
+            const double den = dmul(dt, vk);
+            const double num = dsub(f[kk], kh[kk]);
+            kh[kk] = frb_arith::div_fast(num, den, ok[kk]);
+            if (den == 0.0) {
+              kh[kk] = 0.0;
+              ok[kk] = true;
+            }
           }
-        }
-      }
+          bool all_ok = true;
 #pragma unroll
-      for (int kk = 0; kk < KC; ++kk) {
-        const int k = k0 + kk, dl = t + k * T;
-        if (k < MAXK && dl < nfo) {
-          if (adaptive) {
-            const double khc = (kh[kk] > 0.0 || isnan(kh[kk])) ? kh[kk] : 0.0;
-            g_smem[o.pos + dl] = dmul(dmul(u[k], khc), u[k]);
-            g_smem[o.cf + dl] = dmul(dmul(u[k], m[kk]), u[k]);
+          for (int kk = 0; kk < KC; ++kk) all_ok &= ok[kk];
+          if (!all_ok) {  // one branch per chunk: the rare exact fallbacks
+#pragma unroll
+            for (int kk = 0; kk < KC; ++kk) {
+              const int dl = t + (k0 + kk) * T;
+              if (!ok[kk] && dl < nfo) kh[kk] = exact_div(dsub(f[kk], FPRV(dl)), dmul(dt, v[k0 + kk]));
+            }
           }
-          g_smem[o.fcur + dl] = dmul(f[kk], f[kk]);
-          if (energy) {  // f . v_half, f_prev . v_half, (m v_half) . v_half (:538-544)
-            const double vh = v[k];
-            es[0] = dadd(es[0], dmul(f[kk], vh));
-            es[1] = dadd(es[1], dmul(FPRV(dl), vh));
-            es[2] = dadd(es[2], dmul(dmul(m[kk], vh), vh));
+        }
+#pragma unroll
+        for (int kk = 0; kk < KC; ++kk) {
+          const int k = k0 + kk, dl = t + k * T;
+          if (k < MAXK && dl < nfo) {
+            if constexpr (kAd) {
+              const double khc = (kh[kk] > 0.0 || isnan(kh[kk])) ? kh[kk] : 0.0;
+              g_smem[o.pos + dl] = dmul(dmul(u[k], khc), u[k]);
+              g_smem[o.cf + dl] = dmul(dmul(u[k], m[kk]), u[k]);
+            }
+            g_smem[o.fcur + dl] = dmul(f[kk], f[kk]);
+            if (energy) {  // f . v_half, f_prev . v_half, (m v_half) . v_half (:538-544)
+              const double vh = v[k];
+              es[0] = dadd(es[0], dmul(f[kk], vh));
+              es[1] = dadd(es[1], dmul(FPRV(dl), vh));
+              es[2] = dadd(es[2], dmul(dmul(m[kk], vh), vh));
+            }
+            SET_FPRV(dl, f[kk]);
           }
-          SET_FPRV(dl, f[kk]);
         }
       }
+    };
+    if (adaptive) {
+      a_phase(std::true_type{});
+    } else {
+      a_phase(std::false_type{});
     }
     if (energy) {  // warp partials of the ledger dots -> sc.red
 #pragma unroll
