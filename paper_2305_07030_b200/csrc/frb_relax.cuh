@@ -91,7 +91,10 @@ namespace {
 constexpr int kMaxThreads = 1024;
 constexpr int kMaxWarps = kMaxThreads / 32;
 constexpr double kCollapse = 1e-12;  // microsolver.py:30
-constexpr int kChunk = 4;
+#ifndef FRB_KCHUNK
+#define FRB_KCHUNK 4
+#endif
+constexpr int kChunk = FRB_KCHUNK;
 // instrumentation slots (frb_batch.phase_cycles): F1, F2, A, C, T local tree +
 // exports, T exchange wait, T top tree + scalars, U, epilogue, prologue, halo wait
 constexpr int kPhases = 12;
