@@ -795,7 +795,7 @@ __device__ __forceinline__ Layout layout(const Rank& R) {
 
 // Replay one combine program (plan.py _program: warp rounds of up to 32
 // independent ops, lane-packed, slot indices premultiplied by 3, idle lanes
-// folding a scratch slot, one idle pad round) on g_smem[o_slot + ...] with
+// folding their own scratch slots, one idle pad round) on g_smem[o_slot + ...] with
 // the calling warp: no branch in the loop, the next round's op is fetched
 // while the current one runs.  Not unrolled: a single warp runs it while
 // the rest of the CTA waits, so its code must stay small.

@@ -153,21 +153,24 @@ def _program(ops: list[tuple[int, int, int, int]], scratch: int) -> np.ndarray:
     Ops (height, dst, left, right) of one height are independent; each round
     holds up to 32 of them, one per lane, as the pair (3 dst, 3 left |
     3 right << 16) -- slot indices premultiplied by the 3 components.  Idle
-    lanes combine the scratch slot into itself, so the device loop has no
-    branch.  Rounds run in order with a __syncwarp between them."""
+    lane l combines its own scratch slot `scratch + l` into itself, so the
+    device loop has no branch and no two lanes touch the same slot.  Rounds
+    run in order with a __syncwarp between them."""
     ops = sorted(ops, key=lambda o: o[0])
-    idle = [3 * scratch, 3 * scratch | (3 * scratch << 16)]
+    assert 3 * (scratch + PROG_LANES - 1) < (1 << 16), "tree slot index exceeds 16 bits / 3"
+    idle = [w for lane in range(PROG_LANES)
+            for w in (3 * (scratch + lane), 3 * (scratch + lane) | (3 * (scratch + lane) << 16))]
     rounds = []
     for h in sorted({o[0] for o in ops}):
         level = [o for o in ops if o[0] == h]
         for i in range(0, len(level), PROG_LANES):
-            words = idle * PROG_LANES
+            words = list(idle)
             for lane, (_, d, a, b) in enumerate(level[i:i + PROG_LANES]):
-                assert 3 * max(d, a, b, scratch) < (1 << 16), "tree slot index exceeds 16 bits / 3"
+                assert 3 * max(d, a, b) < (1 << 16), "tree slot index exceeds 16 bits / 3"
                 words[2 * lane] = 3 * d
                 words[2 * lane + 1] = 3 * a | (3 * b << 16)
             rounds.append(words)
-    rounds.append(idle * PROG_LANES)
+    rounds.append(list(idle))
     return np.array([len(rounds) - 1, 0] + [w for r in rounds for w in r], dtype=np.int32)
 
 
@@ -249,9 +252,9 @@ def tree_split(flat: np.ndarray, ranges: list[tuple[int, int]]) -> list[np.ndarr
         h = 1 + max(theight.get(a, 0), theight.get(b, 0))
         theight[d] = h
         top_ops.append((h, int(top_of[d]), int(top_of[a]), int(top_of[b])))
-    TS = E + len(top_internal) + 1            # + a scratch slot for idle lanes
+    TS = E + len(top_internal) + PROG_LANES   # + a scratch slot per lane for idle lanes
     root_top = int(top_of[p.root])
-    tprog = _program(top_ops, TS - 1)
+    tprog = _program(top_ops, TS - PROG_LANES)
     blocks = []
     children = {int(p.op_dst[k]): (int(p.op_left[k]), int(p.op_right[k])) for k in range(K)}
     pending = []
@@ -300,9 +303,9 @@ def tree_split(flat: np.ndarray, ranges: list[tuple[int, int]]) -> list[np.ndarr
                        dtype=np.int32).reshape(-1)
         mode = MODE_QUAD if quad else 0
         pending.append((nl, lops, exp, mode))
-    LS = max(nl for nl, _, _, _ in pending) + 1   # + a scratch slot for idle lanes
+    LS = max(nl for nl, _, _, _ in pending) + PROG_LANES   # + a scratch slot per lane for idle lanes
     for nl, lops, exp, mode in pending:
-        lprog = _program(lops, LS - 1)
+        lprog = _program(lops, LS - PROG_LANES)
         lprog_off = TREE_HEADER
         tprog_off = lprog_off + len(lprog)
         exp_off = tprog_off + len(tprog)
