@@ -253,6 +253,8 @@ class Batch:
     arrays: dict                       # flat host arrays uploaded to the device
     node_base: np.ndarray              # (P+1,) int64 node offsets
     _packed_state: dict | None = field(default=None, repr=False)
+    _orig_rows: np.ndarray | None = field(default=None, repr=False)  # solver -> original node rows
+    _u_pinned: object = field(default=None, repr=False)               # reused pinned download buffer
     pinned: dict | None = field(default=None, repr=False)
 
     @property
@@ -589,8 +591,21 @@ def config_struct(cfg: SolverConfig) -> nat.FrbConfig:
 
 def results_to_solve_results(batch: Batch, dres: DeviceResults, raise_singular: bool = True):
     """Download and unpermute (DofMap.unpermute, dofmap.py:33-38)."""
+    torch = _torch()
     rec = dres.host_results()
-    u_all = dres.u.cpu().numpy()
+    # one pinned download, one row gather for every problem (solver -> original node order)
+    u_pin = batch._u_pinned
+    if u_pin is None or u_pin.shape != dres.u.shape:
+        u_pin = batch._u_pinned = torch.empty(dres.u.shape, dtype=dres.u.dtype, pin_memory=True)
+    u_pin.copy_(dres.u)
+    u_all = u_pin.numpy().reshape(-1, 3)
+    if batch._orig_rows is None:
+        rows = np.empty(int(batch.node_base[-1]), dtype=np.int64)
+        for i, p in enumerate(batch.problems):
+            b0 = int(batch.node_base[i])
+            rows[b0 + p.node_order] = b0 + np.arange(len(p.node_order))
+        batch._orig_rows = rows
+    u_orig = u_all[batch._orig_rows].reshape(-1)
     out = []
     first_bad = None
     for i, p in enumerate(batch.problems):
@@ -600,9 +615,7 @@ def results_to_solve_results(batch: Batch, dres: DeviceResults, raise_singular: 
                 first_bad = (i, int(r["bad_element"]))
             out.append(None)
             continue
-        b0, b1 = 3 * int(batch.node_base[i]), 3 * int(batch.node_base[i + 1])
-        u = np.empty(b1 - b0)
-        u.reshape(-1, 3)[p.node_order] = u_all[b0:b1].reshape(-1, 3)
+        u = u_orig[3 * int(batch.node_base[i]):3 * int(batch.node_base[i + 1])]
         e = float(r["energy_residual"])
         out.append(SolveResult(converged=bool(r["converged"]), iters=int(r["iters"]),
                                final_residual=float(r["final_residual"]), u=u,
