@@ -3,7 +3,7 @@ reference ``pkg/src/fibrelax/microsolver.py``).
 
 The relaxation loop itself (reference ``_relax``, ``microsolver.py:379-530``,
 plus ``finalize_result`` ``:549-564``) runs on the B200 inside one persistent
-CUDA kernel (``csrc/frb_kernels.cu``) reached through the C-ABI
+CUDA kernel (``csrc/frb_relax.cuh``) reached through the C-ABI
 ``libfrb200.so``.  This module keeps the reference's public types, their
 validation, and the small host-side helpers; ``dynamic_relaxation_solve`` is
 a batch of one through ``batch.solve_batch``.  There is no CPU fallback: if

@@ -13,7 +13,7 @@ builds it once per distinct free-DOF count and the kernel replays it:
 * combine ops (dst, left, right) over slots [leaves..., internal...], grouped
   by height so every op of one level is independent (one lane per op).
 
-Flat int32 layout consumed by ``csrc/frb_kernels.cu`` (``PlanView``):
+Flat int32 layout consumed by ``csrc/frb_relax.cuh`` (``PlanView``):
     [n_leaves, n_levels, root, pad,
      leaf_start[L], leaf_size[L], level_off[n_levels + 1],
      op_dst[K], op_left[K], op_right[K]]          K = L - 1
