@@ -15,7 +15,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("FRB_LIB") or os.path.join(HERE, "lib", "libfrb200.so")
 
-ABI_VERSION = 6
+ABI_VERSION = 7
 MAX_CLUSTER = 16
 FRB_OK, FRB_E_INVALID, FRB_E_TOO_LARGE, FRB_E_CUDA, FRB_E_UNSUPPORTED = 0, -1, -2, -3, -4
 STATUS_CONVERGED, STATUS_MAX_ITERS, STATUS_SINGULAR = 0, 1, 2
@@ -65,14 +65,16 @@ PART_DTYPE = np.dtype([
 GROUP_DTYPE = np.dtype([
     ("cluster", "<i4"), ("first", "<i4"), ("count", "<i4"), ("block_threads", "<i4"),
     ("smem_bytes", "<i4"), ("max_own_dofs", "<i4"), ("grid_clusters", "<i4"), ("fprv_global", "<i4"),
+    ("max_rank_leaves", "<i4"), ("flags", "<i4"),
 ])
+GF_SERIAL = 1
 RESULT_DTYPE = np.dtype([
     ("status", "<i4"), ("iters", "<i4"), ("bad_element", "<i4"), ("converged", "<i4"),
     ("final_residual", "<f8"), ("r_ref", "<f8"), ("energy_residual", "<f8"),
     ("avg_stress", "<f8", (9,)), ("energy", "<f8", (4,)),
 ])
 assert PROBLEM_DTYPE.itemsize == 168 and PART_DTYPE.itemsize == 104
-assert GROUP_DTYPE.itemsize == 32 and RESULT_DTYPE.itemsize == 144
+assert GROUP_DTYPE.itemsize == 40 and RESULT_DTYPE.itemsize == 144
 
 
 class NativeError(RuntimeError):

@@ -82,17 +82,26 @@ class NaiveLoop:
 @dataclass(frozen=True)
 class TeamBatched:
     """Shared work queue; each team (a CTA cluster) runs whole solves
-    (SPEC.md:361).  teams=None sizes the persistent grid by occupancy;
-    team_size overrides the threads per CTA."""
+    (SPEC.md:361).  teams=None sizes the persistent grid by occupancy.
+
+    team_size is the spec's lanes per team (any value >= 1).  On
+    the device a lane is a thread and a team is one CTA per cluster rank, so
+    the CTA gets ``cta_threads(team_size)`` threads: team_size rounded up to a
+    whole number of 32-thread warps (at least 32, at most 1024).  The kernel
+    template then runs the smallest of 256 / 512 / 768 / 1024 threads that
+    holds it; results are bit-identical for every team size."""
     teams: int | None = None
     team_size: int | None = None
 
     def __post_init__(self):
         if self.teams is not None and self.teams < 1:
             raise ValueError("teams must be >= 1")
-        if self.team_size is not None and (self.team_size < 32 or self.team_size % 32
-                                           or self.team_size > MAX_CTA_THREADS):
-            raise ValueError("team_size must be a multiple of 32 in [32, 1024]")
+        if self.team_size is not None and not 1 <= self.team_size <= MAX_CTA_THREADS:
+            raise ValueError(f"team_size must be in [1, {MAX_CTA_THREADS}] (lanes = CTA threads)")
+
+    @staticmethod
+    def cta_threads(team_size: int) -> int:
+        return max(32, 32 * math.ceil(team_size / 32))
 
 
 ExecutionStrategy = SerialReference | NaiveLoop | TeamBatched
@@ -131,15 +140,23 @@ class Topology:
         smallest cluster that fits with f_prev in global memory (32^3)."""
         nf = 3 * self.n_free_nodes
         want = max(1, math.ceil(nf / DOFS_PER_RANK))
+        reasons = []
         for fprv_global in (False, True):  # on-chip f_prev at any cluster size first
             for C in CLUSTER_SIZES:
                 if C < want and C != CLUSTER_SIZES[-1]:
                     continue
-                part = self.partition(C)
+                try:
+                    part = self.partition(C)
+                except ValueError as e:  # e.g. a node that is halo to more than two ranks
+                    reasons.append(f"C={C}: {e}")
+                    continue
                 if partition_smem_bytes(part, fprv_global) <= SMEM_BUDGET:
                     return part, fprv_global
+                reasons.append(f"C={C}{' (f_prev global)' if fprv_global else ''}: "
+                               f"{partition_smem_bytes(part, fprv_global)} B of SMEM per rank")
         raise nat.NativeError(nat.FRB_E_TOO_LARGE,
-                              f"network with {nf} free DOFs does not fit a {CLUSTER_SIZES[-1]}-CTA cluster")
+                              f"network with {nf} free DOFs fits no cluster of {CLUSTER_SIZES} CTAs ("
+                              + "; ".join(dict.fromkeys(reasons)) + ")")
 
 
 def _topology(network: FiberNetwork, node_rank: np.ndarray, n_free_nodes: int) -> Topology:
@@ -418,6 +435,7 @@ def _pack(networks, bcs, probs, cluster: int | None = None) -> Batch:
         g["block_threads"] = _group_threads(own, leaves, len(ids), C, fglob)
         g["smem_bytes"], g["max_own_dofs"] = smem, own
         g["fprv_global"] = int(fglob)
+        g["max_rank_leaves"] = leaves
         groups.append(g)
         order.extend(ids)
     arrays = dict(
@@ -506,15 +524,23 @@ class DeviceBatch:
         for g in groups:
             if isinstance(strategy, TeamBatched):
                 if strategy.team_size is not None:
-                    g["block_threads"] = strategy.team_size
+                    g["block_threads"] = TeamBatched.cta_threads(strategy.team_size)
                 if strategy.teams is not None:
                     g["grid_clusters"] = strategy.teams
             elif isinstance(strategy, SerialReference):
                 g["grid_clusters"] = 1
+                g["flags"] |= nat.GF_SERIAL  # groups one after another on the caller's stream
             T = int(g["block_threads"])
             if int(g["max_own_dofs"]) > dofs_per_thread_cap(T) * T:
                 raise nat.NativeError(nat.FRB_E_TOO_LARGE,
                                       f"team_size {T} cannot hold {int(g['max_own_dofs'])} own DOFs")
+            ledger_T = min(T, 512) if cfg.energy_check_interval > 0 else T
+            if ledger_T < 8 * int(g["max_rank_leaves"]):
+                raise nat.NativeError(
+                    nat.FRB_E_INVALID,
+                    f"a team of {ledger_T} threads is below the {8 * int(g['max_rank_leaves'])} the pairwise "
+                    f"chain sums of a rank need (8 per leaf, {int(g['max_rank_leaves'])} leaves)"
+                    + ("; the work-ledger kernels run at most 512 threads" if ledger_T < T else ""))
         n = int(h.node_base[-1])
         dev = self.device
         u = torch.empty(3 * n, dtype=torch.float64, device=dev)

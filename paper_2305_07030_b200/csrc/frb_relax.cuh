@@ -61,8 +61,14 @@
 //   fprv  [NFO]    f of the previous iteration; the current f after A (in
 //                  global memory instead for networks too large for it)
 //   cf    [CF]     F1 element coefficients, then sq2
-//   lslot [LS][3], tslot [TS][3]  local / top tree slots; flag[16] peers'
-//                  singular flags; [16][3] work-ledger partials
+//   lslot [LS][3]  local tree slots
+//   tslot [2][TS][3], flag [2][64]  top tree slots and the peers' singular
+//                  flags [16] + work-ledger partials [16][3], double-buffered
+//                  by iteration parity: a peer that is not a halo neighbour
+//                  can run one iteration ahead and send its next exports
+//                  while this rank still reads the current ones (it cannot
+//                  run two ahead: that needs this rank's next exports)
+//   fin  [16]      per-rank final kinetic-energy partials (epilogue)
 //   rm    [NFO/3]  refined reciprocal (div_fast's r2) of each own node's
 //                  mass: (-f)/m then costs 3 FP64 ops instead of 9 + MUFU
 //   prog           the rank's tree block (programs, exports)
@@ -787,8 +793,8 @@ __device__ __forceinline__ Layout layout(const Rank& R) {
   o.cf = o.fprv + (kFG ? 0 : R.NFO);
   o.lslot = o.cf + R.CF;
   o.tslot = o.lslot + 3 * R.LS;
-  o.flag = o.tslot + 3 * R.TS;
-  o.rm = o.flag + 64;  // flags[16], energy partials [16][3]
+  o.flag = o.tslot + 6 * R.TS;  // two parity buffers of top slots
+  o.rm = o.flag + 2 * 64 + 16;    // two parity buffers of flags[16] + partials[16][3]; fin[16]
   o.prog = 2 * (o.rm + R.NFO / 3);  // refined reciprocal masses of the own nodes
   return o;
 }
@@ -866,7 +872,6 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
   const double ea = n.ea;
   const int2* __restrict__ send = R.send;
   const uint32_t peer_pos = 8u * o.pos;  // byte offsets in a peer's dynamic SMEM
-  const uint32_t peer_tslot = 8u * o.tslot, peer_flag = 8u * o.flag;
   // f_prev of own DOF dl: SMEM, or the `f` output array for networks too
   // large for the cluster's SMEM (it ends up holding the final f either way)
   double* const fprv_g = b.f + 3 * n.node_base + dof0;
@@ -1246,20 +1251,27 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
     // rank (with this rank's singular flag), the top tree over all ranks'
     // exports, then the scalar bookkeeping.  Meanwhile the other warps
     // compute U's c-independent part, fm = (-f)/m (warp 0 does after T).
+#ifndef FRB_NO_SHADOW
     if (T > 32 && t >= 32) accel(32, T - 32);
+#endif
     if (t < 32) {
+      const int ob = static_cast<int>(mb.ph_s);  // exchange buffer of this iteration's parity
+      const int o_ts = o.tslot + ob * 3 * R.TS, o_fl = o.flag + ob * 64;
       run_prog(lprog, o.lslot, lane);
       mark(sc, prof, PH_TLP);
+      // every (export, rank) pair on its own lane: the own copy for qr ==
+      // rank, three st.async into the peer's top slots otherwise
 #pragma unroll 1
-      for (int x = lane; x < n_exp; x += 32) {
-        const int ls = o.lslot + 3 * exps[2 * x], ts = 3 * exps[2 * x + 1];
+      for (int x = lane; x < n_exp * C; x += 32) {
+        const int e = x / C, qr = x - e * C;
+        const int ls = o.lslot + 3 * exps[2 * e], ts = 3 * exps[2 * e + 1];
         const double v0 = g_smem[ls], v1 = g_smem[ls + 1], v2 = g_smem[ls + 2];
-        g_smem[o.tslot + ts] = v0;
-        g_smem[o.tslot + ts + 1] = v1;
-        g_smem[o.tslot + ts + 2] = v2;
-        for (int qr = 0; qr < C; ++qr) {
-          if (qr == rank) continue;
-          const uint32_t ad = sc.peer_smem[qr] + peer_tslot + 8u * ts;
+        if (qr == rank) {
+          g_smem[o_ts + ts] = v0;
+          g_smem[o_ts + ts + 1] = v1;
+          g_smem[o_ts + ts + 2] = v2;
+        } else {
+          const uint32_t ad = sc.peer_smem[qr] + 8u * (o_ts + ts);
           st_async(ad, v0, sc.peer_bar_s[qr]);
           st_async(ad + 8, v1, sc.peer_bar_s[qr]);
           st_async(ad + 16, v2, sc.peer_bar_s[qr]);
@@ -1270,16 +1282,16 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
         double e3[3] = {0.0, 0.0, 0.0};
         for (int wp = 0; wp < (T + 31) / 32; ++wp)
           for (int e = 0; e < 3; ++e) e3[e] = dadd(e3[e], sc.red[wp * 9 + e]);
-        for (int e = 0; e < 3; ++e) g_smem[o.flag + 16 + 3 * rank + e] = e3[e];
+        for (int e = 0; e < 3; ++e) g_smem[o_fl + 16 + 3 * rank + e] = e3[e];
         if (rank != 0)
           for (int e = 0; e < 3; ++e)
-            st_async(sc.peer_smem[0] + peer_flag + 8u * (16 + 3 * rank + e), e3[e], sc.peer_bar_s[0]);
+            st_async(sc.peer_smem[0] + 8u * (o_fl + 16 + 3 * rank + e), e3[e], sc.peer_bar_s[0]);
       }
       if (C > 1) {
         if (lane == 0) {
           const double fl = sc.singular ? 1.0 : 0.0;
           for (int qr = 0; qr < C; ++qr)
-            if (qr != rank) st_async(sc.peer_smem[qr] + peer_flag + 8u * rank, fl, sc.peer_bar_s[qr]);
+            if (qr != rank) st_async(sc.peer_smem[qr] + 8u * (o_fl + rank), fl, sc.peer_bar_s[qr]);
         }
         mbar_wait(mb.s, mb.ph_s);  // every peer's exports and flag
         if (lane == 0) mbar_expect(mb.s, leaf_bytes);  // next exchange phase
@@ -1287,13 +1299,13 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
       }
       __syncwarp();
       bool singular = sc.singular != 0;
-      for (int qr = 0; qr < C; ++qr) singular |= (qr != rank) && g_smem[o.flag + qr] != 0.0;
-      if (!singular) run_prog(tprog, o.tslot, lane);
+      for (int qr = 0; qr < C; ++qr) singular |= (qr != rank) && g_smem[o_fl + qr] != 0.0;
+      if (!singular) run_prog(tprog, o_ts, lane);
       double s_sq = 0.0, s_m = 0.0, s_f = 0.0;  // the three pairwise sums
       if (root_top >= 0) {
-        s_sq = g_smem[o.tslot + 3 * root_top];
-        s_m = g_smem[o.tslot + 3 * root_top + 1];
-        s_f = g_smem[o.tslot + 3 * root_top + 2];
+        s_sq = g_smem[o_ts + 3 * root_top];
+        s_m = g_smem[o_ts + 3 * root_top + 1];
+        s_f = g_smem[o_ts + 3 * root_top + 2];
       }
       // lanes 0 and 1 run the same instructions (no divergence): lane 0
       // lam = s_sq / s_m and c = 2 sqrt(lam); lane 1 s_f / 1 = s_f and the
@@ -1315,7 +1327,7 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
             if (energy && rank == 0) {  // _accumulate_energy (microsolver.py:533-546), ranks in order
               double d[3] = {0.0, 0.0, 0.0};
               for (int qr = 0; qr < C; ++qr)
-                for (int e = 0; e < 3; ++e) d[e] = dadd(d[e], g_smem[o.flag + 16 + 3 * qr + e]);
+                for (int e = 0; e < 3; ++e) d[e] = dadd(d[e], g_smem[o_fl + 16 + 3 * qr + e]);
               w[1] = dadd(w[1], dmul(0.5, dmul(dt, dadd(d[0], d[1]))));
               if (wfix != 0.0 || (ramp && it < ramp_n)) {
                 w[1] = dadd(w[1], wfix);
@@ -1345,10 +1357,16 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
           }
         }
       }
+#ifndef FRB_NO_SHADOW
       if (T <= 32) accel(0, T);
+#endif
     }
     mb.ph_s ^= 1u;
     __syncthreads();
+#ifdef FRB_NO_SHADOW  // experiment: (-f)/m after the tree phase, by every warp
+    accel(0, T);
+    __syncthreads();
+#endif
     mark(sc, prof, PH_TT);
     if (sc.singular) {
       if (C > 1) drain(mb, R.halo_bytes, leaf_bytes);
@@ -1424,14 +1442,14 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
     if (t == 0) {
       double e = 0.0;
       for (int wp = 0; wp < (T + 31) / 32; ++wp) e = dadd(e, sc.red[wp * 9]);
-      double* dst = &g_smem[o.flag + 16 + 3 * rank];
+      double* dst = &g_smem[o.flag + 128 + rank];  // fin[rank]
       *(C > 1 ? peer(dst, 0) : dst) = e;
     }
   }
   csync(C);
   if (rank == 0 && energy && t == 0) {
     double e = 0.0;
-    for (int qr = 0; qr < C; ++qr) e = dadd(e, g_smem[o.flag + 16 + 3 * qr]);
+    for (int qr = 0; qr < C; ++qr) e = dadd(e, g_smem[o.flag + 128 + qr]);
     w[0] = dmul(0.5, e);
   }
   if (rank == 0) fixed_forces_and_stress(b, p, n, sc, it, alpha, ramp, full_bc_iter, energy, w);

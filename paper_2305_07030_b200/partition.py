@@ -204,10 +204,11 @@ def rank_smem_bytes(rt: RankTables, fprv_global: bool = False) -> int:
     positions [n_local + n_fix][3] (a DOF's own position slot doubles as its
     sq entry between the force and update phases), f and -- unless it lives
     in global memory -- f_prev (8 B per own DOF each), coefficients / sq2
-    max(own DOFs, n_act), local + top tree slots (3 doubles each), 64 cluster
-    flag words, one refined reciprocal mass per own node and the int32 tree
-    block (programs + exports)."""
-    return smem_bytes(rt.n_local + rt.n_fix, rt.n_own, rt.n_act, int(rt.tree[0]) + int(rt.tree[1]),
+    max(own DOFs, n_act), local tree slots and two parity buffers of top
+    tree slots (3 doubles each), two parity buffers of 64 cluster flag /
+    ledger words plus 16 final ledger words, one refined reciprocal mass per
+    own node and the int32 tree block (programs + exports)."""
+    return smem_bytes(rt.n_local + rt.n_fix, rt.n_own, rt.n_act, int(rt.tree[0]) + 2 * int(rt.tree[1]),
                       int(rt.tree[2]), fprv_global)
 
 
@@ -217,11 +218,11 @@ def partition_smem_bytes(part: "Partition", fprv_global: bool = False) -> int:
     offsets), each region sized by its maximum over the ranks."""
     rs = part.ranks
     return smem_bytes(max(r.n_local + r.n_fix for r in rs), max(r.n_own for r in rs),
-                      max(r.n_act for r in rs), int(rs[0].tree[0]) + int(rs[0].tree[1]), int(rs[0].tree[2]),
+                      max(r.n_act for r in rs), int(rs[0].tree[0]) + 2 * int(rs[0].tree[1]), int(rs[0].tree[2]),
                       fprv_global)
 
 
 def smem_bytes(n_pos: int, n_own: int, n_act: int, n_slots: int, n_prog: int, fprv_global: bool = False) -> int:
     nf = 3 * n_own
-    return 8 * (3 * n_pos + (1 if fprv_global else 2) * nf + max(nf, n_act) + n_own + 3 * n_slots + 64) + \
+    return 8 * (3 * n_pos + (1 if fprv_global else 2) * nf + max(nf, n_act) + n_own + 3 * n_slots + 144) + \
         4 * ((n_prog + 1) & ~1)

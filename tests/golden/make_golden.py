@@ -2,6 +2,7 @@
 /root/reference/pkg/src) in the build container.
 
     PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py --big   # big_index.json
 
 Each case is written to ``tests/golden/<name>.npz`` with the inputs (so the
 GPU box can rebuild the network without the reference) and the reference's
@@ -105,6 +106,69 @@ def cases():
         np.diag([1e-13, 1.0, 1.0]), C()
 
 
+def c5_gradient(i):
+    """Random macro deformation gradient of FE2 network i."""
+    rng = np.random.default_rng(10 ** 6 + i)
+    diag = rng.uniform(0.0, 0.1, 3)
+    off = rng.uniform(-0.05, 0.05, (3, 3))
+    np.fill_diagonal(off, 0.0)
+    return np.eye(3) + np.diag(diag) + off
+
+
+def big_cases():
+    """Full-length cases of the BASELINE configs that run on 8- and 16-CTA
+    clusters (and the c4 / c5 recipes).  Stored compactly: the lattice
+    parameters (the product's generate_lattice is bit-identical to the
+    reference's, tests/test_packing.py) and SHA-256 digests of the exact u / f
+    bytes plus a strided sample, so a multi-megabyte network costs a few KB."""
+    C = fr.SolverConfig
+    yield "c3_32cube_seed0", (32, 32, 32, 0.3, 0), UNIAX, C()                 # C3 (16-CTA cluster)
+    yield "c4_i77_32cube_shear", (32, 32, 32, 0.3, 77), SHEAR, C()           # c4 i=77: 32^3 shear
+    yield "c4_i71_26cube_shear", (26, 26, 26, 0.3, 71), SHEAR, C()           # c4 i=71: 26^3 shear
+    yield "c4_i13_20cube_biax", (20, 20, 20, 0.3, 13), BIAX, C()             # c4 i=13: 20^3 biax
+    yield "lat24_shear_seed3", (24, 24, 24, 0.3, 3), SHEAR, C()              # 8-CTA cluster
+    yield "c5_i0_15cube_randF", (15, 15, 15, 0.3, 0), c5_gradient(0), C()    # c5 network 0
+    yield "c5_i1_15cube_randF", (15, 15, 15, 0.3, 1), c5_gradient(1), C()    # c5 network 1
+
+
+def digest(a):
+    import hashlib
+    return hashlib.sha256(np.ascontiguousarray(a, dtype="<f8").tobytes()).hexdigest()
+
+
+SAMPLE_STRIDE = 97
+
+
+def main_big(only=None):
+    import time
+    path = os.path.join(HERE, "big_index.json")
+    for name, lat, F, cfg in big_cases():
+        if only and name not in only:
+            continue
+        net = fr.generate_lattice(*lat)
+        t0 = time.perf_counter()
+        out, err = run_reference(net, F, cfg)
+        assert err is None, err
+        res, f = out
+        rec = dict(lattice=list(lat), F=np.asarray(F, dtype=np.float64).tolist(), cfg=cfg_dict(cfg),
+                   converged=bool(res.converged), iters=int(res.iters),
+                   final_residual=float(res.final_residual).hex(), r_ref=float(res.r_ref).hex(),
+                   avg_stress=[float(x).hex() for x in res.avg_stress.reshape(-1)],
+                   u_sha256=digest(res.u), f_sha256=digest(f),
+                   u_sample=[float(x).hex() for x in res.u[::SAMPLE_STRIDE]],
+                   f_sample=[float(x).hex() for x in f[::SAMPLE_STRIDE]],
+                   n_nodes=net.n_nodes, n_elements=net.n_elements,
+                   reference_seconds=round(time.perf_counter() - t0, 1))
+        import fcntl
+        with open(path + ".lock", "w") as lk:  # several generators may run at once
+            fcntl.flock(lk, fcntl.LOCK_EX)
+            index = json.load(open(path)) if os.path.exists(path) else {}
+            index[name] = rec
+            with open(path, "w") as fh:
+                json.dump(dict(sorted(index.items())), fh, indent=0)
+        print(name, rec["iters"], rec["converged"], rec["reference_seconds"], "s", flush=True)
+
+
 def cfg_dict(cfg):
     return dict(tol_rel=cfg.tol_rel, tol_abs=cfg.tol_abs, max_iters=cfg.max_iters,
                 dt_safety=cfg.dt_safety,
@@ -158,4 +222,7 @@ def main(only=None):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1:] or None)
+    if sys.argv[1:2] == ["--big"]:
+        main_big(sys.argv[2:] or None)
+    else:
+        main(sys.argv[1:] or None)

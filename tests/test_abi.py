@@ -29,7 +29,7 @@ def test_struct_layouts():
     assert C.sizeof(nat.FrbBatch) == 8 + 26 * 8
     assert nat.PROBLEM_DTYPE.itemsize == 168
     assert nat.PART_DTYPE.itemsize == 104
-    assert nat.GROUP_DTYPE.itemsize == 32
+    assert nat.GROUP_DTYPE.itemsize == 40
     assert nat.RESULT_DTYPE.itemsize == 144
 
 

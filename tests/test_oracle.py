@@ -11,6 +11,7 @@ import pytest
 
 import golden_cases as gc
 from oracle import frb_oracle as orc
+import paper_2305_07030_b200 as frb
 
 FAST = [n for n in gc.names() if n not in ("random60", "c2_15cube_seed0")]
 
@@ -54,3 +55,19 @@ def test_oracle_internal_forces_matches_solver_state():
     case = gc.load("c1_7x7x8_uniax")
     f = orc.internal_forces(case.network, case.data["u"])
     assert np.array_equal(f, case.data["f"])
+
+
+@pytest.mark.parametrize("name", ["c5_i0_15cube_randF", "c5_i1_15cube_randF", "c4_i13_20cube_biax"])
+def test_oracle_matches_big_reference_records(name):
+    """The oracle reproduces the real reference on c4 / c5 recipe networks
+    (tests/golden/big_index.json, SHA-256 of the exact u bytes)."""
+    import hashlib
+    import json
+    import os
+    rec = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "big_index.json")))[name]
+    lat = rec["lattice"]
+    net = frb.generate_lattice(lat[0], lat[1], lat[2], float(lat[3]), int(lat[4]))
+    o = orc.solve(net, np.array(rec["F"]), frb.SolverConfig())
+    assert o.iters == rec["iters"]
+    assert hashlib.sha256(np.ascontiguousarray(o.u, dtype="<f8").tobytes()).hexdigest() == rec["u_sha256"]
+    assert o.residual == float.fromhex(rec["final_residual"])
