@@ -1,28 +1,38 @@
 #!/usr/bin/env python
 """Benchmark: batched dynamic relaxation of fiber networks on B200.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2]
-    python bench.py --impl reference ...      # CPU reference arm (oracle port)
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3]
+    python bench.py --impl reference ...   # the reference's CPU path on this host
 
 A *step* is one solve of the whole batch (every network relaxed to
-convergence) by one persistent-kernel launch.  Default workload is
-BASELINE.json configs[1] (c2): 256 networks generate_lattice(15,15,15,0.3,s)
-s = 0..255 (10,125 DOF, 9,450 fibers each) under uniaxial F=diag(1.1,1,1),
-default SolverConfig, FP64.  Under torchrun each rank solves its own 256
-networks (seeds offset by rank; weak scaling) and the per-network stresses
-are gathered to rank 0 with NCCL at the end of every step.
+convergence) by one persistent-kernel launch per launch group.  The default
+workload is BASELINE.json configs[2] (c3), the largest single-GPU
+configuration and the one the north-star target is quoted on: 1,024 networks
+generate_lattice(32,32,32,0.3,s), s = 0..1023 (98,304 DOF, 95,232 fibers
+each; the 16-CTA cluster path) under uniaxial F = diag(1.1,1,1), default
+SolverConfig, FP64.  Under torchrun the 1,024 networks are sharded by index
+over the GPUs (strided shards, paper_2305_07030_b200.distributed; strong
+scaling) and every step ends with the NCCL gather of all networks' result
+records.  --config c1/c2/c4/c5 select the other BASELINE configs (c2: 256
+networks per GPU, weak scaling; c5: the 16,384-network FE2 macro step in
+contiguous shards).
 
 Printed JSON (rank 0): value = networks/s for the whole job (device-resident
-batch, kernel + result gather), e2e = the same through the public API from
-pinned host buffers (upload, solve, download, unpermute), roofline of the
-kernel against the measured HBM copy bandwidth using the algorithmic bytes
-B_iter = 48 N + 48 nf + 24 M per network-iteration, and a
-CPU baseline: the oracle port timed on this host's cores.
+batch: kernel + result gather), e2e = the same through the public API
+(solve_batch: upload of the packed batch from pinned host memory, solve,
+download, unpermute) timed over the same number of steps, the roofline of
+the relaxation kernel against the measured HBM copy bandwidth using the
+algorithmic bytes B_iter = 48 N + 48 nf + 24 M per network-iteration
+(SURVEY.md 8d), a bench-side parity spot check of the timed batch against
+the real reference's golden records (tests/golden), and a CPU baseline: the
+reference's own solver (fibrelax.dynamic_relaxation_solve from baseline/_ref
+when installed, else the bit-exact oracle port) on this host's cores.
 """
 
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
 import math
 import os
@@ -44,26 +54,26 @@ UNIAX = np.diag([1.1, 1.0, 1.0])
 BIAX = np.diag([1.1, 1.1, 1.0])
 SHEAR = np.eye(3) + 0.2 * np.outer([1, 0, 0], [0, 1, 0])
 L2_FLUSH_BYTES = 256 << 20
-
-
 C5_TOTAL = 16384
+TOTAL = {"c1": 1, "c3": 1024, "c4": 1024, "c5": C5_TOTAL}
+SCALING = {"c1": "weak", "c2": "weak", "c3": "strong", "c4": "strong", "c5": "strong"}
+REF_PATH = os.path.join(ROOT, "baseline", "_ref")
 
 
 def shard_indices(name: str, rank: int, world: int) -> list[int]:
-    """Network indices a rank solves: c2 is weak-scaled (256 per
-    GPU), c3/c4 are strided (iteration counts vary by size/load), c5 is split
-    into contiguous shards of the FE2 macro-step's 16,384 networks."""
+    """Network indices a rank solves (through the product's
+    distributed.shard_indices): c2 is weak-scaled (256 per GPU), c3/c4 are
+    strided shards of 1,024 (iteration counts vary by size / load), c5 is
+    split into contiguous shards of the FE2 macro step's 16,384 networks."""
+    from paper_2305_07030_b200.distributed import shard_indices as shard
     if name == "c1":
         return [0]
     if name == "c2":
         return list(range(rank * 256, (rank + 1) * 256))
-    if name == "c3":
-        return list(range(rank, 1024, world))
-    if name == "c4":
-        return list(range(rank, 1024, world))
+    if name in ("c3", "c4"):
+        return [int(i) for i in shard(1024, rank, world, "strided")]
     if name == "c5":
-        per = -(-C5_TOTAL // world)
-        return list(range(rank * per, min(C5_TOTAL, (rank + 1) * per)))
+        return [int(i) for i in shard(C5_TOTAL, rank, world, "contiguous")]
     raise SystemExit(f"unknown --config {name}")
 
 
@@ -76,54 +86,32 @@ def c5_gradient(i: int) -> np.ndarray:
     return np.eye(3) + np.diag(diag) + off
 
 
-def config_networks(name: str, rank: int, world: int, limit: int | None = None):
-    """(workload description, networks, deformation gradients) for one rank."""
-    import paper_2305_07030_b200 as frb
-    idx = shard_indices(name, rank, world)
-    n_all = len(idx)  # limit=0: the description only (names the whole shard)
-    if limit is not None:
-        idx = idx[:limit]
-        n_all = n_all if limit == 0 else len(idx)
+def network_spec(name: str, i: int):
+    """(lattice args, F) of network i of a workload (same recipe on the GPU
+    and the CPU arm, and in tests/golden/make_golden.py)."""
     if name == "c1":
-        return ("c1: 1 x generate_lattice(7,7,8,0.3,seed=0), uniaxial F=diag(1.1,1,1)",
-                [frb.generate_lattice(7, 7, 8, 0.3, 0)], [UNIAX])
+        return (7, 7, 8, 0.3, 0), UNIAX
     if name == "c2":
-        return (f"c2: {n_all} x generate_lattice(15,15,15,0.3,seed=s) per GPU (10,125 DOF, 9,450 fibers), "
-                "uniaxial F=diag(1.1,1,1)",
-                [frb.generate_lattice(15, 15, 15, 0.3, s) for s in idx], [UNIAX] * len(idx))
+        return (15, 15, 15, 0.3, i), UNIAX
     if name == "c3":
-        return (f"c3: 1024 x generate_lattice(32,32,32,0.3,seed=s) (98,304 DOF, 95,232 fibers), uniaxial, "
-                f"strided shards ({n_all} on this GPU)",
-                [frb.generate_lattice(32, 32, 32, 0.3, s) for s in idx], [UNIAX] * len(idx))
+        return (32, 32, 32, 0.3, i), UNIAX
     if name == "c4":
-        nets, Fs = [], []
-        for i in idx:
-            n = 7 + (i % 26)
-            nets.append(frb.generate_lattice(n, n, n, 0.3, i))
-            Fs.append([UNIAX, BIAX, SHEAR][i % 3])
-        return ("c4: 1024 heterogeneous lattices n=7+(i mod 26) (1k-100k DOF), "
-                "loads uniax/biax/shear by i mod 3, strided shards", nets, Fs)
-    return (f"c5: FE2 macro-step, {C5_TOTAL} x 15^3 networks, random F, contiguous shards",
-            [frb.generate_lattice(15, 15, 15, 0.3, i) for i in idx], [c5_gradient(i) for i in idx])
+        n = 7 + (i % 26)
+        return (n, n, n, 0.3, i), [UNIAX, BIAX, SHEAR][i % 3]
+    return (15, 15, 15, 0.3, i), c5_gradient(i)
 
 
-def gather_stresses(sig, world: int, dist):
-    """Final homogenized-stress gather of the macro step: every rank's
-    [P, 9] float64 block to every rank (NCCL on the GPU box, gloo in tests)."""
-    import torch
-    P = sig.shape[0]
-    counts = torch.tensor([P], dtype=torch.int64, device=sig.device)
-    all_counts = [torch.zeros_like(counts) for _ in range(world)]
-    dist.all_gather(all_counts, counts)
-    Pmax = int(max(c.item() for c in all_counts))
-    pad = torch.zeros((Pmax, 9), dtype=sig.dtype, device=sig.device)
-    pad[:P] = sig
-    out = torch.empty((world, Pmax, 9), dtype=sig.dtype, device=sig.device)
-    if sig.is_cuda:
-        dist.all_gather_into_tensor(out.view(world * Pmax, 9), pad)
-    else:  # gloo has no all_gather_into_tensor
-        dist.all_gather(list(out.unbind(0)), pad)
-    return torch.cat([out[r, :int(all_counts[r].item())] for r in range(world)])
+def describe(name: str, n_here: int) -> str:
+    return {
+        "c1": "c1: 1 x generate_lattice(7,7,8,0.3,seed=0), uniaxial F=diag(1.1,1,1)",
+        "c2": f"c2: {n_here} x generate_lattice(15,15,15,0.3,seed=s) per GPU (10,125 DOF, 9,450 fibers), "
+              "uniaxial F=diag(1.1,1,1)",
+        "c3": f"c3: 1024 x generate_lattice(32,32,32,0.3,seed=s) (98,304 DOF, 95,232 fibers), uniaxial "
+              f"F=diag(1.1,1,1), strided shards ({n_here} on this GPU)",
+        "c4": f"c4: 1024 heterogeneous lattices n=7+(i mod 26) (1k-100k DOF), loads uniax/biax/shear by "
+              f"i mod 3, strided shards ({n_here} on this GPU)",
+        "c5": f"c5: FE2 macro-step, {C5_TOTAL} x 15^3 networks, random F, contiguous shards ({n_here} on this GPU)",
+    }[name]
 
 
 def b_iter(N: int, nf: int, M: int) -> int:
@@ -183,91 +171,191 @@ class ClockSampler:
 
 # --------------------------------------------------------------------- CPU arm
 
-def _oracle_solve(args):
+_REF = {}
+
+
+def reference_module():
+    """The reference's own package (fibrelax 0.1.0, pip-installed from
+    /root/reference/pkg into baseline/_ref) if it is present on this host,
+    else None (the CPU arm then times the bit-exact oracle port)."""
+    if "mod" not in _REF:
+        _REF["mod"] = None
+        if os.path.isdir(os.path.join(REF_PATH, "fibrelax")):
+            sys.path.insert(0, REF_PATH)
+            try:
+                import fibrelax  # noqa: F401
+                _REF["mod"] = sys.modules["fibrelax"]
+            except ImportError:
+                _REF["mod"] = None
+    return _REF["mod"]
+
+
+def _cpu_solve(args):
+    """One network of a workload through the reference's public solver (or
+    the oracle port); returns (seconds, iterations, nodes).  Network
+    generation is outside the timed call, setup inside."""
     cfgname, i = args
-    sys.path.insert(0, ROOT)
-    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    ref = reference_module()
+    if cfgname == "warm":
+        lat, F = (3, 3, 3, 0.3, 0), UNIAX
+    else:
+        lat, F = network_spec(cfgname, i)
+    if ref is not None:
+        net = ref.generate_lattice(*lat)
+        t0 = time.perf_counter()
+        r = ref.dynamic_relaxation_solve(net, ref.AffineBC(F), ref.SolverConfig())
+        return time.perf_counter() - t0, r.iters, net.n_nodes
     import paper_2305_07030_b200 as frb
     from oracle import frb_oracle as orc
-    if cfgname == "warm":
-        net, F = frb.generate_lattice(3, 3, 3, 0.3, 0), UNIAX
-    else:
-        _, nets, Fs = config_networks(cfgname, 0, 1, limit=None) if cfgname == "c1" else \
-            _one_network(cfgname, i)
-        net, F = nets[0], Fs[0]
+    net = frb.generate_lattice(*lat)
     t0 = time.perf_counter()
     r = orc.solve(net, F, frb.SolverConfig())
     return time.perf_counter() - t0, r.iters, net.n_nodes
 
 
-def _one_network(cfgname: str, i: int):
-    """Network i of a workload (the CPU sample takes the first ones)."""
-    import paper_2305_07030_b200 as frb
-    if cfgname == "c2":
-        return "", [frb.generate_lattice(15, 15, 15, 0.3, i)], [UNIAX]
-    if cfgname == "c3":
-        return "", [frb.generate_lattice(32, 32, 32, 0.3, i)], [UNIAX]
-    if cfgname == "c4":
-        n = 7 + (i % 26)
-        return "", [frb.generate_lattice(n, n, n, 0.3, i)], [[UNIAX, BIAX, SHEAR][i % 3]]
-    return "", [frb.generate_lattice(15, 15, 15, 0.3, i)], [c5_gradient(i)]
+def cpu_arm_name() -> tuple[str, str]:
+    if reference_module() is not None:
+        return "reference", "fibrelax.dynamic_relaxation_solve (the reference package, baseline/_ref)"
+    return "port", "oracle/frb_oracle.py (bit-exact numpy restatement of fibrelax; reference not installed)"
 
 
-def cpu_sample(config: str, cores: int, per_core: int = 1):
-    """Time the oracle port on `cores` worker processes over a bounded sample
-    of the workload: its first cores * per_core networks (networks/s over the
-    sample; generation excluded)."""
-    import multiprocessing as mp
-    jobs = [(config, i) for i in range(cores * per_core)]
-    ctx = mp.get_context("fork")
-    with ctx.Pool(cores) as pool:
-        pool.map(_oracle_solve, [("warm", 0)] * cores)  # warm the workers (imports)
+class CpuPool:
+    """A fork pool of one worker per host core (OPENBLAS_NUM_THREADS=1), warmed
+    by one tiny solve per worker (imports, allocator)."""
+
+    def __init__(self, cores: int):
+        import multiprocessing as mp
+        reference_module()  # imported before the fork: workers inherit it
+        self.cores = cores
+        self.pool = mp.get_context("fork").Pool(cores)
+        self.pool.map(_cpu_solve, [("warm", 0)] * cores)
+
+    def step(self, config: str, k: int) -> dict:
+        """Step k: the workload's networks k*cores .. (k+1)*cores - 1 (mod its
+        size), one per core."""
+        n_total = TOTAL.get(config, 256)
+        jobs = [(config, (k * self.cores + j) % n_total) for j in range(self.cores)]
         t0 = time.perf_counter()
-        out = pool.map(_oracle_solve, jobs)
+        out = self.pool.map(_cpu_solve, jobs, chunksize=1)
         wall = time.perf_counter() - t0
-    node_upd = sum(it * n for _, it, n in out)
-    return dict(networks=len(jobs), wall_s=wall, nets_per_s=len(jobs) / wall,
-                node_updates_per_s=node_upd / wall, cpu_s=sum(t for t, _, _ in out))
+        return dict(networks=len(jobs), wall_s=wall, cpu_s=sum(t for t, _, _ in out),
+                    node_updates=sum(it * n for _, it, n in out), first=jobs[0][1], last=jobs[-1][1])
+
+    def close(self):
+        self.pool.terminate()
+
+
+def summarize_cpu(config: str, samples: list, cores: int) -> dict:
+    nets = sum(s["networks"] for s in samples)
+    wall = sum(s["wall_s"] for s in samples)
+    kind, arm = cpu_arm_name()
+    per_net = sum(s["cpu_s"] for s in samples) / nets
+    return {
+        "value": nets / wall, "unit": "networks/s", "cores": cores, "kind": kind,
+        "sample": (f"{nets} networks of the {config} workload ({len(samples)} step(s) of {cores}, one network "
+                   f"per core per step, networks {samples[0]['first']}..{samples[-1]['last']}); {wall:.1f} s wall, "
+                   f"{per_net:.2f} s per network per core; {arm}; OPENBLAS_NUM_THREADS=1 fork pool"),
+        "single_core": {"value": 1.0 / per_net, "unit": "networks/s",
+                        "note": "mean per-network solve time of the same sample on one core"},
+        "node_updates_per_s": sum(s["node_updates"] for s in samples) / wall,
+    }
 
 
 def run_reference_arm(args, rank: int):
     if rank != 0:
         return
-    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
     cores = os.cpu_count() or 1
-    for _ in range(args.warmup):
-        cpu_sample(args.config, cores)
-    samples = [cpu_sample(args.config, cores) for _ in range(args.steps)]
-    value = sum(s["networks"] for s in samples) / sum(s["wall_s"] for s in samples)
-    ms = 1e3 * statistics.mean(s["wall_s"] for s in samples)
-    sample = (f"{samples[0]['networks']} networks of the {args.config} workload per step "
-              f"(one per core, fork pool, OPENBLAS_NUM_THREADS=1)")
+    pool = CpuPool(cores)
+    try:
+        for _ in range(args.warmup):  # light warm-ups: one tiny solve per worker
+            pool.pool.map(_cpu_solve, [("warm", 0)] * cores)
+        samples = [pool.step(args.config, k) for k in range(args.steps)]
+    finally:
+        pool.close()
+    cb = summarize_cpu(args.config, samples, cores)
+    n_here = len(shard_indices(args.config, 0, 1))
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": "networks/s",
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "impl": "reference", "metric": METRIC, "value": cb["value"], "unit": "networks/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * statistics.mean(s["wall_s"] for s in samples),
+        "higher_is_better": True, "scaling": SCALING[args.config], "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (reference generate_lattice inputs)",
-        "config": {"workload": config_networks(args.config, 0, 1, limit=0)[0],
-                   "arm": "oracle/frb_oracle.py (numpy restatement of fibrelax, bit-exact)"},
-        "node_updates_per_s": statistics.mean(s["node_updates_per_s"] for s in samples),
-        "cpu_baseline": {"value": value, "unit": "networks/s", "cores": cores, "kind": "port",
-                         "sample": sample},
-        "e2e": {"value": value, "unit": "networks/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "config": {"workload": describe(args.config, n_here), "arm": cpu_arm_name()[1],
+                   "per_step": f"{cores} networks (one per host core)"},
+        "node_updates_per_s": cb["node_updates_per_s"],
+        "cpu_baseline": cb,
+        "e2e": {"value": cb["value"], "unit": "networks/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
+# --------------------------------------------------------------------- parity spot check
+
+def spot_check(config: str, indices: list, results) -> dict:
+    """Networks of the timed batch that have a golden record of the real
+    reference (tests/golden): iterations, residual and u must match exactly.
+    results: the public-API SolveResults of this rank's shard."""
+    gdir = os.path.join(ROOT, "tests", "golden")
+    checks = []
+    big = {}
+    if os.path.exists(os.path.join(gdir, "big_index.json")):
+        with open(os.path.join(gdir, "big_index.json")) as fh:
+            big = json.load(fh)
+    pos = {g: k for k, g in enumerate(indices)}
+    for name, rec in big.items():
+        lat = tuple(rec["lattice"])
+        for g, k in pos.items():
+            spec, F = network_spec(config, g)
+            if tuple(spec) == (lat[0], lat[1], lat[2], lat[3], lat[4]) and np.array_equal(F, np.array(rec["F"])):
+                r = results[k]
+                ok = (r.iters == rec["iters"] and r.final_residual == float.fromhex(rec["final_residual"])
+                      and hashlib.sha256(np.ascontiguousarray(r.u, "<f8").tobytes()).hexdigest() == rec["u_sha256"])
+                checks.append({"network": g, "golden": name, "iters": r.iters, "bit_equal": bool(ok)})
+    if config in ("c1", "c2") and 0 in pos:
+        name = "c1_7x7x8_uniax" if config == "c1" else "c2_15cube_seed0"
+        z = np.load(os.path.join(gdir, f"{name}.npz"))
+        r = results[pos[0]]
+        ok = r.iters == int(z["iters"]) and np.array_equal(r.u, z["u"]) and r.final_residual == float(z["final_residual"])
+        checks.append({"network": 0, "golden": name, "iters": r.iters, "bit_equal": bool(ok)})
+    return {"checked": len(checks), "all_bit_equal": all(c["bit_equal"] for c in checks), "cases": checks}
+
+
 # --------------------------------------------------------------------- GPU arm
+
+def layout_of(name: str, world: int, limit: int | None):
+    """(n_total, shard mode) of a workload at `world` ranks."""
+    n_total, mode = {"c1": (world, "contiguous"), "c2": (256 * world, "contiguous"), "c3": (1024, "strided"),
+                     "c4": (1024, "strided"), "c5": (C5_TOTAL, "contiguous")}[name]
+    if limit is not None:
+        n_total = min(n_total, limit * world)
+    return n_total, mode
+
+
+def traffic_per_launch(config: str, n_networks: int):
+    """DRAM bytes (read + write) of the relaxation kernel from the committed
+    ncu --set full capture of this config (profiles/traffic.json), scaled to
+    this launch's network count; None when no capture exists."""
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    if not os.path.exists(path):
+        return None, None
+    with open(path) as fh:
+        t = json.load(fh).get(config)
+    if not isinstance(t, dict):
+        return None, None
+    return t["bytes"] * n_networks / t["networks"], t["source"]
+
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
-    ap.add_argument("--limit", type=int, default=None, help="networks per rank (c3/c4/c5 samples)")
+    ap.add_argument("--config", default="c3", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--limit", type=int, default=None, help="networks per rank (ncu captures)")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true", help="skip the end-to-end leg (profiling runs)")
     ap.add_argument("--team-size", type=int, default=None, help="CTA size override (TeamBatched)")
     args = ap.parse_args()
     if args.warmup < 3:
@@ -285,24 +373,30 @@ def main():
 
     import paper_2305_07030_b200 as frb
     from paper_2305_07030_b200 import batch as fb
+    from paper_2305_07030_b200.distributed import ShardedBatch, decode_records
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
 
-    workload, nets, Fs = config_networks(args.config, rank, world, args.limit)
-    cfg = frb.SolverConfig()
+    def make(i):
+        lat, F = network_spec(args.config, i)
+        return frb.generate_lattice(*lat), frb.AffineBC(F)
+
+    n_total, mode = layout_of(args.config, world, args.limit)
     t0 = time.perf_counter()
-    batch = frb.pack_batch(nets, [frb.AffineBC(F) for F in Fs])
-    setup_s = time.perf_counter() - t0
+    sb = ShardedBatch(make, n_total, mode, device=dev, rank=rank, world=world)
+    build_s = time.perf_counter() - t0   # generation + host setup + upload
+    batch = sb.batch
     batch.pin()
-    dbatch = batch.to_device(dev)
+    cfg = frb.SolverConfig()
     strategy = frb.TeamBatched(team_size=args.team_size)
-    launch = dbatch.prepare(cfg, strategy)
+    launch = sb.prepare(cfg, strategy)
     flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
     P = batch.n_problems
     stream = torch.cuda.current_stream(dev)
+    gathered = [None]
 
     def step(ev=None):
         flush.zero_()
@@ -311,9 +405,8 @@ def main():
         launch.run(stream)
         if ev is not None:
             ev[1].record(stream)
-        if world > 1:  # final homogenized-stress gather (C1 result gather)
-            sig = launch.out.results.view(torch.float64).view(P, -1)[:, 5:14]
-            gather_stresses(sig, world, dist)
+        if world > 1:  # every network's result record to every rank (NCCL, no host sync)
+            gathered[0] = sb.gather(launch.out.results)
 
     for _ in range(args.warmup):
         step()
@@ -332,12 +425,6 @@ def main():
         torch.cuda.synchronize(dev)
     elapsed = t_start.elapsed_time(t_end) / 1e3
     kern = [a.elapsed_time(b) / 1e3 for a, b in kev]
-    if world > 1:
-        t = torch.tensor([elapsed, statistics.mean(kern)], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        elapsed, kern_mean = t.tolist()
-    else:
-        kern_mean = statistics.mean(kern)
 
     rec = launch.out.host_results()
     iters = rec["iters"].astype(np.int64)
@@ -346,75 +433,107 @@ def main():
     Ms = np.array([p.network.n_elements for p in batch.problems], dtype=np.int64)
     alg_bytes = float((iters * (48 * Ns + 48 * nfs + 24 * Ms)).sum())
     node_updates = float((iters * Ns).sum())
-    assert (rec["status"] == 0).all(), "not every network converged"
-
-    # ---- e2e through the public API (pinned host buffers -> results) ----
-    def e2e_step():
-        return fb.results_to_solve_results(batch, batch.to_device(dev).solve(cfg, strategy))
-    for _ in range(1):
-        e2e_step()
-    torch.cuda.synchronize(dev)
+    converged_local = int((rec["status"] == 0).sum())
     if world > 1:
-        dist.barrier()
-    e_steps = max(1, min(args.steps, 3))
-    te = time.perf_counter()
-    for _ in range(e_steps):
-        res = e2e_step()
-    torch.cuda.synchronize(dev)
-    e2e_s = (time.perf_counter() - te) / e_steps
-    if world > 1:
-        t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+        t = torch.tensor([elapsed, statistics.mean(kern)], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = t.item()
-    h2d = sum(a.nbytes for a in batch.arrays.values()) + batch.desc.nbytes
-    d2h = 3 * int(batch.node_base[-1]) * 8 + P * 144
-    assert all(r.converged for r in res)
+        elapsed, kern_mean = t.tolist()
+        s = torch.tensor([alg_bytes, node_updates, float(converged_local)], dtype=torch.float64, device=dev)
+        dist.all_reduce(s, op=dist.ReduceOp.SUM)
+        alg_all, node_updates_all, converged_all = s.tolist()
+        all_rec = decode_records(gathered[0])
+        assert len(all_rec) == n_total and (all_rec["status"] == 0).all(), "not every network converged"
+    else:
+        kern_mean = statistics.mean(kern)
+        alg_all, node_updates_all, converged_all = alg_bytes, node_updates, converged_local
+    assert converged_all == n_total, "not every network converged"
+
+    # ---- e2e through the public API: pinned host batch -> results ----
+    e2e = None
+    spot = None
+    if not args.no_e2e:
+        def e2e_step():
+            dres = batch.to_device(dev).solve(cfg, strategy)
+            out = fb.results_to_solve_results(batch, dres)
+            if world > 1:
+                sb.gather(dres.results)
+            return out
+        e2e_step()
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        te = time.perf_counter()
+        for _ in range(args.steps):
+            res = e2e_step()
+        torch.cuda.synchronize(dev)
+        e2e_s = (time.perf_counter() - te) / args.steps
+        if world > 1:
+            t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_s = t.item()
+        h2d = sum(a.nbytes for a in batch.arrays.values())
+        d2h = 3 * int(batch.node_base[-1]) * 8 + P * nat_result_bytes()
+        assert all(r.converged for r in res)
+        e2e = {"value": n_total / e2e_s, "unit": "networks/s", "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h),
+               "note": "solve_batch path per step: upload of the packed batch from pinned memory, solve, "
+                       "download of u and the result records, unpermute to the original node order; "
+                       "host setup (pack_batch) excluded, reported as setup_s_per_rank"}
+        if rank == 0:
+            spot = spot_check(args.config, sb.indices.tolist(), res)
+            assert spot["all_bit_equal"], f"parity spot check failed: {spot}"
 
     ms_per_step = 1e3 * elapsed / args.steps
-    value = world * P / (elapsed / args.steps)
+    value = n_total / (elapsed / args.steps)
     peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     peak, peak_src = 6650.0, "fallback (B200_PROFILING.md)"
     if os.path.exists(peaks_path):
         with open(peaks_path) as fh:
             peak, peak_src = float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
-    achieved = alg_bytes / kern_mean / 1e9
-    traffic = None
-    prof = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(prof):
-        with open(prof) as fh:
-            traffic = json.load(fh).get(args.config)
+    achieved = alg_all / world / kern_mean / 1e9
+    traffic, traffic_src = traffic_per_launch(args.config, P)
 
     line = {
         "metric": METRIC, "value": value, "unit": "networks/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": SCALING[args.config], "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (generate_lattice jittered lattices, same generator as the reference)",
-        "config": {"workload": workload, "networks_per_gpu": P, "parallelism": f"shard{world}",
+        "config": {"workload": describe(args.config, P), "networks_total": n_total, "networks_per_gpu": P,
+                   "parallelism": f"shard{world} ({mode})",
                    "l2": "flushed (256 MiB memset before every step)",
-                   "setup_s_per_rank": round(setup_s, 3), "cta_threads": launch.threads},
-        "node_updates_per_s": world * node_updates / (elapsed / args.steps),
+                   "setup_s_per_rank": round(batch.setup_s, 3),
+                   "build_s_per_rank": round(build_s, 3),
+                   "cta_threads": launch.threads,
+                   "clusters": sorted({int(c) for c in batch.desc["cluster"]})},
+        "node_updates_per_s": node_updates_all / (elapsed / args.steps),
         "iters_mean": float(iters.mean()),
-        "e2e": {"value": world * P / e2e_s, "unit": "networks/s", "h2d_bytes_per_step": int(h2d),
-                "d2h_bytes_per_step": int(d2h)},
+        "e2e": e2e,
         "gpu_launches": args.steps * int((launch.groups["count"] > 0).sum()),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                     "kernel": "frb_relax_kernel", "kernel_ms": 1e3 * kern_mean,
-                     "alg_bytes_per_launch": alg_bytes},
+                     "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
+                     "peak_source": peak_src, "kernel": "frb_relax_kernel", "kernel_ms": 1e3 * kern_mean,
+                     "alg_bytes_per_launch": alg_all / world,
+                     "alg_bytes_model": "sum over networks of iters * (48 N + 48 nf + 24 M) (SURVEY.md 8d)"},
+        "parity_spot_check": spot,
         "clocks": clocks.summary(),
         "kernel_ms_per_step": [round(1e3 * k, 3) for k in kern],
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cores = os.cpu_count() or 1
-        s = cpu_sample(args.config, cores)
-        line["cpu_baseline"] = {
-            "value": s["nets_per_s"], "unit": "networks/s", "cores": cores, "kind": "port",
-            "sample": f"{s['networks']} networks of the {args.config} workload, one per core "
-                      f"({s['wall_s']:.1f} s wall, {s['cpu_s']:.1f} s CPU)"}
+        pool = CpuPool(cores)
+        try:
+            line["cpu_baseline"] = summarize_cpu(args.config, [pool.step(args.config, 0)], cores)
+        finally:
+            pool.close()
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def nat_result_bytes() -> int:
+    from paper_2305_07030_b200 import _native as nat
+    return nat.RESULT_DTYPE.itemsize
 
 
 if __name__ == "__main__":

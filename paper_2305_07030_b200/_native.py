@@ -27,7 +27,7 @@ PHASE_NAMES = ("F1 coefs", "F2 gather", "A per-DOF", "C chains", "T local+exp", 
 
 EXPORTS = ("frb_abi_version", "frb_last_error", "frb_device_info", "frb_rank_smem_bytes",
            "frb_max_dofs_per_thread", "frb_solve_batch", "frb_internal_forces",
-           "frb_selftest_arith")
+           "frb_selftest_arith", "frb_setup_problem", "frb_setup_batch")
 
 
 class FrbConfig(C.Structure):
@@ -50,7 +50,7 @@ class FrbBatch(C.Structure):
 # frb_problem / frb_part / frb_group / frb_result as numpy record types
 PROBLEM_DTYPE = np.dtype([
     ("node_base", "<i8"), ("elem_base", "<i8"), ("inc_base", "<i8"), ("plan_base", "<i8"),
-    ("part_base", "<i8"), ("actv_base", "<i8"),
+    ("part_base", "<i8"), ("actv_base", "<i8"), ("tnode_base", "<i8"), ("telem_base", "<i8"),
     ("n_nodes", "<i4"), ("n_free_nodes", "<i4"), ("n_elems", "<i4"), ("cluster", "<i4"),
     ("flags", "<i4"), ("pad", "<i4"),
     ("dt", "<f8"), ("volume", "<f8"), ("ea", "<f8"), ("F", "<f8", (9,)),
@@ -68,13 +68,19 @@ GROUP_DTYPE = np.dtype([
     ("max_rank_leaves", "<i4"), ("flags", "<i4"),
 ])
 GF_SERIAL = 1
+SETUP_ITEM_DTYPE = np.dtype([
+    ("coords", "<u8"), ("elements", "<u8"), ("materials", "<u8"), ("node_order", "<u8"), ("act_elem", "<u8"),
+    ("X_out", "<u8"), ("mass_out", "<u8"), ("L_out", "<u8"), ("EA_out", "<u8"), ("act_L_out", "<u8"),
+    ("act_EA_out", "<u8"), ("mass_scratch", "<u8"), ("n_act", "<i8"), ("n_nodes", "<i4"), ("n_elems", "<i4"),
+    ("n_materials", "<i4"), ("rc", "<i4"), ("scalars", "<f8", (3,)),
+])
 RESULT_DTYPE = np.dtype([
     ("status", "<i4"), ("iters", "<i4"), ("bad_element", "<i4"), ("converged", "<i4"),
     ("final_residual", "<f8"), ("r_ref", "<f8"), ("energy_residual", "<f8"),
     ("avg_stress", "<f8", (9,)), ("energy", "<f8", (4,)),
 ])
-assert PROBLEM_DTYPE.itemsize == 168 and PART_DTYPE.itemsize == 104
-assert GROUP_DTYPE.itemsize == 40 and RESULT_DTYPE.itemsize == 144
+assert PROBLEM_DTYPE.itemsize == 184 and PART_DTYPE.itemsize == 104
+assert SETUP_ITEM_DTYPE.itemsize == 144 and GROUP_DTYPE.itemsize == 40 and RESULT_DTYPE.itemsize == 144
 
 
 class NativeError(RuntimeError):
@@ -104,6 +110,9 @@ def lib() -> C.CDLL:
     h.frb_solve_batch.argtypes = [C.POINTER(FrbBatch), C.POINTER(FrbConfig), C.c_void_p]
     h.frb_internal_forces.argtypes = [C.POINTER(FrbBatch), C.c_void_p, C.c_void_p, C.c_void_p]
     h.frb_selftest_arith.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]
+    h.frb_setup_problem.argtypes = [C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32,
+                                    C.c_void_p, C.c_void_p, C.c_int64] + [C.c_void_p] * 8
+    h.frb_setup_batch.argtypes = [C.c_void_p, C.c_int32, C.c_int32]
     if h.frb_abi_version() != ABI_VERSION:
         raise ImportError("libfrb200.so ABI version mismatch (rebuild)")
     _lib = h

@@ -29,6 +29,8 @@ import ctypes as C
 import hashlib
 import math
 import os
+import threading
+from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass, field
 from typing import Sequence
 
@@ -125,6 +127,7 @@ class Topology:
     slots_a: int
     slots_b: int
     parts: dict = field(default_factory=dict)   # cluster size -> Partition
+    _chosen: tuple | None = None
 
     def partition(self, C: int) -> Partition:
         if C not in self.parts:
@@ -132,6 +135,12 @@ class Topology:
                                       self.elem_ab[:, 1].astype(np.int64), self.ell_other, self.ell_elem,
                                       self.slots_a, self.slots_b, self.plan, C)
         return self.parts[C]
+
+    def chosen(self) -> tuple[Partition, bool]:
+        """choose_cluster(), computed once per topology."""
+        if self._chosen is None:
+            self._chosen = self.choose_cluster()
+        return self._chosen
 
     def choose_cluster(self) -> tuple[Partition, bool]:
         """Smallest cluster with at most DOFS_PER_RANK free DOFs per rank whose
@@ -199,59 +208,152 @@ def _topology(network: FiberNetwork, node_rank: np.ndarray, n_free_nodes: int) -
                     slots_a=sa, slots_b=sb)
 
 
-_TOPO_CACHE: dict[bytes, Topology] = {}
+@dataclass
+class _TopoEntry:
+    """One cached topology: the connectivity it was built from (to verify a
+    sampled-key hit), the DOF map's node order and the device tables."""
+    elements: np.ndarray
+    boundary: frozenset
+    order: np.ndarray
+    topo: Topology
+    key: bytes
+    elements_bytes: bytes = b""
+
+
+_TOPO_CACHE: dict[bytes, list] = {}
+_TOPO_LOCK = threading.Lock()
+_TOPO_SERIAL = [0]
+
+
+def _topo_entry(network: FiberNetwork) -> _TopoEntry:
+    """The topology of a network, built once per distinct (connectivity,
+    boundary set).  Lookup hashes a strided sample of the element rows and
+    confirms a hit with a full comparison, so packing thousands of networks
+    of one lattice costs one memcmp each instead of hashing megabytes."""
+    n, el = network.n_nodes, network.elements
+    m = len(el)
+    h = hashlib.blake2b(digest_size=16)
+    h.update(np.int64([n, m, len(network.boundary_nodes), hash(network.boundary_nodes)]).tobytes())
+    h.update(el[::max(1, m // 256)].tobytes())
+    k = h.digest()
+    with _TOPO_LOCK:  # one build per topology even when networks are packed on several threads
+        for ent in _TOPO_CACHE.get(k, ()):
+            # confirm the sampled-key hit: byte comparison of the whole
+            # element table (C-contiguous int64, FiberNetwork guarantees it)
+            if ent.boundary == network.boundary_nodes and (
+                    ent.elements is el or ent.elements_bytes == el.tobytes()):
+                return ent
+        dm = build_dofmap(n, network.boundary_nodes)
+        order = dm.node_order
+        rank = np.empty(n, dtype=np.int64)
+        rank[order] = np.arange(n)
+        topo = _topology(network, rank, dm.n_free // 3)
+        if sum(len(v) for v in _TOPO_CACHE.values()) > 4096:
+            _TOPO_CACHE.clear()
+        _TOPO_SERIAL[0] += 1
+        ent = _TopoEntry(elements=el, boundary=network.boundary_nodes, order=order, topo=topo,
+                         key=k + _TOPO_SERIAL[0].to_bytes(8, "little"), elements_bytes=el.tobytes())
+        _TOPO_CACHE.setdefault(k, []).append(ent)
+        return ent
 
 
 @dataclass
 class HostProblem:
-    """Solver-order setup of one network (ProblemSetup, microsolver.py:138-163)."""
+    """Solver-order setup of one network (ProblemSetup, microsolver.py:138-163).
+    X / node_mass / L / ea are views into the packed batch arrays once packed."""
     network: FiberNetwork
     F: np.ndarray
     node_order: np.ndarray       # solver position -> original node
-    X: np.ndarray                # (N, 3)
-    node_mass: np.ndarray        # (N,)
-    dt_base: float               # min_e L sqrt(rho/E); dt = dt_safety * dt_base
     topo_key: bytes
     topo: Topology
+    check_mass: bool = True
+    X: np.ndarray = None         # (N, 3) solver order
+    node_mass: np.ndarray = None # (N,) solver order
+    dt_base: float = math.nan    # min_e L sqrt(rho/E); dt = dt_safety * dt_base
+    L: np.ndarray = None         # reference lengths, original element order
+    ea: np.ndarray = None        # E*A per element
+    volume: float = math.nan     # FiberNetwork.volume
 
     @property
     def n_nodes(self) -> int:
-        return len(self.X)
+        return self.network.n_nodes
 
     @property
     def n_free_nodes(self) -> int:
         return self.topo.n_free_nodes
 
 
+_MAT_CACHE: dict = {}
+
+
+def _material_table(network: FiberNetwork) -> np.ndarray:
+    """(n_materials, 3) float64 rows (E, A, rho), cached per material tuple."""
+    key = tuple(network.materials)
+    tab = _MAT_CACHE.get(key)
+    if tab is None:
+        tab = np.ascontiguousarray(np.array([[m.elastic_modulus, m.cross_section_area, m.density]
+                                             for m in network.materials], dtype=np.float64).reshape(-1, 3))
+        if len(_MAT_CACHE) > 1024:
+            _MAT_CACHE.clear()
+        _MAT_CACHE[key] = tab
+    return tab
+
+
+def _native_setup(p: HostProblem, X, mass, L, EA, act_elem=None, act_L=None, act_EA=None) -> int:
+    """Fill one problem's packed values with frb_setup_problem (GIL released
+    while it runs).  Returns the zero-mass node or -1; sets dt_base / volume."""
+    net = p.network
+    n, m = net.n_nodes, net.n_elements
+    mats = _material_table(net)
+    scal = np.empty(3)
+    scratch = np.empty(max(n, 1))
+    ptr = lambda a: None if a is None else a.ctypes.data  # noqa: E731
+    n_act = 0 if act_elem is None else len(act_elem)
+    nat.check(nat.lib().frb_setup_problem(
+        n, m, ptr(net.node_coords), ptr(net.elements), ptr(mats), len(mats), ptr(p.node_order),
+        ptr(act_elem), n_act, ptr(X), ptr(mass), ptr(L), ptr(EA), ptr(act_L), ptr(act_EA),
+        ptr(scal), ptr(scratch)))
+    p.dt_base = float(scal[0])
+    p.volume = float(net.rve_volume) if net.rve_volume is not None else float(scal[1])
+    p.X, p.node_mass, p.L, p.ea = X.reshape(n, 3), mass, L, EA
+    return int(scal[2])
+
+
+def _mass_error(node: int):
+    """compute_lumped_mass's error (microsolver.py:179-181); node in original order."""
+    from .microsolver import NetworkMassError
+    return NetworkMassError(f"node {node} has zero mass (no incident elements)")
+
+
+def _meta(network: FiberNetwork, bc: AffineBC, check_mass: bool = True) -> HostProblem:
+    ent = _topo_entry(network)
+    return HostProblem(network=network, F=np.asarray(bc.deformation_gradient, dtype=np.float64),
+                       node_order=ent.order, topo_key=ent.key, topo=ent.topo, check_mass=check_mass)
+
+
 def build_problem(network: FiberNetwork, bc: AffineBC, check_mass: bool = True) -> HostProblem:
-    """Host setup for one network (reference build_problem, :302-335).
+    """Host setup for one network (reference build_problem, :302-335): the
+    DOF map and device topology (cached per topology) plus the native
+    per-network values (frb_setup_problem: lengths, lumped mass in np.add.at
+    order, dt base, volume -- bit-identical to the reference's numpy).
 
     Raises NetworkMassError for a node without incident elements (like
     compute_lumped_mass, :179-181)."""
-    n = network.n_nodes
-    dm = build_dofmap(n, network.boundary_nodes)
-    order = dm.node_order
-    rank = np.empty(n, dtype=np.int64)
-    rank[order] = np.arange(n)
-    nfn = dm.n_free // 3
-    node_mass = _lumped_node_mass(network)[order] if check_mass else np.ones(n)
-    emod, _, rho = network.material_columns()
-    L = network.reference_lengths()
-    dt_base = float(np.min(L * np.sqrt(rho / emod))) if L.size else math.nan
-    h = hashlib.blake2b(digest_size=16)
-    h.update(np.int64([n, network.n_elements]).tobytes())
-    h.update(network.elements[:, :2].tobytes())
-    h.update(np.asarray(sorted(network.boundary_nodes), dtype=np.int64).tobytes())
-    key = h.digest()
-    topo = _TOPO_CACHE.get(key)
-    if topo is None:
-        topo = _topology(network, rank, nfn)
-        if len(_TOPO_CACHE) > 4096:
-            _TOPO_CACHE.clear()
-        _TOPO_CACHE[key] = topo
-    return HostProblem(network=network, F=np.asarray(bc.deformation_gradient, dtype=np.float64),
-                       node_order=order, X=np.ascontiguousarray(network.node_coords[order]),
-                       node_mass=node_mass, dt_base=dt_base, topo_key=key, topo=topo)
+    p = _meta(network, bc, check_mass)
+    n, m = network.n_nodes, network.n_elements
+    bad = _native_setup(p, np.empty(3 * n), np.empty(n), np.empty(m), np.empty(m))
+    if check_mass and bad >= 0:
+        raise _mass_error(bad)
+    if not check_mass:
+        p.node_mass = np.ones(n)
+    return p
+
+
+def setup_threads() -> int:
+    """Host threads for the per-network setup (FRB_SETUP_THREADS, default all
+    cores): frb_setup_problem runs with the GIL released."""
+    env = os.environ.get("FRB_SETUP_THREADS")
+    return max(1, int(env)) if env else (os.cpu_count() or 1)
 
 
 # ------------------------------------------------------------------ batch
@@ -260,7 +362,7 @@ def build_problem(network: FiberNetwork, bc: AffineBC, check_mass: bool = True) 
 class Batch:
     """Host-side packed batch (space "a").  ``packed_state`` exposes the
     spec's per-problem PackedStorage rows for u, v, a, f_int, m (built on
-    first access)."""
+    first access).  ``setup_s`` is the host setup time of pack_batch."""
     networks: list
     bcs: list
     problems: list                     # HostProblem per network
@@ -273,6 +375,7 @@ class Batch:
     _orig_rows: np.ndarray | None = field(default=None, repr=False)  # solver -> original node rows
     _u_pinned: object = field(default=None, repr=False)               # reused pinned download buffer
     pinned: dict | None = field(default=None, repr=False)
+    setup_s: float = math.nan
 
     @property
     def n_problems(self) -> int:
@@ -300,11 +403,17 @@ class Batch:
 
 
 def pack_batch(networks: Sequence[FiberNetwork], bcs: Sequence[AffineBC]) -> Batch:
-    """Build the packed batch."""
+    """Build the packed batch: topologies once (cached),
+    then every network's values written straight into the packed arrays by
+    the native setup on a pool of host threads."""
+    import time
     if len(networks) != len(bcs):
         raise ValueError(f"networks and bcs differ in length ({len(networks)} vs {len(bcs)})")
-    probs = [build_problem(net, bc) for net, bc in zip(networks, bcs)]
-    return _pack(list(networks), list(bcs), probs)
+    t0 = time.perf_counter()
+    metas = [_meta(net, bc) for net, bc in zip(networks, bcs)]
+    batch = _pack(list(networks), list(bcs), metas)
+    batch.setup_s = time.perf_counter() - t0
+    return batch
 
 
 def _cat(parts, dtype, width=None):
@@ -332,28 +441,39 @@ def _group_threads(max_own_dofs: int, max_rank_leaves: int, n_problems: int, clu
 
 
 def _pack(networks, bcs, probs, cluster: int | None = None) -> Batch:
+    """Pack problems whose topology is known (HostProblem from _meta).
+
+    Tables that depend only on the topology (incidence CSR, element
+    endpoints, per-rank slot tables, trees) are stored once per topology;
+    per-network values (coordinates, masses, lengths, E*A, active-element
+    values) are written into the packed arrays by frb_setup_problem on a pool
+    of host threads."""
     P = len(probs)
     desc = np.zeros(P, dtype=nat.PROBLEM_DTYPE)
     node_base = np.zeros(P + 1, dtype=np.int64)
+    elem_base = np.zeros(P + 1, dtype=np.int64)
+    actv_base = np.zeros(P + 1, dtype=np.int64)
     plan_slot: dict[int, int] = {}
     shared_slot: dict[tuple, list] = {}       # (topo, C) -> per-rank base offsets
-    topo_slot: dict[bytes, int] = {}
-    inc, plans, ell, act_ab, halo_g, send, fix_g, trees = [], [], [], [], [], [], [], []
-    n_inc = n_plan = n_ell = n_act = n_halo = n_send = n_fix = n_tree = 0
-    X, mass, EL, EA, inc_node, elem_ab, act_L, act_EA = [], [], [], [], [], [], [], []
+    topo_slot: dict[bytes, tuple] = {}        # topo -> (inc base, topo node base, topo elem base)
+    inc, plans, ell, act_ab, halo_g, send, fix_g, trees, inc_node, elem_ab = ([] for _ in range(10))
+    n_inc = n_plan = n_ell = n_act = n_halo = n_send = n_fix = n_tree = n_tnode = n_telem = 0
     parts_rows = []
-    elem_base = actv_base = 0
-    any_nonuniform = False
-    part_of, fglob_of = [], []
+    part_of, fglob_of, act_of, cols = [], [], [], []
+    n_parts = 0
     for i, p in enumerate(probs):
         t = p.topo
-        part, fglob = (t.partition(cluster), False) if cluster else t.choose_cluster()
+        part, fglob = (t.partition(cluster), False) if cluster else t.chosen()
         part_of.append(part)
         fglob_of.append(fglob)
         if p.topo_key not in topo_slot:
-            topo_slot[p.topo_key] = n_inc
+            topo_slot[p.topo_key] = (n_inc, n_tnode, n_telem)
             inc.append(t.inc)
+            inc_node.append(t.inc_node)
+            elem_ab.append(t.elem_ab)
             n_inc += len(t.inc)
+            n_tnode += len(t.inc_node)
+            n_telem += len(t.elem_ab)
         key = (p.topo_key, part.C)
         if key not in shared_slot:
             bases = []
@@ -371,57 +491,92 @@ def _pack(networks, bcs, probs, cluster: int | None = None) -> Batch:
                 n_halo += len(rt.halo_g)
                 n_send += len(rt.send)
                 n_fix += rt.n_fix
-            shared_slot[key] = bases
+            rows = np.zeros(len(part.ranks), dtype=nat.PART_DTYPE)  # identical for every network of (topo, C)
+            off = 0
+            for row, rt, (b_ell, b_act, b_halo, b_send, b_fix, b_tree) in zip(rows, part.ranks, bases):
+                row["ell_base"], row["act_base"], row["actv_off"] = b_ell, b_act, off
+                row["halo_base"], row["send_base"], row["fix_base"] = b_halo, b_send, b_fix
+                row["n_fix"] = rt.n_fix
+                row["tree_base"], row["tree_len"] = b_tree, len(rt.tree)
+                row["node0"], row["n_own"], row["n_local"], row["n_act"] = rt.node0, rt.n_own, rt.n_local, rt.n_act
+                row["ell_stride"], row["slots_a"], row["slots_b"] = rt.stride, part.slots_a, part.slots_b
+                row["leaf0"], row["n_leaves"] = rt.leaf0, rt.n_leaves
+                off += rt.n_act
+            shared_slot[key] = (rows, np.concatenate([rt.act_elem for rt in part.ranks]).astype(np.int64), off)
+        rows, act_elem, n_actv = shared_slot[key]
+        act_of.append(act_elem)
         nf = 3 * t.n_free_nodes
         if nf not in plan_slot:
             plan_slot[nf] = n_plan
             plans.append(t.plan)
             n_plan += len(t.plan)
-        emod, area, _ = p.network.material_columns()
-        ea = emod * area
-        L = p.network.reference_lengths()
-        uniform = bool(ea.size == 0 or np.all(ea == ea[0]))
-        any_nonuniform |= not uniform
-        d = desc[i]
-        d["node_base"] = node_base[i]
-        d["elem_base"] = elem_base
-        d["inc_base"] = topo_slot[p.topo_key]
-        d["plan_base"] = plan_slot[nf]
-        d["part_base"] = len(parts_rows)
-        d["actv_base"] = actv_base
-        d["n_nodes"] = p.n_nodes
-        d["n_free_nodes"] = t.n_free_nodes
-        d["n_elems"] = p.network.n_elements
-        d["cluster"] = part.C
-        d["flags"] = nat.PF_EA_UNIFORM if uniform else 0
-        d["volume"] = p.network.volume
-        d["ea"] = ea[0] if ea.size else 0.0
-        d["F"] = p.F.reshape(9)
-        off = 0
-        for rt, (b_ell, b_act, b_halo, b_send, b_fix, b_tree) in zip(part.ranks, shared_slot[key]):
-            row = np.zeros((), dtype=nat.PART_DTYPE)
-            row["ell_base"], row["act_base"], row["actv_off"] = b_ell, b_act, off
-            row["halo_base"], row["send_base"], row["fix_base"] = b_halo, b_send, b_fix
-            row["n_fix"] = rt.n_fix
-            row["tree_base"], row["tree_len"] = b_tree, len(rt.tree)
-            row["node0"], row["n_own"], row["n_local"], row["n_act"] = rt.node0, rt.n_own, rt.n_local, rt.n_act
-            row["ell_stride"], row["slots_a"], row["slots_b"] = rt.stride, part.slots_a, part.slots_b
-            row["leaf0"], row["n_leaves"] = rt.leaf0, rt.n_leaves
-            parts_rows.append(row)
-            act_L.append(L[rt.act_elem])
-            act_EA.append(ea[rt.act_elem])
-            off += rt.n_act
-        actv_base += off
+        cols.append(topo_slot[p.topo_key] + (plan_slot[nf], n_parts, t.n_free_nodes, part.C))
+        parts_rows.append(rows)
+        n_parts += len(rows)
+        actv_base[i + 1] = actv_base[i] + n_actv
         node_base[i + 1] = node_base[i] + p.n_nodes
-        X.append(p.X.reshape(-1))
-        mass.append(p.node_mass)
-        EL.append(L)
-        EA.append(ea)
-        inc_node.append(t.inc_node)
-        elem_ab.append(t.elem_ab)
-        elem_base += p.network.n_elements
+        elem_base[i + 1] = elem_base[i] + p.network.n_elements
+    if P:
+        cv = np.array(cols, dtype=np.int64).reshape(P, 7)
+        desc["node_base"], desc["elem_base"], desc["actv_base"] = node_base[:-1], elem_base[:-1], actv_base[:-1]
+        desc["inc_base"], desc["tnode_base"], desc["telem_base"] = cv[:, 0], cv[:, 1], cv[:, 2]
+        desc["plan_base"], desc["part_base"], desc["n_free_nodes"], desc["cluster"] = cv[:, 3], cv[:, 4], cv[:, 5], \
+            cv[:, 6]
+        desc["n_nodes"], desc["n_elems"] = np.diff(node_base), np.diff(elem_base)
+        desc["F"] = np.array([p.F.reshape(9) for p in probs])
 
-    parts = np.array(parts_rows, dtype=nat.PART_DTYPE) if parts_rows else np.zeros(0, nat.PART_DTYPE)
+    # per-network values, native, straight into the packed arrays
+    X = np.empty(3 * int(node_base[-1]))
+    mass = np.empty(int(node_base[-1]))
+    EL = np.empty(int(elem_base[-1]))
+    EA = np.empty(int(elem_base[-1]))
+    act_L = np.empty(int(actv_base[-1]))
+    act_EA = np.empty(int(actv_base[-1]))
+
+    items = np.zeros(P, dtype=nat.SETUP_ITEM_DTYPE)
+    mats = [_material_table(p.network) for p in probs]
+    it = items
+    it["coords"] = [p.network.node_coords.ctypes.data for p in probs]
+    it["elements"] = [p.network.elements.ctypes.data for p in probs]
+    it["materials"] = [m.ctypes.data for m in mats]
+    it["node_order"] = [p.node_order.ctypes.data for p in probs]
+    it["act_elem"] = [a.ctypes.data for a in act_of]
+    it["n_act"] = [len(a) for a in act_of]
+    it["n_nodes"] = np.diff(node_base)
+    it["n_elems"] = np.diff(elem_base)
+    it["n_materials"] = [len(m) for m in mats]
+    # output pointers: offsets into the packed arrays (vectorised)
+    it["X_out"] = X.ctypes.data + 24 * node_base[:-1]
+    it["mass_out"] = mass.ctypes.data + 8 * node_base[:-1]
+    it["L_out"] = EL.ctypes.data + 8 * elem_base[:-1]
+    it["EA_out"] = EA.ctypes.data + 8 * elem_base[:-1]
+    it["act_L_out"] = act_L.ctypes.data + 8 * actv_base[:-1]
+    it["act_EA_out"] = act_EA.ctypes.data + 8 * actv_base[:-1]
+    nthr = min(setup_threads(), max(P, 1))
+    scratch = np.empty(int(node_base[-1]) + 1)  # per-network original-order masses
+    it["mass_scratch"] = scratch.ctypes.data + 8 * node_base[:-1]
+    nat.check(nat.lib().frb_setup_batch(items.ctypes.data, P, nthr))
+    for i, p in enumerate(probs):
+        dt_base, vol, bad = items["scalars"][i]
+        nb, eb, ab = int(node_base[i]), int(elem_base[i]), int(actv_base[i])
+        p.dt_base = float(dt_base)
+        p.volume = float(p.network.rve_volume) if p.network.rve_volume is not None else float(vol)
+        p.X = X[3 * nb:3 * (nb + p.n_nodes)].reshape(-1, 3)
+        p.node_mass = mass[nb:nb + p.n_nodes]
+        p.L = EL[eb:eb + p.network.n_elements]
+        p.ea = EA[eb:eb + p.network.n_elements]
+        if not p.check_mass:
+            p.node_mass[:] = 1.0
+        elif bad >= 0:
+            raise _mass_error(int(bad))
+    uniform = [bool(p.ea.size == 0 or (p.ea == p.ea[0]).all()) for p in probs]
+    any_nonuniform = not all(uniform)
+    if P:
+        desc["flags"] = np.where(uniform, nat.PF_EA_UNIFORM, 0)
+        desc["volume"] = [p.volume for p in probs]
+        desc["ea"] = [p.ea[0] if p.ea.size else 0.0 for p in probs]
+
+    parts = np.concatenate(parts_rows) if parts_rows else np.zeros(0, nat.PART_DTYPE)
     # launch groups by cluster size, longest problems first inside a group
     order, groups = [], []
     for C, fglob in sorted({(pt.C, fg) for pt, fg in zip(part_of, fglob_of)}):
@@ -439,18 +594,18 @@ def _pack(networks, bcs, probs, cluster: int | None = None) -> Batch:
         groups.append(g)
         order.extend(ids)
     arrays = dict(
-        X=_cat(X, np.float64), node_mass=_cat(mass, np.float64),
+        X=X, node_mass=mass,
         inc_node=_cat(inc_node, np.int32, 2), inc=_cat(inc, np.int32, 2),
-        elem_ab=_cat(elem_ab, np.int32, 2), elem_L=_cat(EL, np.float64),
-        elem_EA=_cat(EA, np.float64), plans=_cat(plans, np.int32),
+        elem_ab=_cat(elem_ab, np.int32, 2), elem_L=EL,
+        elem_EA=EA, plans=_cat(plans, np.int32),
         ell=_cat(ell, np.uint32).view(np.int32), fix_g=_cat(fix_g, np.int32),
-        act_ab=_cat(act_ab, np.uint32).view(np.int32), act_L=_cat(act_L, np.float64),
+        act_ab=_cat(act_ab, np.uint32).view(np.int32), act_L=act_L,
         halo_g=_cat(halo_g, np.int32), send=_cat(send, np.int32, MAX_SEND), trees=_cat(trees, np.int32),
         order=np.asarray(order, dtype=np.int32),
         problems=desc.view(np.uint8).copy(), parts=parts.view(np.uint8).copy(),
     )
     if any_nonuniform:
-        arrays["act_EA"] = _cat(act_EA, np.float64)
+        arrays["act_EA"] = act_EA
     return Batch(networks=networks, bcs=bcs, problems=probs, desc=desc, parts=parts,
                  groups=np.array(groups, dtype=nat.GROUP_DTYPE), arrays=arrays, node_base=node_base)
 
@@ -673,7 +828,7 @@ def solve_batch(batch: Batch, strategy=None, config: SolverConfig | None = None)
 def internal_forces_device(network: FiberNetwork, u: np.ndarray) -> np.ndarray:
     """f(u) for one network on the GPU, original DOF order."""
     torch = _torch()
-    p = build_problem(network, AffineBC(np.eye(3)), check_mass=False)
+    p = _meta(network, AffineBC(np.eye(3)), check_mass=False)
     batch = _pack([network], [None], [p], cluster=1)
     dbatch = batch.to_device()
     n = p.n_nodes

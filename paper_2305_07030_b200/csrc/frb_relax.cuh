@@ -221,9 +221,9 @@ __device__ void load_views(Net& n, Rank& R, const frb_batch& b, int p, int r) {
   n.node_base = P.node_base;
   n.X = b.X + 3 * P.node_base;
   n.mass = b.node_mass + P.node_base;
-  n.incn = reinterpret_cast<const int2*>(b.inc_node) + P.node_base;
+  n.incn = reinterpret_cast<const int2*>(b.inc_node) + P.tnode_base;
   n.inc = reinterpret_cast<const int2*>(b.inc) + P.inc_base;
-  n.eab = reinterpret_cast<const int2*>(b.elem_ab) + P.elem_base;
+  n.eab = reinterpret_cast<const int2*>(b.elem_ab) + P.telem_base;
   n.EL = b.elem_L + P.elem_base;
   n.EA = b.elem_EA + P.elem_base;
   n.plan = b.plans + P.plan_base;

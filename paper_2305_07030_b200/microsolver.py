@@ -150,11 +150,12 @@ class SolveResult:
 
 # --------------------------------------------------------------- host helpers
 
-def _lumped_node_mass(network: FiberNetwork) -> NDArray[np.float64]:
+def _lumped_node_mass(network: FiberNetwork, columns=None, lengths=None) -> NDArray[np.float64]:
     """rho*A*L/2 to each end; role a in element order, then role b
-    (reference ``microsolver.py:170-182``; np.add.at is sequential)."""
-    _, area, rho = network.material_columns()
-    half = rho * area * network.reference_lengths() / 2.0
+    (reference ``microsolver.py:170-182``; np.add.at is sequential).
+    columns / lengths: precomputed material_columns() / reference_lengths()."""
+    _, area, rho = columns if columns is not None else network.material_columns()
+    half = rho * area * (lengths if lengths is not None else network.reference_lengths()) / 2.0
     node_mass = np.zeros(network.n_nodes)
     np.add.at(node_mass, network.elements[:, 0], half)
     np.add.at(node_mass, network.elements[:, 1], half)

@@ -1,9 +1,12 @@
-"""Multi-GPU host logic on CPU: two gloo ranks shard the FE2 macro-step by
-index and gather the homogenized stresses (bench.py).
+"""Multi-GPU host logic on CPU: index shards and the result
+gather of ``paper_2305_07030_b200.distributed`` with two gloo ranks.
 
-The solves themselves need the GPU; here each rank evaluates the stress of
-its shard with the CPU oracle on tiny networks, which is enough to prove the
-shard bookkeeping (disjoint, complete, order-preserving) and the gather."""
+The solves need the GPU; here every rank injects synthetic per-network
+result records (the bytes the kernel writes, frb_result) for its shard and
+calls the product's ``gather_results`` -- the same function ``ShardedBatch``
+and ``bench.py`` use with NCCL -- which must return every network's record
+in global index order on every rank, for contiguous (FE2 macro step) and
+strided (heterogeneous batches) shards of uneven size."""
 
 import os
 import socket
@@ -16,6 +19,10 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from paper_2305_07030_b200 import _native as nat  # noqa: E402
+from paper_2305_07030_b200.distributed import ShardLayout, decode_records, shard_indices  # noqa: E402
 
 
 def _free_port():
@@ -24,55 +31,69 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, out_path):
+def synthetic_records(indices: np.ndarray) -> np.ndarray:
+    """A distinguishable frb_result per global network index."""
+    rec = np.zeros(len(indices), dtype=nat.RESULT_DTYPE)
+    rec["status"] = indices % 3
+    rec["iters"] = 1000 + indices
+    rec["converged"] = (indices % 3 == 0).astype(np.int32)
+    rec["final_residual"] = 1e-9 * indices
+    rec["r_ref"] = 0.5 + indices
+    rec["avg_stress"] = indices[:, None] * 10.0 + np.arange(9)[None, :]
+    return rec
+
+
+def _worker(rank, world, port, n_total, mode, out_path):
     sys.path.insert(0, ROOT)
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    import bench
-    import paper_2305_07030_b200 as frb
-    from oracle import frb_oracle as orc
-    idx = bench.shard_indices("c5", rank, world)[:3] if rank == 0 else bench.shard_indices("c5", rank, world)[:2]
-    sig = []
-    for i in idx:  # a tiny stand-in network per index, the c5 gradient of that index
-        net = frb.generate_lattice(3, 3, 3, 0.3, i)
-        sig.append(orc.solve(net, bench.c5_gradient(i), frb.SolverConfig()).sigma.reshape(9))
-    g = bench.gather_stresses(torch.tensor(np.array(sig)), world, dist)
-    ids = [torch.zeros(1, dtype=torch.int64) for _ in range(world)]
-    dist.all_gather(ids, torch.tensor([idx[0]]))
-    if rank == 0:
-        np.savez(out_path, sig=g.numpy(), first=np.array([int(t.item()) for t in ids]))
+    from paper_2305_07030_b200.distributed import gather_results
+    layout = ShardLayout(n_total, world, mode)
+    mine = layout.shard(rank)
+    local = torch.from_numpy(synthetic_records(mine).view(np.uint8).copy())
+    out = gather_results(local, layout)
+    np.save(f"{out_path}.{rank}.npy", out.numpy())
     dist.barrier()
     dist.destroy_process_group()
 
 
-def test_c5_shards_are_contiguous_disjoint_and_complete():
-    sys.path.insert(0, ROOT)
-    import bench
-    for world in (1, 2, 3, 8):
-        shards = [bench.shard_indices("c5", r, world) for r in range(world)]
-        flat = [i for s in shards for i in s]
-        assert flat == list(range(bench.C5_TOTAL))
-        assert all(s == list(range(s[0], s[-1] + 1)) for s in shards if s)
-    for world in (2, 4):   # strided shards of the heterogeneous / 100k-DOF batches
-        for cfg in ("c3", "c4"):
-            flat = sorted(i for r in range(world) for i in bench.shard_indices(cfg, r, world))
-            assert flat == list(range(1024))
+def test_shards_are_disjoint_complete_and_ordered():
+    for n in (0, 1, 7, 1024, 16384):
+        for world in (1, 2, 3, 8):
+            c = [shard_indices(n, r, world, "contiguous") for r in range(world)]
+            assert np.array_equal(np.concatenate(c), np.arange(n))
+            assert all((np.diff(s) == 1).all() for s in c if len(s))
+            s = [shard_indices(n, r, world, "strided") for r in range(world)]
+            assert np.array_equal(np.sort(np.concatenate(s)), np.arange(n))
+            assert max(len(x) for x in s) - min(len(x) for x in s) <= 1
+    with pytest.raises(ValueError):
+        shard_indices(10, 2, 2)
 
 
-def test_two_rank_stress_gather(tmp_path):
+def test_layout_rows_invert_the_shards():
+    lay = ShardLayout(11, 3, "strided")
+    rows = lay.global_rows()
+    m = lay.max_shard
+    for r in range(3):
+        for k, i in enumerate(lay.shard(r)):
+            assert rows[i] == r * m + k
+
+
+@pytest.mark.parametrize("mode,n_total", [("contiguous", 13), ("strided", 13), ("contiguous", 16384)])
+def test_two_rank_result_gather(tmp_path, mode, n_total):
     world = 2
-    out = str(tmp_path / "g.npz")
-    mp.start_processes(_worker, args=(world, _free_port(), out), nprocs=world, start_method="spawn")
-    z = np.load(out)
-    sys.path.insert(0, ROOT)
+    out = str(tmp_path / "g")
+    mp.start_processes(_worker, args=(world, _free_port(), n_total, mode, out), nprocs=world, start_method="spawn")
+    expect = synthetic_records(np.arange(n_total))
+    for r in range(world):
+        got = decode_records(np.load(f"{out}.{r}.npy"))
+        assert got.shape == (n_total,)
+        assert np.array_equal(got.view(np.uint8), expect.view(np.uint8)), f"rank {r}"
+
+
+def test_bench_uses_the_product_shards():
     import bench
-    import paper_2305_07030_b200 as frb
-    from oracle import frb_oracle as orc
-    expect = []
-    for r, k in ((0, 3), (1, 2)):
-        for i in bench.shard_indices("c5", r, world)[:k]:
-            net = frb.generate_lattice(3, 3, 3, 0.3, i)
-            expect.append(orc.solve(net, bench.c5_gradient(i), frb.SolverConfig()).sigma.reshape(9))
-    assert z["sig"].shape == (5, 9)
-    assert np.array_equal(z["sig"], np.array(expect))          # rank order, uneven shards
-    assert list(z["first"]) == [0, bench.C5_TOTAL // 2]
+    for world in (1, 2, 8):
+        for r in range(world):
+            assert list(bench.shard_indices("c5", r, world)) == list(shard_indices(16384, r, world, "contiguous"))
+            assert list(bench.shard_indices("c3", r, world)) == list(shard_indices(1024, r, world, "strided"))

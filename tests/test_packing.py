@@ -203,3 +203,43 @@ def test_isolated_node_is_mass_error():
                            [frb.Material(1, 1, 1)], frozenset({0}))
     with pytest.raises(frb.NetworkMassError):
         frb.pack_batch([net], [frb.AffineBC(np.eye(3))])
+
+
+@pytest.mark.parametrize("name", ["random60", "random90_fixed", "lat6_general_F", "c1_7x7x8_uniax"])
+def test_native_setup_bit_equal_to_numpy(name):
+    """frb_setup_problem (native host setup, GIL-free) reproduces the numpy
+    restatement of build_problem bit for bit: lengths, E*A, lumped masses in
+    np.add.at order, dt base and volume (reference microsolver.py:170-193,
+    302-335; network.py:154-172)."""
+    import golden_cases as gc
+    from paper_2305_07030_b200.microsolver import _lumped_node_mass
+    net = gc.load(name).network
+    p = fb.build_problem(net, frb.AffineBC(np.eye(3)))
+    emod, area, rho = net.material_columns()
+    L = net.reference_lengths()
+    assert np.array_equal(p.L, L)
+    assert np.array_equal(p.ea, emod * area)
+    assert np.array_equal(p.node_mass, _lumped_node_mass(net)[p.node_order])
+    assert np.array_equal(p.X, net.node_coords[p.node_order])
+    assert p.dt_base == float(np.min(L * np.sqrt(rho / emod)))
+    assert p.volume == net.volume
+
+
+def test_packed_values_are_per_network_and_topology_tables_shared():
+    """Networks of one lattice share the topology tables (inc_node / elem_ab
+    stored once); coordinates, lengths and masses are per network."""
+    nets = [frb.generate_lattice(5, 5, 5, 0.3, s) for s in range(3)]
+    b = frb.pack_batch(nets, [frb.AffineBC(np.eye(3))] * 3)
+    assert len(b.arrays["elem_ab"]) == nets[0].n_elements
+    assert len(b.arrays["inc_node"]) == nets[0].n_nodes
+    assert (b.desc["telem_base"] == 0).all() and (b.desc["tnode_base"] == 0).all()
+    for i, net in enumerate(nets):
+        eb = int(b.desc[i]["elem_base"])
+        assert np.array_equal(b.arrays["elem_L"][eb:eb + net.n_elements], net.reference_lengths())
+
+
+def test_zero_mass_node_raises_like_reference():
+    X = np.array([[0.0, 0, 0], [1.0, 0, 0], [0.0, 1, 0], [5.0, 5, 5]])
+    net = frb.FiberNetwork(X, np.array([[0, 1, 0], [1, 2, 0]]), [frb.Material(1, 1, 1)], frozenset({0}))
+    with pytest.raises(frb.NetworkMassError, match="node 3 has zero mass"):
+        frb.pack_batch([net], [frb.AffineBC(np.eye(3))])
