@@ -15,7 +15,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("FRB_LIB") or os.path.join(HERE, "lib", "libfrb200.so")
 
-ABI_VERSION = 7
+ABI_VERSION = 8
 MAX_CLUSTER = 16
 FRB_OK, FRB_E_INVALID, FRB_E_TOO_LARGE, FRB_E_CUDA, FRB_E_UNSUPPORTED = 0, -1, -2, -3, -4
 STATUS_CONVERGED, STATUS_MAX_ITERS, STATUS_SINGULAR = 0, 1, 2
@@ -38,7 +38,7 @@ class FrbConfig(C.Structure):
 
 BATCH_POINTERS = ("groups", "problems", "parts", "order", "X", "node_mass", "inc_node", "inc",
                   "elem_ab", "elem_L", "elem_EA", "plans", "ell", "act_ab", "act_L",
-                  "act_EA", "halo_g", "send", "fix_g", "trees", "u", "f", "work", "results", "queue",
+                  "act_EA", "halo_g", "runs", "fix_g", "trees", "u", "f", "work", "results", "queue",
                   "phase_cycles")
 
 
@@ -57,10 +57,11 @@ PROBLEM_DTYPE = np.dtype([
 ])
 PART_DTYPE = np.dtype([
     ("ell_base", "<i8"), ("act_base", "<i8"), ("actv_off", "<i8"), ("halo_base", "<i8"),
-    ("send_base", "<i8"), ("fix_base", "<i8"), ("tree_base", "<i8"),
+    ("runs_base", "<i8"), ("fix_base", "<i8"), ("tree_base", "<i8"),
     ("node0", "<i4"), ("n_own", "<i4"), ("n_local", "<i4"), ("n_act", "<i4"),
     ("ell_stride", "<i4"), ("slots_a", "<i4"), ("slots_b", "<i4"), ("leaf0", "<i4"),
-    ("n_leaves", "<i4"), ("n_fix", "<i4"), ("tree_len", "<i4"), ("pad", "<i4"),
+    ("n_leaves", "<i4"), ("n_fix", "<i4"), ("tree_len", "<i4"), ("n_runs", "<i4"),
+    ("halo_bytes", "<i4"), ("ack_from", "<u4"), ("n_int", "<i4"), ("pad", "<i4"),
 ])
 GROUP_DTYPE = np.dtype([
     ("cluster", "<i4"), ("first", "<i4"), ("count", "<i4"), ("block_threads", "<i4"),
@@ -79,7 +80,7 @@ RESULT_DTYPE = np.dtype([
     ("final_residual", "<f8"), ("r_ref", "<f8"), ("energy_residual", "<f8"),
     ("avg_stress", "<f8", (9,)), ("energy", "<f8", (4,)),
 ])
-assert PROBLEM_DTYPE.itemsize == 184 and PART_DTYPE.itemsize == 104
+assert PROBLEM_DTYPE.itemsize == 184 and PART_DTYPE.itemsize == 120
 assert SETUP_ITEM_DTYPE.itemsize == 144 and GROUP_DTYPE.itemsize == 40 and RESULT_DTYPE.itemsize == 144
 
 
@@ -106,7 +107,7 @@ def lib() -> C.CDLL:
     h.frb_device_info.argtypes = [C.c_int] + [C.POINTER(C.c_int)] * 4
     h.frb_rank_smem_bytes.restype = C.c_int64
     h.frb_rank_smem_bytes.argtypes = [C.c_int32] * 6
-    h.frb_max_dofs_per_thread.argtypes = [C.c_int]
+    h.frb_max_dofs_per_thread.argtypes = [C.c_int, C.c_int]
     h.frb_solve_batch.argtypes = [C.POINTER(FrbBatch), C.POINTER(FrbConfig), C.c_void_p]
     h.frb_internal_forces.argtypes = [C.POINTER(FrbBatch), C.c_void_p, C.c_void_p, C.c_void_p]
     h.frb_selftest_arith.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]

@@ -44,7 +44,7 @@ from .microsolver import (
 )
 from .network import AffineBC, FiberNetwork
 from .packed import PackedStorage
-from .partition import MAX_SEND, Partition, partition, partition_smem_bytes
+from .partition import RUN_WORDS, Partition, partition, partition_smem_bytes
 from .plan import reduction_plan
 
 __all__ = ["Batch", "DeviceBatch", "ExecutionStrategy", "NaiveLoop", "SerialReference",
@@ -62,9 +62,10 @@ SMEM_BUDGET = 227 * 1024 - 4 * 1024
 DOFS_PER_RANK = int(os.environ.get("FRB_DOFS_PER_RANK", "8000"))
 
 
-def dofs_per_thread_cap(threads: int) -> int:
-    """Register-resident DOFs per thread the kernel instantiates (frb200.h)."""
-    return 8 if threads > 768 else 12 if threads > 512 else 16
+def dofs_per_thread_cap(threads: int, fprv_global: bool = False) -> int:
+    """Register-resident DOFs per thread the kernel instantiates (frb200.h;
+    24 exists only for the global-f_prev kernels of 256-thread CTAs)."""
+    return 8 if threads > 768 else 12 if threads > 512 else 16 if (threads > 256 or not fprv_global) else 24
 
 
 # ------------------------------------------------------------------ strategies
@@ -432,10 +433,10 @@ def _group_threads(max_own_dofs: int, max_rank_leaves: int, n_problems: int, clu
     need = max(64, 8 * max_rank_leaves, math.ceil(max_own_dofs / 16))
     if n_problems * cluster < 148:
         need = max(need, min(512, 32 * math.ceil(max_own_dofs / 32)))
-    if fprv_global:  # global-f_prev kernels exist for 512..1024 threads; c2 (one 15^3
-        need = max(need, 768)  # network per CTA): 768 -> 82.3 ms, 512 -> 83.3 ms
+    if fprv_global:  # 32^3 on 16 ranks: FRB_FG_THREADS overrides (experiments)
+        need = max(need, int(os.environ.get("FRB_FG_THREADS", "768")))
     threads = min(MAX_CTA_THREADS, 32 * math.ceil(need / 32))
-    while max_own_dofs > dofs_per_thread_cap(threads) * threads and threads < MAX_CTA_THREADS:
+    while max_own_dofs > dofs_per_thread_cap(threads, fprv_global) * threads and threads < MAX_CTA_THREADS:
         threads += 32
     return threads
 
@@ -456,8 +457,8 @@ def _pack(networks, bcs, probs, cluster: int | None = None) -> Batch:
     plan_slot: dict[int, int] = {}
     shared_slot: dict[tuple, list] = {}       # (topo, C) -> per-rank base offsets
     topo_slot: dict[bytes, tuple] = {}        # topo -> (inc base, topo node base, topo elem base)
-    inc, plans, ell, act_ab, halo_g, send, fix_g, trees, inc_node, elem_ab = ([] for _ in range(10))
-    n_inc = n_plan = n_ell = n_act = n_halo = n_send = n_fix = n_tree = n_tnode = n_telem = 0
+    inc, plans, ell, act_ab, halo_g, runs, fix_g, trees, inc_node, elem_ab = ([] for _ in range(10))
+    n_inc = n_plan = n_ell = n_act = n_halo = n_runs = n_fix = n_tree = n_tnode = n_telem = 0
     parts_rows = []
     part_of, fglob_of, act_of, cols = [], [], [], []
     n_parts = 0
@@ -478,24 +479,26 @@ def _pack(networks, bcs, probs, cluster: int | None = None) -> Batch:
         if key not in shared_slot:
             bases = []
             for rt in part.ranks:
-                bases.append((n_ell, n_act, n_halo, n_send, n_fix, n_tree))
+                bases.append((n_ell, n_act, n_halo, n_runs, n_fix, n_tree))
                 trees.append(rt.tree)
                 n_tree += len(rt.tree)
                 ell.append(rt.ell.reshape(-1))
                 act_ab.append(rt.act_ab[:, 0].astype(np.uint32) | (rt.act_ab[:, 1].astype(np.uint32) << 16))
                 halo_g.append(rt.halo_g)
-                send.append(rt.send)
+                runs.append(rt.runs)
                 fix_g.append(rt.fix_g)
                 n_ell += rt.ell_o.size
                 n_act += len(rt.act_ab)
                 n_halo += len(rt.halo_g)
-                n_send += len(rt.send)
+                n_runs += len(rt.runs)
                 n_fix += rt.n_fix
             rows = np.zeros(len(part.ranks), dtype=nat.PART_DTYPE)  # identical for every network of (topo, C)
             off = 0
-            for row, rt, (b_ell, b_act, b_halo, b_send, b_fix, b_tree) in zip(rows, part.ranks, bases):
+            for row, rt, (b_ell, b_act, b_halo, b_runs, b_fix, b_tree) in zip(rows, part.ranks, bases):
                 row["ell_base"], row["act_base"], row["actv_off"] = b_ell, b_act, off
-                row["halo_base"], row["send_base"], row["fix_base"] = b_halo, b_send, b_fix
+                row["halo_base"], row["runs_base"], row["fix_base"] = b_halo, b_runs, b_fix
+                row["n_runs"], row["halo_bytes"], row["ack_from"] = len(rt.runs), rt.halo_bytes, rt.ack_from
+                row["n_int"] = rt.n_int
                 row["n_fix"] = rt.n_fix
                 row["tree_base"], row["tree_len"] = b_tree, len(rt.tree)
                 row["node0"], row["n_own"], row["n_local"], row["n_act"] = rt.node0, rt.n_own, rt.n_local, rt.n_act
@@ -600,7 +603,7 @@ def _pack(networks, bcs, probs, cluster: int | None = None) -> Batch:
         elem_EA=EA, plans=_cat(plans, np.int32),
         ell=_cat(ell, np.uint32).view(np.int32), fix_g=_cat(fix_g, np.int32),
         act_ab=_cat(act_ab, np.uint32).view(np.int32), act_L=act_L,
-        halo_g=_cat(halo_g, np.int32), send=_cat(send, np.int32, MAX_SEND), trees=_cat(trees, np.int32),
+        halo_g=_cat(halo_g, np.int32), runs=_cat(runs, np.int32, RUN_WORDS), trees=_cat(trees, np.int32),
         order=np.asarray(order, dtype=np.int32),
         problems=desc.view(np.uint8).copy(), parts=parts.view(np.uint8).copy(),
     )
@@ -686,16 +689,10 @@ class DeviceBatch:
                 g["grid_clusters"] = 1
                 g["flags"] |= nat.GF_SERIAL  # groups one after another on the caller's stream
             T = int(g["block_threads"])
-            if int(g["max_own_dofs"]) > dofs_per_thread_cap(T) * T:
+            if int(g["max_own_dofs"]) > dofs_per_thread_cap(T, bool(g["fprv_global"])) * T:
                 raise nat.NativeError(nat.FRB_E_TOO_LARGE,
                                       f"team_size {T} cannot hold {int(g['max_own_dofs'])} own DOFs")
-            ledger_T = min(T, 512) if cfg.energy_check_interval > 0 else T
-            if ledger_T < 8 * int(g["max_rank_leaves"]):
-                raise nat.NativeError(
-                    nat.FRB_E_INVALID,
-                    f"a team of {ledger_T} threads is below the {8 * int(g['max_rank_leaves'])} the pairwise "
-                    f"chain sums of a rank need (8 per leaf, {int(g['max_rank_leaves'])} leaves)"
-                    + ("; the work-ledger kernels run at most 512 threads" if ledger_T < T else ""))
+
         n = int(h.node_base[-1])
         dev = self.device
         u = torch.empty(3 * n, dtype=torch.float64, device=dev)
@@ -713,7 +710,7 @@ class DeviceBatch:
         fb.groups = groups_c.ctypes.data
         t = self.t
         for k in ("parts", "order", "X", "node_mass", "inc_node", "inc", "elem_ab", "elem_L", "elem_EA",
-                  "plans", "ell", "act_ab", "act_L", "act_EA", "halo_g", "send", "fix_g", "trees"):
+                  "plans", "ell", "act_ab", "act_L", "act_EA", "halo_g", "runs", "fix_g", "trees"):
             setattr(fb, k, t[k].data_ptr() if k in t and t[k].numel() else None)
         fb.problems = desc_t.data_ptr()
         fb.u, fb.f, fb.work = u.data_ptr(), f.data_ptr(), work.data_ptr()

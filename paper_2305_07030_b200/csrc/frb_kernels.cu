@@ -84,11 +84,11 @@ int64_t frb_rank_smem_bytes(int32_t n_pos, int32_t n_own, int32_t n_act, int32_t
                             int32_t fprv_global) {
   const int64_t nf = 3 * static_cast<int64_t>(n_own);
   return 8 * (3 * static_cast<int64_t>(n_pos) + (fprv_global ? 1 : 2) * nf + (nf > n_act ? nf : n_act) + n_own +
-              3 * static_cast<int64_t>(n_slots) + 144) +
+              3 * static_cast<int64_t>(n_slots) + 160) +
          4 * ((static_cast<int64_t>(n_prog) + 1) & ~1LL);
 }
 
-int frb_max_dofs_per_thread(int block_threads) { return dofs_cap(block_threads); }
+int frb_max_dofs_per_thread(int block_threads, int fprv_global) { return dofs_cap(block_threads, fprv_global != 0); }
 
 }  // extern "C"
 
@@ -107,9 +107,6 @@ int launch_one(const frb_batch* batch, const frb_config* cfg, int gi, int optin,
     // work-ledger kernels (a diagnostic, kept out of the production
     // kernels' code): CTAs of at most 512 threads, up to 16 DOFs each
     const int T = g.block_threads < 512 ? g.block_threads : 512;
-    if (T < 8 * g.max_rank_leaves)
-      return set_err(FRB_E_INVALID, "the work-ledger kernels run at most 512 threads per CTA, fewer than the 8 per "
-                                    "pairwise leaf a rank needs; use a larger cluster");
     const int ke = (g.max_own_dofs + T - 1) / T;
     if (ke > 16) return set_err(FRB_E_TOO_LARGE, "too many free DOFs per thread for the ledger kernels");
     return frb_tu::dispatch_energy(batch, cfg, g, q, s, T, ke);
@@ -117,10 +114,8 @@ int launch_one(const frb_batch* batch, const frb_config* cfg, int gi, int optin,
   // production kernels run with exactly MAXT threads (the template's CTA
   // size, >= block_threads): DOFs per thread follow from that
   const int tpl = g.block_threads <= 256 ? 256 : g.block_threads <= 512 ? 512 : g.block_threads <= 768 ? 768 : 1024;
-  if (tpl < 8 * g.max_rank_leaves)
-    return set_err(FRB_E_INVALID, "block_threads below 8 threads per pairwise leaf of a rank");
   const int k = (g.max_own_dofs + tpl - 1) / tpl;
-  if (k > dofs_cap(g.block_threads)) return set_err(FRB_E_TOO_LARGE, "too many free DOFs per thread");
+  if (k > dofs_cap(g.block_threads, g.fprv_global != 0)) return set_err(FRB_E_TOO_LARGE, "too many free DOFs per thread");
   if (g.block_threads <= 256) rc = frb_tu::dispatch_256(batch, cfg, g, q, s, k);
   else if (g.block_threads <= 512) rc = frb_tu::dispatch_512(batch, cfg, g, q, s, k);
   else if (g.block_threads <= 768) rc = frb_tu::dispatch_768(batch, cfg, g, q, s, k);

@@ -31,8 +31,8 @@
 // Work per iteration on each rank (T threads; own DOF d owned by thread d%T):
 //   F1 coefs   per active element (>= 1 own endpoint): EA (l-L)/(L l)
 //   F2 gather  per own node: f = A + B from the coefficients
-//   A  per DOF k_hat, sq = (u k_hat) u, sq2 = (u m) u, ff = f f
-//   C  chains  per (own leaf, chain): ordered sums, folds -> local tree slots
+//   A  per DOF k_hat, sq = (u k_hat) u, sq2 = (u m) u
+//   C  chains  per (own leaf, chain): ordered sums of sq, sq2, f f, folds -> local tree slots
 //   T  tree    warp 0: local program, exports (+ flags, ledger partials) to the
 //              peers, wait, top program, c / residual / convergence; warps
 //              1.. meanwhile form (-f)/m of every own DOF
@@ -57,7 +57,7 @@
 // peer's buffer is addressed by the same offset; Layout):
 //   pos   [PN][3]  positions (AoS) of own, halo and fixed local nodes; an own
 //                  DOF's slot holds its sq between A and C.
-//   fcur  [NFO]    f from F2; ff after A; (-f)/m after T
+//   fcur  [NFO]    f from F2 (C squares it where it sums f f); (-f)/m after T
 //   fprv  [NFO]    f of the previous iteration; the current f after A (in
 //                  global memory instead for networks too large for it)
 //   cf    [CF]     F1 element coefficients, then sq2
@@ -69,6 +69,7 @@
 //                  while this rank still reads the current ones (it cannot
 //                  run two ahead: that needs this rank's next exports)
 //   fin  [16]      per-rank final kinetic-energy partials (epilogue)
+//   ack  [16]      halo-copy acknowledgements from the receiving ranks
 //   rm    [NFO/3]  refined reciprocal (div_fast's r2) of each own node's
 //                  mass: (-f)/m then costs 3 FP64 ops instead of 9 + MUFU
 //   prog           the rank's tree block (programs, exports)
@@ -138,6 +139,18 @@ __device__ __forceinline__ void st_async(uint32_t addr, double v, uint32_t bar) 
                : "r"(addr), "l"(__double_as_longlong(v)), "r"(bar)
                : "memory");
 }
+// Bulk copy (TMA engine) of `bytes` from this CTA's shared memory into a
+// peer's, completing `bytes` transaction bytes on the peer's mbarrier.
+// Addresses and size are 16-byte multiples (partition.py lays out the halo).
+__device__ __forceinline__ void bulk_copy_to_peer(uint32_t dst, uint32_t src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               :
+               : "r"(dst), "r"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
+// Generic-proxy shared-memory writes become visible to the async proxy (the
+// bulk copies read what the threads wrote).
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" : : "r"(smem_u32(bar)), "r"(count) : "memory");
 }
@@ -189,19 +202,21 @@ struct Net {
 };
 
 struct Rank {
-  int node0, n_own, n_local, n_fix, n_act;
+  int node0, n_own, n_local, n_fix, n_act, n_int;
   int S, SA, SB, leaf0, n_leaves;
   int PN, NFO, CF;  // uniform SMEM extents of the problem (max over ranks)
   int LS, TS, PI;   // tree: local slots, top slots, block words (uniform)
   int tree_len, n_exp, root_top;
   uint32_t halo_bytes, leaf_bytes;  // transaction bytes this rank receives per phase
+  uint32_t ack_from;                // ranks that copy halo positions to this one
+  int n_runs, n_dst;                // outgoing halo copies, distinct ranks they go to
+  const int4* runs;                 // (dst rank, src byte, dst byte, bytes)
   const int* tree;
   const uint32_t* ell;
   const uint32_t* act_ab;
   const double* act_L;
   const double* act_EA;
   const int* halo_g;
-  const int2* send;
   const int* fix_g;
 };
 
@@ -237,6 +252,7 @@ __device__ void load_views(Net& n, Rank& R, const frb_batch& b, int p, int r) {
   R.n_local = Q.n_local;
   R.n_fix = Q.n_fix;
   R.n_act = Q.n_act;
+  R.n_int = Q.n_int;
   R.S = Q.ell_stride;
   R.SA = Q.slots_a;
   R.SB = Q.slots_b;
@@ -249,7 +265,15 @@ __device__ void load_views(Net& n, Rank& R, const frb_batch& b, int p, int r) {
   R.PI = R.tree[2];
   R.n_exp = R.tree[6];
   R.root_top = R.tree[7];
-  R.halo_bytes = 24u * static_cast<uint32_t>(Q.n_local - Q.n_own);
+  R.halo_bytes = static_cast<uint32_t>(Q.halo_bytes);
+  R.ack_from = Q.ack_from;
+  R.n_runs = Q.n_runs;
+  R.runs = reinterpret_cast<const int4*>(b.runs) + Q.runs_base;
+  {
+    uint32_t dst = 0;
+    for (int i = 0; i < Q.n_runs; ++i) dst |= 1u << R.runs[i].x;
+    R.n_dst = __popc(dst);
+  }
   R.leaf_bytes = 24u * static_cast<uint32_t>(R.tree[8] - R.n_exp) + 8u * static_cast<uint32_t>(n.C - 1);
   // uniform extents: maxima over the problem's ranks
   R.PN = R.NFO = R.CF = 0;
@@ -265,7 +289,6 @@ __device__ void load_views(Net& n, Rank& R, const frb_batch& b, int p, int r) {
   R.act_L = b.act_L + P.actv_base + Q.actv_off;
   R.act_EA = (b.act_EA && !n.ea_uniform) ? b.act_EA + P.actv_base + Q.actv_off : nullptr;
   R.halo_g = b.halo_g + Q.halo_base;
-  R.send = reinterpret_cast<const int2*>(b.send) + Q.send_base;
   R.fix_g = b.fix_g + Q.fix_base;
 }
 
@@ -392,12 +415,16 @@ __device__ __noinline__ LenCoef exact_elem(int o_pos, uint32_t ab, double L, dou
   return exact_len_coef(dsub(pb[0], pa[0]), dsub(pb[1], pa[1]), dsub(pb[2], pa[2]), L, EA);
 }
 
-__device__ __forceinline__ bool element_coefs(int T, int n_act, const uint32_t* __restrict__ act_ab,
+// Active elements [first, end) of the rank: the interior ones (no halo
+// endpoint, partition.py orders them first) overlap the halo copies, the cut
+// ones follow the halo wait.
+__device__ __forceinline__ bool element_coefs(int T, int first, int n_act, const uint32_t* __restrict__ act_ab,
                                               const double* __restrict__ act_L, const double* __restrict__ act_EA,
                                               double ea, int o_pos, int o_cf) {
   bool bad = false;
+  if (first >= n_act) return bad;
   const int last = n_act - 1;
-  for (int e0 = threadIdx.x; e0 < n_act; e0 += kElem * T) {
+  for (int e0 = first + threadIdx.x; e0 < n_act; e0 += kElem * T) {
     uint32_t ab[kElem];
     double L[kElem], EA[kElem], l[kElem], cf[kElem];
     bool ok[kElem];
@@ -533,6 +560,7 @@ struct Scalars {
   uint32_t peer_smem[FRB_MAX_CLUSTER];  // shared::cluster base of each rank's dynamic SMEM
   uint32_t peer_bar_h[FRB_MAX_CLUSTER]; // each rank's halo mbarrier
   uint32_t peer_bar_s[FRB_MAX_CLUSTER]; // each rank's leaf-sum mbarrier
+  uint32_t peer_bar_a[FRB_MAX_CLUSTER]; // each rank's halo-copy acknowledgement mbarrier
 };
 
 // Phase timing: thread 0 charges the cycles since the previous mark to
@@ -794,7 +822,7 @@ __device__ __forceinline__ Layout layout(const Rank& R) {
   o.lslot = o.cf + R.CF;
   o.tslot = o.lslot + 3 * R.LS;
   o.flag = o.tslot + 6 * R.TS;  // two parity buffers of top slots
-  o.rm = o.flag + 2 * 64 + 16;    // two parity buffers of flags[16] + partials[16][3]; fin[16]
+  o.rm = o.flag + 2 * 64 + 32;    // two parity buffers of flags[16] + partials[16][3]; fin[16]; ack[16]
   o.prog = 2 * (o.rm + R.NFO / 3);  // refined reciprocal masses of the own nodes
   return o;
 }
@@ -828,9 +856,10 @@ __device__ __forceinline__ void run_prog(const int* prog, int o_slot, int lane) 
 }
 
 struct Mbar {
-  uint64_t* h;   // halo positions
+  uint64_t* h;   // halo positions (bulk copies from the peers)
   uint64_t* s;   // leaf sums + flags
-  uint32_t ph_h, ph_s;
+  uint64_t* a;   // acknowledgements of this rank's outgoing halo copies
+  uint32_t ph_h, ph_s, ph_a;
 };
 
 // Complete the two phases posted for an iteration that will not run, so the
@@ -870,7 +899,6 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
   const double* __restrict__ act_L = R.act_L;
   const double* __restrict__ act_EA = R.act_EA;
   const double ea = n.ea;
-  const int2* __restrict__ send = R.send;
   const uint32_t peer_pos = 8u * o.pos;  // byte offsets in a peer's dynamic SMEM
   // f_prev of own DOF dl: SMEM, or the `f` output array for networks too
   // large for the cluster's SMEM (it ends up holding the final f either way)
@@ -932,39 +960,34 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
     nt = lsize - 8 * q;
   }
 
-  // reference coordinates of the own DOFs stay in registers; bit k of
-  // sendbits: own DOF k is halo to some peer (its node has a send target)
+  // reference coordinates of the own DOFs stay in registers
   double xr[MAXK];
-  uint32_t sendbits = 0;
 #pragma unroll
-  for (int k = 0; k < MAXK; ++k) {
-    const int dl = min(t + k * T, dl_max);
-    xr[k] = __ldg(Xg + dof0 + dl);
-    if (C > 1 && t + k * T < nfo && __ldg(send + dl / 3).x >= 0) sendbits |= 1u << k;
-  }
+  for (int k = 0; k < MAXK; ++k) xr[k] = __ldg(Xg + dof0 + min(t + k * T, dl_max));
 
-  // new position of own DOF k (= dl): local slot + the halo copies of peers
-  auto send_pos = [&](int dl, double x) {
-    {
-      const int node = dl / 3, axis = dl - 3 * node;
-      const int2 tg = __ldg(send + node);
-      if (tg.x >= 0) {
-        const int qr = tg.x >> 24;
-        st_async(sc.peer_smem[qr] + peer_pos + 8u * (3u * (tg.x & 0xffffff) + axis), x, sc.peer_bar_h[qr]);
-      }
-      if (tg.y >= 0) {
-        const int qr = tg.y >> 24;
-        st_async(sc.peer_smem[qr] + peer_pos + 8u * (3u * (tg.y & 0xffffff) + axis), x, sc.peer_bar_h[qr]);
-      }
-    }
-  };
   auto put_local = [&](int dl, double x) {
     g_smem[o.pos + dl] = x;
     if (eramp && alpha < 1.0) n.posg[dof0 + dl] = x;  // ramp reactions read every position
   };
-  auto put_pos = [&](int k, int dl, double x) {
-    put_local(dl, x);
-    if (C > 1 && ((sendbits >> k) & 1u)) send_pos(dl, x);
+  // Halo exchange (thread 0, after every thread's position writes, a proxy
+  // fence and a CTA barrier): one bulk DSMEM copy per run of own nodes a peer
+  // keeps as halo, completing on the peer's halo mbarrier; the peers
+  // acknowledge receipt on this rank's ack mbarrier, which A waits for
+  // before it reuses the own position slots as sq scratch.
+  const uint32_t smem_base = smem_u32(g_smem);
+  auto issue_halo = [&]() {
+    if (R.n_dst > 0) mbar_expect(mb.a, 8u * static_cast<uint32_t>(R.n_dst));
+    for (int i = 0; i < R.n_runs; ++i) {
+      const int4 run = __ldg(R.runs + i);
+      bulk_copy_to_peer(sc.peer_smem[run.x] + static_cast<uint32_t>(run.z), smem_base + static_cast<uint32_t>(run.y),
+                        static_cast<uint32_t>(run.w), sc.peer_bar_h[run.x]);
+    }
+  };
+  auto ack_halo = [&]() {  // thread 0, after the halo wait
+    for (uint32_t bits = R.ack_from; bits; bits &= bits - 1) {
+      const int qr = __ffs(bits) - 1;
+      st_async(sc.peer_smem[qr] + 8u * static_cast<uint32_t>(o.flag + 144 + rank), 0.0, sc.peer_bar_a[qr]);
+    }
   };
 
   // (-f)/m of every own DOF into its f slot of SMEM (free once C has
@@ -978,8 +1001,8 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
 #pragma unroll
       for (int kk = 0; kk < kChunk; ++kk) {
         const int dl = min(d0 + kk * nthr, dl_max);
-        const int i = dl / 3;  // f_prev is read-only in T
-        q[kk] = frb_arith::div_fast_r(-FPRV(dl), __ldg(nmass + i), g_smem[o.rm + i], ok[kk]);
+        const int i = dl / 3;  // f of this iteration, left in fcur by A
+        q[kk] = frb_arith::div_fast_r(-g_smem[o.fcur + dl], __ldg(nmass + i), g_smem[o.rm + i], ok[kk]);
       }
       bool all_ok = true;
 #pragma unroll
@@ -988,7 +1011,7 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
 #pragma unroll
         for (int kk = 0; kk < kChunk; ++kk) {
           const int dl = d0 + kk * nthr;
-          if (!ok[kk] && dl < nfo) q[kk] = exact_div(-FPRV(dl), __ldg(nmass + dl / 3));
+          if (!ok[kk] && dl < nfo) q[kk] = exact_div(-g_smem[o.fcur + dl], __ldg(nmass + dl / 3));
         }
       }
 #pragma unroll
@@ -1024,7 +1047,7 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
     return;
   }
   // initial internal forces on own nodes (:413-420), kept as f_prev
-  element_coefs(T, n_act, act_ab, act_L, act_EA, ea, o.pos, o.cf);
+  element_coefs(T, 0, n_act, act_ab, act_L, act_EA, ea, o.pos, o.cf);
   __syncthreads();
   node_forces(T, n_own, ell, S, SA, SB, o.pos, o.cf, o.fcur);
   __syncthreads();
@@ -1050,7 +1073,7 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
     if (dl < nfo) {
       v[k] = dadd(0.0, dmul(hdt, g_smem[o.fcur + dl]));
       u[k] = dadd(0.0, dmul(dt, v[k]));
-      put_pos(k, dl, dadd(xr[k], u[k]));
+      put_local(dl, dadd(xr[k], u[k]));
     }
   }
   if (ramp) {  // iteration 0's ramp step (:449-453)
@@ -1058,17 +1081,13 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
     set_local_fixed(n, R, &g_smem[o.pos], alpha, ramp);
     if (energy) set_fixed_positions(n, rank, alpha, ramp);
   }
+  if (C > 1) fence_proxy_async();
   __syncthreads();
 
   // ---- relaxation loop (microsolver.py:434-530) ---------------------------
   mark(sc, prof, PH_PRO);
   int it = 0;
   for (;; ++it) {
-    if (C > 1) {  // halo positions of this iteration
-      mbar_wait(mb.h, mb.ph_h);
-      mb.ph_h ^= 1u;
-      mark(sc, prof, PH_HALO);
-    }
     double wfix = 0.0;  // ramp work at the fixed nodes this step (rank 0, thread 0)
     if (eramp && it < ramp_n) {
       csync(C);  // every rank's positions of this step are in posg
@@ -1079,8 +1098,20 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
       }
       alpha_prev = alpha;
     }
-    // F: internal forces at the drifted positions (:456-465)
-    bool bad = element_coefs(T, n_act, act_ab, act_L, act_EA, ea, o.pos, o.cf);
+    // F: internal forces at the drifted positions (:456-465).  With peers:
+    // send this rank's halo copies, evaluate the interior elements while
+    // they fly, then wait for the peers' copies, acknowledge them and
+    // evaluate the elements cut by the rank boundary.
+    if (C > 1 && t == 0) issue_halo();
+    bool bad = element_coefs(T, 0, C > 1 ? R.n_int : n_act, act_ab, act_L, act_EA, ea, o.pos, o.cf);
+    if (C > 1) {
+      mark(sc, prof, PH_F1);
+      mbar_wait(mb.h, mb.ph_h);
+      mb.ph_h ^= 1u;
+      if (t == 0) ack_halo();
+      mark(sc, prof, PH_HALO);
+      bad |= element_coefs(T, R.n_int, n_act, act_ab, act_L, act_EA, ea, o.pos, o.cf);
+    }
     if (ramp && it < ramp_n && rank == 0) bad |= check_elements(n, PosFixed{&n, alpha, ramp}, false);
     __syncthreads();
     mark(sc, prof, PH_F1);
@@ -1091,9 +1122,13 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
 
     // A: k_hat = (f - f_prev)/(dt v) where dt v != 0 else 0, clamped with
     // np.maximum(k_hat, 0) (:468-476); sq = (u k_hat) u, sq2 = (u m) u,
-    // ff = f f (:489).  Outputs: sq -> own position slot, sq2 -> cf,
-    // ff -> fcur, f -> fprv.
+    // f f (:489) is formed by C.  Outputs: sq -> own position slot, sq2 -> cf,
+    // f stays in fcur and is copied to fprv.
     if (C > 1 && t == 0) mbar_expect(mb.h, R.halo_bytes);  // next halo phase
+    if (C > 1 && R.n_dst > 0) {  // the peers have read this rank's positions (they become sq below)
+      mbar_wait(mb.a, mb.ph_a);
+      mb.ph_a ^= 1u;
+    }
     double es[3] = {0.0, 0.0, 0.0};
     // damping mode hoisted out of the per-DOF loop (one copy per mode)
     auto a_phase = [&](auto ad) {
@@ -1145,7 +1180,6 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
               g_smem[o.pos + dl] = dmul(dmul(u[k], khc), u[k]);
               g_smem[o.cf + dl] = dmul(dmul(u[k], m[kk]), u[k]);
             }
-            g_smem[o.fcur + dl] = dmul(f[kk], f[kk]);
             if (energy) {  // f . v_half, f_prev . v_half, (m v_half) . v_half (:538-544)
               const double vh = v[k];
               es[0] = dadd(es[0], dmul(f[kk], vh));
@@ -1174,29 +1208,36 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
     mark(sc, prof, PH_A);
 
     // C: ordered chain sums of one leaf chain + fold + tails -> every rank's
-    // slots; the singular flag travels with them
-    if ((t & ~31) < 8 * R.n_leaves) {  // warp holds at least one chain
+    // slots; the singular flag travels with them.  Round 0 covers leaves
+    // 0 .. T/8 - 1 with the chain role cached in registers; ranks with more
+    // leaves than T/8 (a 512-thread CTA on a 16-rank 32^3 network) run
+    // further rounds, warp w taking leaves 4w + k T/8 .. (quads stay aligned:
+    // T/8 is a multiple of 4).
+    auto chain_round = [&](int lloc, bool has, int ls, int qn, int ntl) {
       double r0 = 0.0, r1 = 0.0, r2 = 0.0;
       double t0 = 0.0, t1 = 0.0, t2 = 0.0;
-      if (chain) {
-        int dl = lstart + j;
-        if (q > 0) {
+      if (has) {
+        int dl = ls + j;
+        if (qn > 0) {
           r0 = g_smem[o.pos + dl];
           r1 = g_smem[o.cf + dl];
-          r2 = g_smem[o.fcur + dl];
+          const double f0 = g_smem[o.fcur + dl];
+          r2 = dmul(f0, f0);  // f f (microsolver.py:494), squared where it is summed
 #pragma unroll 4
-          for (int k = 1; k < q; ++k) {
+          for (int k = 1; k < qn; ++k) {
             dl += 8;
             r0 = dadd(r0, g_smem[o.pos + dl]);
             r1 = dadd(r1, g_smem[o.cf + dl]);
-            r2 = dadd(r2, g_smem[o.fcur + dl]);
+            const double fk = g_smem[o.fcur + dl];
+            r2 = dadd(r2, dmul(fk, fk));
           }
         }
-        if (j < nt) {
-          const int dtl = lstart + 8 * q + j;
+        if (j < ntl) {
+          const int dtl = ls + 8 * qn + j;
           t0 = g_smem[o.pos + dtl];
           t1 = g_smem[o.cf + dtl];
-          t2 = g_smem[o.fcur + dtl];
+          const double ft = g_smem[o.fcur + dtl];
+          t2 = dmul(ft, ft);
         }
         if (!adaptive) r0 = r1 = t0 = t1 = 0.0;
       }
@@ -1207,7 +1248,7 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
         r2 = dadd(r2, __shfl_xor_sync(0xffffffffu, r2, sh));
       }
       const int base = lane & ~7;
-      const int my_nt = chain ? nt : 0;
+      const int my_nt = has ? ntl : 0;
 #pragma unroll
       for (int i = 0; i < 7; ++i) {
         const double a0 = __shfl_sync(0xffffffffu, t0, base + i);
@@ -1232,17 +1273,30 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
         const double q1 = __shfl_down_sync(0xffffffffu, r1, 16);
         const double q2 = __shfl_down_sync(0xffffffffu, r2, 16);
         if (lane == 0) {
-          const int sl = o.lslot + 3 * (t >> 5);  // local slot = the warp's quad
+          const int sl = o.lslot + 3 * (lloc >> 2);  // local slot = the quad of the warp's leaves
           g_smem[sl] = dadd(r0, q0);
           g_smem[sl + 1] = dadd(r1, q1);
           g_smem[sl + 2] = dadd(r2, q2);
         }
-      } else if (chain && j == 0) {
+      } else if (has && j == 0) {
         const int sl = o.lslot + 3 * lloc;  // local leaf lloc
         g_smem[sl] = r0;
         g_smem[sl + 1] = r1;
         g_smem[sl + 2] = r2;
       }
+    };
+    if ((t & ~31) < 8 * R.n_leaves) chain_round(lloc, chain, lstart, q, nt);  // warp holds a chain
+    for (int l0 = (T >> 3) + ((t & ~31) >> 3); l0 < R.n_leaves; l0 += T >> 3) {  // rare extra rounds
+      const int ll = l0 + (lane >> 3);
+      const bool has = ll < R.n_leaves;
+      int ls = 0, qn = 0, ntl = 0;
+      if (has) {
+        ls = __ldg(n.plan + 4 + R.leaf0 + ll) - dof0;
+        const int lsize = __ldg(n.plan + 4 + L + R.leaf0 + ll);
+        qn = lsize >= 8 ? (lsize >> 3) : 0;
+        ntl = lsize - 8 * qn;
+      }
+      chain_round(ll, has, ls, qn, ntl);
     }
     __syncthreads();
     mark(sc, prof, PH_C);
@@ -1399,18 +1453,13 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
         }
       }
     }
-    if (C > 1 && !done) {  // halo copies to the peers: only the few DOFs that have one
-      for (uint32_t bits = sendbits; bits; bits &= bits - 1) {
-        const int dl = t + (__ffs(bits) - 1) * T;
-        send_pos(dl, g_smem[o.pos + dl]);
-      }
-    }
     if (!done && ramp && alpha < 1.0) {
       alpha = ramp_alpha(it + 2, ramp_n);
       set_local_fixed(n, R, &g_smem[o.pos], alpha, ramp);
       if (energy) set_fixed_positions(n, rank, alpha, ramp);
     }
     if (done) break;
+    if (C > 1) fence_proxy_async();  // the positions feed the next halo copies
     __syncthreads();
     mark(sc, prof, PH_U);
   }
@@ -1464,7 +1513,7 @@ __global__ void __launch_bounds__(MAXT, 1)
   __shared__ Scalars sc;
   __shared__ Net net;
   __shared__ Rank rk;
-  __shared__ uint64_t bars[2];
+  __shared__ uint64_t bars[3];
   const int C = static_cast<int>(cg::this_cluster().num_blocks());
   const int rank = C > 1 ? static_cast<int>(cg::this_cluster().block_rank()) : 0;
   if (threadIdx.x == 0) {
@@ -1473,15 +1522,17 @@ __global__ void __launch_bounds__(MAXT, 1)
     if (C > 1) {
       mbar_init(&bars[0], 1);
       mbar_init(&bars[1], 1);
+      mbar_init(&bars[2], 1);
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
       for (int q = 0; q < C; ++q) {
         sc.peer_smem[q] = mapa(smem_u32(g_smem), q);
         sc.peer_bar_h[q] = mapa(smem_u32(&bars[0]), q);
         sc.peer_bar_s[q] = mapa(smem_u32(&bars[1]), q);
+        sc.peer_bar_a[q] = mapa(smem_u32(&bars[2]), q);
       }
     }
   }
-  Mbar mb{&bars[0], &bars[1], 0u, 0u};
+  Mbar mb{&bars[0], &bars[1], &bars[2], 0u, 0u, 0u};
   csync(C);  // barriers initialised cluster-wide before any remote use
   for (;;) {
     if (rank == 0 && threadIdx.x == 0) {
@@ -1520,7 +1571,9 @@ int cuda_check(cudaError_t e, const char* where) {
   return FRB_E_CUDA;
 }
 
-int dofs_cap(int threads) { return threads > 768 ? 8 : threads > 512 ? 12 : 16; }
+// most register-held DOFs per thread a CTA size instantiates (24 only for
+// the global-f_prev kernels of 256 threads, 16 otherwise up to 512 threads)
+int dofs_cap(int threads, bool fg) { return threads > 768 ? 8 : threads > 512 ? 12 : (threads > 256 || !fg) ? 16 : 24; }
 
 template <int MAXK, int MAXT, bool kFG, bool kEnergy = false>
 int launch_group(const frb_batch* batch, const frb_config* cfg, const frb_group& g, int32_t* queue,
@@ -1577,7 +1630,12 @@ int launch_group(const frb_batch* batch, const frb_config* cfg, const frb_group&
 template <int MAXT>
 int dispatch_k(const frb_batch* batch, const frb_config* cfg, const frb_group& g, int32_t* queue,
                cudaStream_t s, int k) {
-  if (g.fprv_global) {  // large networks: CTAs of 512 / 768 / 1024 threads, >= 4 DOFs per thread
+  if (g.fprv_global) {  // large networks: CTAs of 256 / 512 / 768 / 1024 threads
+    if constexpr (MAXT == 256) {
+      if (k <= 16) return launch_group<16, MAXT, true>(batch, cfg, g, queue, s);
+      if (k <= 20) return launch_group<20, MAXT, true>(batch, cfg, g, queue, s);
+      if (k <= 24) return launch_group<24, MAXT, true>(batch, cfg, g, queue, s);
+    }
     if constexpr (MAXT == 512) {
       if (k <= 8) return launch_group<8, MAXT, true>(batch, cfg, g, queue, s);
       if (k <= 12) return launch_group<12, MAXT, true>(batch, cfg, g, queue, s);
@@ -1593,7 +1651,7 @@ int dispatch_k(const frb_batch* batch, const frb_config* cfg, const frb_group& g
         if (k <= 12) return launch_group<12, MAXT, true>(batch, cfg, g, queue, s);
       }
     }
-    return set_err(FRB_E_INVALID, "fprv_global groups need 257..1024 threads per CTA");
+    return set_err(FRB_E_TOO_LARGE, "too many free DOFs per thread for this CTA size");
   }
   if (k <= 1) return launch_group<1, MAXT, false>(batch, cfg, g, queue, s);
   if (k <= 4) return launch_group<4, MAXT, false>(batch, cfg, g, queue, s);

@@ -11,7 +11,8 @@ nearest to the even split.
 Per rank the kernel works in *local* node numbering; every local node's
 position lives in the rank's shared memory (AoS, 3 doubles per node):
     [0, n_own)                 own free nodes (global solver ids node0 ...)
-    [n_own, n_local)           halo: free neighbours owned by other ranks
+    [n_own, n_local)           halo: free neighbours owned by other ranks,
+                               grouped by owner, plus alignment gap slots
     [n_local, n_local + n_fix) fixed nodes that end an active element
 Tables built here (all int32, shared by networks of equal topology):
     ell_o / ell_c   slot-major incidence of the own nodes (other endpoint in
@@ -19,10 +20,16 @@ Tables built here (all int32, shared by networks of equal topology):
                     device gets them packed as one u32 per slot (``ell``)
     act_ab          active elements (>= 1 own endpoint) in local numbering
     act_elem        their global element ids (per-network L / EA lookups)
-    halo_g          global solver id of each halo node
+    halo_g          global solver id of each halo slot (gaps: a valid dummy)
     fix_g           global solver id of each local fixed node
-    send            per own node up to two (rank << 24 | local index) targets
-                    that keep it as halo (-1 = none)
+    runs            the rank's outgoing halo copies: (dst rank, src byte, dst
+                    byte, bytes) -- one bulk DSMEM copy (cp.async.bulk) per
+                    run of consecutive own nodes that a peer keeps as
+                    consecutive halo slots.  Bulk copies need 16-byte aligned
+                    addresses and sizes, and a position is 24 bytes, so the
+                    copy widens each run to even node bounds [lo, hi) at the
+                    source and lands it at an even slot of the receiver's
+                    halo layout; the extra nodes fill gap slots.
 """
 
 from __future__ import annotations
@@ -33,8 +40,8 @@ import numpy as np
 
 from .plan import PlanView, tree_split
 
-MAX_SEND = 2
 MAX_LOCAL = 0xFFFF            # local node ids and active-element ids are 16 bit
+RUN_WORDS = 4                 # (dst rank, src byte, dst byte, bytes) per halo run
 
 
 @dataclass
@@ -49,9 +56,12 @@ class RankTables:
     act_ab: np.ndarray       # (n_act, 2) int32
     act_elem: np.ndarray     # (n_act,) int64
     halo_g: np.ndarray       # (n_local - n_own,) int32
-    send: np.ndarray         # (n_own, MAX_SEND) int32
     fix_g: np.ndarray = None # (n_fix,) int32
     tree: np.ndarray = None  # int32 block of plan.tree_split (local/top programs, exports)
+    runs: np.ndarray = None  # (n_runs, RUN_WORDS) int32 outgoing bulk halo copies
+    halo_bytes: int = 0      # bytes of halo copies this rank receives per iteration
+    ack_from: int = 0        # bit q: rank q sends halo copies to this rank
+    n_int: int = 0           # act_elem[:n_int] have no halo endpoint
 
     @property
     def stride(self) -> int:
@@ -137,23 +147,76 @@ def partition(n_nodes: int, n_free: int, ia: np.ndarray, ib: np.ndarray, ell_oth
         ranks_nodes.append((n0, n1))
     elem_ids = np.arange(len(ia))
     ns = slots_a + slots_b
-    ranks = []
-    halo_lists = []
+    # pass 1: active elements, halo and fixed sets per rank
+    acts, halos, fixes, n_ints = [], [], [], []
     for r, (n0, n1) in enumerate(ranks_nodes):
-        n_own = n1 - n0
         own_a = (ia >= n0) & (ia < n1)
         own_b = (ib >= n0) & (ib < n1)
         act = elem_ids[own_a | own_b]
         ends = np.concatenate([ia[act], ib[act]])
-        halo = np.unique(ends[(ends < n_free) & ((ends < n0) | (ends >= n1))])
-        fix = np.unique(ends[ends >= n_free])
-        halo_lists.append(halo)
-        n_local = n_own + len(halo)
+        # interior elements (no halo endpoint) first: the kernel evaluates
+        # them while the halo copies are in flight
+        cut = np.zeros(len(act), dtype=bool)
+        for e_end in (ia[act], ib[act]):
+            cut |= (e_end < n_free) & ((e_end < n0) | (e_end >= n1))
+        act = np.concatenate([act[~cut], act[cut]])
+        n_ints.append(int((~cut).sum()))
+        acts.append(act)
+        halos.append(np.unique(ends[(ends < n_free) & ((ends < n0) | (ends >= n1))]))
+        fixes.append(np.unique(ends[ends >= n_free]))
+    # pass 2: halo layouts (runs of consecutive nodes per owner, parity-aligned)
+    out_runs = [[] for _ in range(C)]
+    layouts = []
+    for r, (n0, n1) in enumerate(ranks_nodes):
+        halo = halos[r]
+        n_own = n1 - n0
+        slot_of = np.empty(len(halo), dtype=np.int64)
+        gids = []
+        cur = n_own
+        recv = 0
+        ack = 0
+        if len(halo):
+            brk = np.flatnonzero(np.diff(halo) != 1) + 1
+            starts = np.r_[0, brk]
+            ends_ = np.r_[brk, len(halo)]
+            for a0, a1 in zip(starts, ends_):
+                # a run may span two owners only if their ranges touch: split there
+                seg_owner = owner[halo[a0:a1]]
+                sp = np.r_[0, np.flatnonzero(np.diff(seg_owner) != 0) + 1, a1 - a0]
+                for c0, c1 in zip(sp[:-1], sp[1:]):
+                    g0 = int(halo[a0 + c0])
+                    q = int(owner[g0])
+                    src = g0 - ranks_nodes[q][0]
+                    n = int(c1 - c0)
+                    # copy source nodes [lo, hi): both ends even (24-byte
+                    # nodes, 16-byte aligned bulk copies), landing at an even
+                    # slot; the extra nodes at either end fill gap slots
+                    lo = src - (src % 2)
+                    hi = src + n + ((src + n) % 2)
+                    if cur % 2:
+                        gids.append(g0)
+                        cur += 1
+                    if src > lo:
+                        gids.append(g0)
+                    slot_of[a0 + c0:a0 + c1] = cur + (src - lo) + np.arange(n)
+                    gids.extend(int(g) for g in halo[a0 + c0:a0 + c1])
+                    if hi > src + n:
+                        gids.append(g0)
+                    out_runs[q].append((r, 24 * lo, 24 * cur, 24 * (hi - lo)))
+                    cur += hi - lo
+                    recv += 24 * (hi - lo)
+                    ack |= 1 << q
+        layouts.append((slot_of, np.asarray(gids, dtype=np.int64), cur, recv, ack))
+    ranks = []
+    for r, (n0, n1) in enumerate(ranks_nodes):
+        n_own = n1 - n0
+        act, halo, fix = acts[r], halos[r], fixes[r]
+        slot_of, gids, n_local, recv, ack = layouts[r]
         if n_local + len(fix) > MAX_LOCAL or len(act) > MAX_LOCAL:
             raise ValueError(f"rank {r} needs {n_local + len(fix)} local nodes / {len(act)} elements "
                              f"(limit {MAX_LOCAL}); use a larger cluster")
 
-        def to_local(g, n0=n0, n1=n1, halo=halo, fix=fix, n_local=n_local, n_own=n_own):
+        def to_local(g, n0=n0, n1=n1, halo=halo, fix=fix, n_local=n_local, slot_of=slot_of):
             g = np.asarray(g, dtype=np.int64)
             out = np.empty_like(g)
             own = (g >= n0) & (g < n1)
@@ -161,7 +224,7 @@ def partition(n_nodes: int, n_free: int, ia: np.ndarray, ib: np.ndarray, ell_oth
             hal = ~own & ~fixed
             out[own] = g[own] - n0
             out[fixed] = n_local + np.searchsorted(fix, g[fixed])
-            out[hal] = n_own + np.searchsorted(halo, g[hal])
+            out[hal] = slot_of[np.searchsorted(halo, g[hal])]
             return out
 
         act_index = np.full(len(ia), -1, dtype=np.int64)
@@ -181,21 +244,13 @@ def partition(n_nodes: int, n_free: int, ia: np.ndarray, ib: np.ndarray, ell_oth
         ranks.append(RankTables(node0=n0, n_own=n_own, n_local=n_local,
                                 leaf0=int(lstarts[0]) if len(lstarts) else 0,
                                 n_leaves=len(lstarts), ell_o=ell_o, ell_c=ell_c, act_ab=act_ab,
-                                act_elem=act.astype(np.int64), halo_g=halo.astype(np.int32),
-                                send=np.full((n_own, MAX_SEND), -1, dtype=np.int32),
-                                fix_g=fix.astype(np.int32)))
+                                act_elem=act.astype(np.int64), halo_g=gids.astype(np.int32),
+                                fix_g=fix.astype(np.int32),
+                                runs=np.asarray(out_runs[r], dtype=np.int32).reshape(-1, RUN_WORDS),
+                                halo_bytes=recv, ack_from=ack, n_int=n_ints[r]))
     blocks = tree_split(plan, [(rt.leaf0, rt.leaf0 + rt.n_leaves) for rt in ranks])
     for rt, bk in zip(ranks, blocks):
         rt.tree = bk
-    # send lists: rank q keeps node g as halo at local index n_own_q + k
-    for q, halo in enumerate(halo_lists):
-        for k, g in enumerate(halo):
-            r = int(owner[g])
-            row = ranks[r].send[g - ranks[r].node0]
-            slot = int(np.flatnonzero(row < 0)[0]) if (row < 0).any() else -1
-            if slot < 0:
-                raise ValueError("node is halo to more than two ranks; use a smaller cluster")
-            row[slot] = (q << 24) | (ranks[q].n_own + k)
     return Partition(C=C, slots_a=slots_a, slots_b=slots_b, ranks=ranks)
 
 
@@ -206,7 +261,8 @@ def rank_smem_bytes(rt: RankTables, fprv_global: bool = False) -> int:
     in global memory -- f_prev (8 B per own DOF each), coefficients / sq2
     max(own DOFs, n_act), local tree slots and two parity buffers of top
     tree slots (3 doubles each), two parity buffers of 64 cluster flag /
-    ledger words plus 16 final ledger words, one refined reciprocal mass per
+    ledger words plus 16 final ledger words and 16 halo-copy acknowledgement
+    words, one refined reciprocal mass per
     own node and the int32 tree block (programs + exports)."""
     return smem_bytes(rt.n_local + rt.n_fix, rt.n_own, rt.n_act, int(rt.tree[0]) + 2 * int(rt.tree[1]),
                       int(rt.tree[2]), fprv_global)
@@ -224,5 +280,5 @@ def partition_smem_bytes(part: "Partition", fprv_global: bool = False) -> int:
 
 def smem_bytes(n_pos: int, n_own: int, n_act: int, n_slots: int, n_prog: int, fprv_global: bool = False) -> int:
     nf = 3 * n_own
-    return 8 * (3 * n_pos + (1 if fprv_global else 2) * nf + max(nf, n_act) + n_own + 3 * n_slots + 144) + \
+    return 8 * (3 * n_pos + (1 if fprv_global else 2) * nf + max(nf, n_act) + n_own + 3 * n_slots + 160) + \
         4 * ((n_prog + 1) & ~1)

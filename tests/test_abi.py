@@ -28,7 +28,7 @@ def test_struct_layouts():
     assert C.sizeof(nat.FrbConfig) == 48
     assert C.sizeof(nat.FrbBatch) == 8 + 26 * 8
     assert nat.PROBLEM_DTYPE.itemsize == 184
-    assert nat.PART_DTYPE.itemsize == 104
+    assert nat.PART_DTYPE.itemsize == 120
     assert nat.GROUP_DTYPE.itemsize == 40
     assert nat.RESULT_DTYPE.itemsize == 144
 
@@ -36,7 +36,8 @@ def test_struct_layouts():
 def test_dofs_per_thread_cap_matches_host():
     from paper_2305_07030_b200.batch import dofs_per_thread_cap
     for t in (64, 256, 512, 544, 768, 800, 1024):
-        assert nat.lib().frb_max_dofs_per_thread(t) == dofs_per_thread_cap(t)
+        for fg in (0, 1):
+            assert nat.lib().frb_max_dofs_per_thread(t, fg) == dofs_per_thread_cap(t, bool(fg))
 
 
 def test_invalid_arguments_fail_loudly():

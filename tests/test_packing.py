@@ -103,12 +103,30 @@ def test_partition_tables(net, C):
                 if o >= 0:
                     assert glob(o) == go
                     assert rt.act_elem[c] == t.ell_elem[k, rt.node0 + i]
-        # every halo node is sent here by its owner at the right local index
-        for k, g in enumerate(halo):
-            owner = next(q for q in part.ranks if q.node0 <= g < q.node0 + q.n_own)
-            q = part.ranks.index(owner)
-            targets = [s for s in owner.send[g - owner.node0] if s >= 0]
-            assert (r << 24 | (rt.n_own + k)) in targets and q != r
+        # every halo slot an element references is filled by exactly one bulk
+        # copy of its owner's position (16-byte aligned addresses and sizes)
+        used = {int(x) for x in rt.act_ab.reshape(-1) if rt.n_own <= x < rt.n_local}
+        filled = {}
+        recv = 0
+        senders = 0
+        for q, src in enumerate(part.ranks):
+            for dst_rank, sb, db, nb in src.runs:
+                assert sb % 16 == 0 and db % 16 == 0 and nb % 16 == 0 and nb > 0
+                if dst_rank != r:
+                    continue
+                assert q != r
+                senders |= 1 << q
+                recv += nb
+                for j in range(nb // 24):
+                    d, sn = db // 24 + j, sb // 24 + j
+                    assert d not in filled and rt.n_own <= d < rt.n_local
+                    filled[d] = src.node0 + sn if sn < src.n_own else None
+        assert recv == rt.halo_bytes and senders == rt.ack_from
+        # interior elements (no halo endpoint) first, cut elements last
+        is_halo = (rt.act_ab >= rt.n_own) & (rt.act_ab < rt.n_local)
+        assert not is_halo[:rt.n_int].any() and is_halo[rt.n_int:].any(axis=1).all()
+        for d in used:
+            assert filled.get(d) == glob(d), (r, d)
     assert nxt == NF and leaf == t.n_leaves
 
 
@@ -243,3 +261,19 @@ def test_zero_mass_node_raises_like_reference():
     net = frb.FiberNetwork(X, np.array([[0, 1, 0], [1, 2, 0]]), [frb.Material(1, 1, 1)], frozenset({0}))
     with pytest.raises(frb.NetworkMassError, match="node 3 has zero mass"):
         frb.pack_batch([net], [frb.AffineBC(np.eye(3))])
+
+
+@pytest.mark.parametrize("n,C", [(15, 2), (24, 8), (32, 16), (17, 3)])
+def test_halo_runs_are_aligned_bulk_copies(n, C):
+    """The BASELINE lattices' cluster partitions: every outgoing halo run is a
+    legal cp.async.bulk (16-byte aligned source, destination and size) and
+    the receiving ranks expect exactly the bytes that arrive."""
+    t = fb.build_problem(frb.generate_lattice(n, n, n, 0.3, 1), frb.AffineBC(np.eye(3))).topo
+    part = t.partition(C)
+    recv = [0] * part.C
+    for q, rt in enumerate(part.ranks):
+        for dst, sb, db, nb in rt.runs:
+            assert sb % 16 == 0 and db % 16 == 0 and nb % 16 == 0 and dst != q
+            assert sb // 24 + nb // 24 <= rt.n_local + rt.n_fix + 1
+            recv[dst] += nb
+    assert recv == [rt.halo_bytes for rt in part.ranks]
