@@ -72,6 +72,7 @@
 //   ack  [16]      halo-copy acknowledgements from the receiving ranks
 //   rm    [NFO/3]  refined reciprocal (div_fast's r2) of each own node's
 //                  mass: (-f)/m then costs 3 FP64 ops instead of 9 + MUFU
+//   ms    [NFO/3]  the own nodes' masses (A and (-f)/m read them on chip)
 //   prog           the rank's tree block (programs, exports)
 // u, v and the reference coordinates of a thread's own DOFs live in registers.
 
@@ -809,7 +810,7 @@ __device__ __forceinline__ void write_singular(const frb_batch& b, int p, int ba
 // SMEM layout of a problem, in doubles from g_smem (identical on every
 // rank of the problem, so a peer's buffer is addressed by the same offset).
 struct Layout {
-  int pos, fcur, fprv, cf, lslot, tslot, flag, rm, prog;  // prog: int32 index
+  int pos, fcur, fprv, cf, lslot, tslot, flag, rm, ms, prog;  // prog: int32 index
 };
 
 template <bool kFG>
@@ -823,7 +824,8 @@ __device__ __forceinline__ Layout layout(const Rank& R) {
   o.tslot = o.lslot + 3 * R.LS;
   o.flag = o.tslot + 6 * R.TS;  // two parity buffers of top slots
   o.rm = o.flag + 2 * 64 + 32;    // two parity buffers of flags[16] + partials[16][3]; fin[16]; ack[16]
-  o.prog = 2 * (o.rm + R.NFO / 3);  // refined reciprocal masses of the own nodes
+  o.ms = o.rm + R.NFO / 3;          // refined reciprocal masses of the own nodes
+  o.prog = 2 * (o.ms + R.NFO / 3);  // the own nodes' masses
   return o;
 }
 
@@ -917,7 +919,11 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
   // the rank's tree block (local + top programs, exports) lives in SMEM
   int* const prog = reinterpret_cast<int*>(g_smem) + o.prog;
   for (int k = t; k < R.tree_len; k += T) prog[k] = __ldg(R.tree + k);
-  for (int i = t; i < n_own; i += T) g_smem[o.rm + i] = frb_arith::rcp_refined(__ldg(nmass + i));
+  for (int i = t; i < n_own; i += T) {
+    const double m = __ldg(nmass + i);
+    g_smem[o.ms + i] = m;
+    g_smem[o.rm + i] = frb_arith::rcp_refined(m);
+  }
   const int* const lprog = prog + R.tree[3];
   const int* const tprog = prog + R.tree[4];
   const int* const exps = prog + R.tree[5];
@@ -1002,7 +1008,7 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
       for (int kk = 0; kk < kChunk; ++kk) {
         const int dl = min(d0 + kk * nthr, dl_max);
         const int i = dl / 3;  // f of this iteration, left in fcur by A
-        q[kk] = frb_arith::div_fast_r(-g_smem[o.fcur + dl], __ldg(nmass + i), g_smem[o.rm + i], ok[kk]);
+        q[kk] = frb_arith::div_fast_r(-g_smem[o.fcur + dl], g_smem[o.ms + i], g_smem[o.rm + i], ok[kk]);
       }
       bool all_ok = true;
 #pragma unroll
@@ -1011,7 +1017,7 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
 #pragma unroll
         for (int kk = 0; kk < kChunk; ++kk) {
           const int dl = d0 + kk * nthr;
-          if (!ok[kk] && dl < nfo) q[kk] = exact_div(-g_smem[o.fcur + dl], __ldg(nmass + dl / 3));
+          if (!ok[kk] && dl < nfo) q[kk] = exact_div(-g_smem[o.fcur + dl], g_smem[o.ms + dl / 3]);
         }
       }
 #pragma unroll
@@ -1146,7 +1152,7 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
           const int dl = k0 + kk < nk ? t + (k0 + kk) * T : dl_last;
           f[kk] = g_smem[o.fcur + dl];
           kh[kk] = FPRV(dl);  // f_prev, until the quotient replaces it
-          m[kk] = __ldg(nmass + dl / 3);
+          m[kk] = g_smem[o.ms + dl / 3];
         }
         if constexpr (kAd) {
 #pragma unroll

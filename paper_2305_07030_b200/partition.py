@@ -262,7 +262,7 @@ def rank_smem_bytes(rt: RankTables, fprv_global: bool = False) -> int:
     max(own DOFs, n_act), local tree slots and two parity buffers of top
     tree slots (3 doubles each), two parity buffers of 64 cluster flag /
     ledger words plus 16 final ledger words and 16 halo-copy acknowledgement
-    words, one refined reciprocal mass per
+    words, one refined reciprocal mass and the mass per
     own node and the int32 tree block (programs + exports)."""
     return smem_bytes(rt.n_local + rt.n_fix, rt.n_own, rt.n_act, int(rt.tree[0]) + 2 * int(rt.tree[1]),
                       int(rt.tree[2]), fprv_global)
@@ -280,5 +280,5 @@ def partition_smem_bytes(part: "Partition", fprv_global: bool = False) -> int:
 
 def smem_bytes(n_pos: int, n_own: int, n_act: int, n_slots: int, n_prog: int, fprv_global: bool = False) -> int:
     nf = 3 * n_own
-    return 8 * (3 * n_pos + (1 if fprv_global else 2) * nf + max(nf, n_act) + n_own + 3 * n_slots + 160) + \
+    return 8 * (3 * n_pos + (1 if fprv_global else 2) * nf + max(nf, n_act) + 2 * n_own + 3 * n_slots + 160) + \
         4 * ((n_prog + 1) & ~1)
