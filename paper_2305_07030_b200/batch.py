@@ -433,8 +433,8 @@ def _group_threads(max_own_dofs: int, max_rank_leaves: int, n_problems: int, clu
     need = max(64, 8 * max_rank_leaves, math.ceil(max_own_dofs / 16))
     if n_problems * cluster < 148:
         need = max(need, min(512, 32 * math.ceil(max_own_dofs / 32)))
-    if fprv_global:  # 32^3 on 16 ranks: FRB_FG_THREADS overrides (experiments)
-        need = max(need, int(os.environ.get("FRB_FG_THREADS", "768")))
+    if fprv_global:  # 32^3 on 16 ranks: 512 threads (57.6 ms per wave of 7) beat 768 (58.5) and 256 (64)
+        need = max(need, int(os.environ.get("FRB_FG_THREADS", "512")))
     threads = min(MAX_CTA_THREADS, 32 * math.ceil(need / 32))
     while max_own_dofs > dofs_per_thread_cap(threads, fprv_global) * threads and threads < MAX_CTA_THREADS:
         threads += 32

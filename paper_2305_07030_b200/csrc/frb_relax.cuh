@@ -1644,6 +1644,7 @@ int dispatch_k(const frb_batch* batch, const frb_config* cfg, const frb_group& g
     }
     if constexpr (MAXT == 512) {
       if (k <= 8) return launch_group<8, MAXT, true>(batch, cfg, g, queue, s);
+      if (k <= 11) return launch_group<11, MAXT, true>(batch, cfg, g, queue, s);  // 32^3 on 16 ranks
       if (k <= 12) return launch_group<12, MAXT, true>(batch, cfg, g, queue, s);
       if (k <= 14) return launch_group<14, MAXT, true>(batch, cfg, g, queue, s);
       if (k <= 16) return launch_group<16, MAXT, true>(batch, cfg, g, queue, s);
@@ -1651,6 +1652,7 @@ int dispatch_k(const frb_batch* batch, const frb_config* cfg, const frb_group& g
     if constexpr (MAXT >= 768) {
       if (k <= 4) return launch_group<4, MAXT, true>(batch, cfg, g, queue, s);
       if (k <= 6) return launch_group<6, MAXT, true>(batch, cfg, g, queue, s);
+      if (k <= 7) return launch_group<7, MAXT, true>(batch, cfg, g, queue, s);  // 32^3 on 16 ranks
       if (k <= 8) return launch_group<8, MAXT, true>(batch, cfg, g, queue, s);
       if constexpr (MAXT <= 768) {
         if (k <= 10) return launch_group<10, MAXT, true>(batch, cfg, g, queue, s);
