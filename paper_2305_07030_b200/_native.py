@@ -27,7 +27,8 @@ PHASE_NAMES = ("F1 coefs", "F2 gather", "A per-DOF", "C chains", "T local+exp", 
 
 EXPORTS = ("frb_abi_version", "frb_last_error", "frb_device_info", "frb_rank_smem_bytes",
            "frb_max_dofs_per_thread", "frb_solve_batch", "frb_internal_forces",
-           "frb_selftest_arith", "frb_setup_problem", "frb_setup_batch")
+           "frb_selftest_arith", "frb_setup_problem", "frb_setup_batch",
+           "frb_naive_solve", "frb_naive_scratch_doubles")
 
 
 class FrbConfig(C.Structure):
@@ -114,6 +115,10 @@ def lib() -> C.CDLL:
     h.frb_setup_problem.argtypes = [C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32,
                                     C.c_void_p, C.c_void_p, C.c_int64] + [C.c_void_p] * 8
     h.frb_setup_batch.argtypes = [C.c_void_p, C.c_int32, C.c_int32]
+    h.frb_naive_solve.argtypes = [C.POINTER(FrbBatch), C.POINTER(FrbConfig), C.c_int32, C.c_void_p, C.c_int64,
+                                  C.c_void_p]
+    h.frb_naive_scratch_doubles.restype = C.c_int64
+    h.frb_naive_scratch_doubles.argtypes = [C.c_int32] * 3
     if h.frb_abi_version() != ABI_VERSION:
         raise ImportError("libfrb200.so ABI version mismatch (rebuild)")
     _lib = h

@@ -77,9 +77,18 @@ class SerialReference:
 
 @dataclass(frozen=True)
 class NaiveLoop:
-    """Per-operation dispatch (the paper's naive baseline).  Not provided on
-    the device: the B200 build exists to remove per-operation launches."""
+    """Per-operation dispatch, the paper's naive baseline (SPEC.md:360,
+    PAPER.md:71-74): problems strictly one after another, one kernel launch
+    per line of the Fig. 1 loop with the kernel boundary as the cross-worker
+    barrier, and the host checking convergence after every iteration
+    (frb_naive_solve).  Bit-identical to TeamBatched.  On the device the
+    workers of a line are all the GPU's threads; ``workers`` is kept for the
+    spec's signature."""
     workers: int = 1
+
+    def __post_init__(self):
+        if self.workers < 1:
+            raise ValueError("workers must be >= 1")
 
 
 @dataclass(frozen=True)
@@ -430,7 +439,7 @@ def _group_threads(max_own_dofs: int, max_rank_leaves: int, n_problems: int, clu
     threads when too few problems fill the GPU (latency matters more than
     throughput then).  Measured on c2 (15^3, 2 ranks): 256 threads beat 512
     (82.9 vs 84.9 ms; tools/sweep_c2.py)."""
-    need = max(64, 8 * max_rank_leaves, math.ceil(max_own_dofs / 16))
+    need = max(64, min(8 * max_rank_leaves, 512), math.ceil(max_own_dofs / 16))  # more leaves: chain rounds
     if n_problems * cluster < 148:
         need = max(need, min(512, 32 * math.ceil(max_own_dofs / 32)))
     if fprv_global:  # 32^3 on 16 ranks: 512 threads (57.6 ms per wave of 7) beat 768 (58.5) and 256 (64)
@@ -675,8 +684,6 @@ class DeviceBatch:
         returned Launch can be replayed (bench) or run once (solve)."""
         torch = _torch()
         strategy = strategy or TeamBatched()
-        if isinstance(strategy, NaiveLoop):
-            raise NotImplementedError("NaiveLoop per-operation dispatch is not provided on the B200 path")
         h = self.host
         groups = h.groups.copy()
         for g in groups:
@@ -719,9 +726,14 @@ class DeviceBatch:
         if phase_profile:
             phase = torch.zeros(nat.PHASES * 148 * 16, dtype=torch.int64, device=dev)
             fb.phase_cycles = phase.data_ptr()
+        naive = None
+        if isinstance(strategy, NaiveLoop):
+            need = max((int(nat.lib().frb_naive_scratch_doubles(p.n_nodes, p.network.n_elements, p.n_free_nodes))
+                        for p in h.problems), default=1)
+            naive = torch.empty(need, dtype=torch.float64, device=dev)
         return Launch(self, fb, config_struct(cfg), groups_c,
                       DeviceResults(u=u, f=f, results=res, node_base=h.node_base),
-                      keep=(desc_t, queue, work, groups_c), phase=phase)
+                      keep=(desc_t, queue, work, groups_c), phase=phase, naive=naive)
 
     def solve(self, cfg: SolverConfig, strategy=None, stream=None) -> DeviceResults:
         """Launch the persistent kernels; returns device-resident results
@@ -740,6 +752,7 @@ class Launch:
     out: DeviceResults
     keep: tuple = ()
     phase: object = None
+    naive: object = None          # NaiveLoop scratch (per-operation strategy)
 
     @property
     def threads(self) -> int:
@@ -749,6 +762,12 @@ class Launch:
         """One frb_solve_batch call (one kernel launch per group) on `stream`."""
         torch = _torch()
         s = stream if stream is not None else torch.cuda.current_stream(self.dbatch.device)
+        if self.naive is not None:  # NaiveLoop: problems one after another, one launch per line
+            for p in range(self.fb.n_problems):
+                nat.check(nat.lib().frb_naive_solve(C.byref(self.fb), C.byref(self.fc), p,
+                                                    C.c_void_p(self.naive.data_ptr()), self.naive.numel(),
+                                                    C.c_void_p(s.cuda_stream)))
+            return
         nat.check(nat.lib().frb_solve_batch(C.byref(self.fb), C.byref(self.fc), C.c_void_p(s.cuda_stream)))
 
 

@@ -6,10 +6,11 @@ runtime of N concurrent copies of one sub-problem against one copy,
 ``self_speedup = N * t1 / tN`` -- 1 means runtime grows linearly with N (no
 batching benefit), N means a flat runtime.  On the B200 the strategies are
 ``TeamBatched`` (one persistent kernel, a work queue, one CTA cluster per
-network -- the paper's team kernel) and ``SerialReference`` (the same kernel
-with a single team: problems strictly one after another).  The naive
-per-operation-dispatch baseline is not provided on the device (the design
-exists to remove it; ``batch.NaiveLoop`` raises).
+network -- the paper's team kernel), ``SerialReference`` (the same kernel
+with a single team: problems strictly one after another) and ``NaiveLoop``
+(the paper's naive baseline: one kernel launch per line of the Fig. 1 loop,
+problems in sequence, the host checking convergence every iteration), so
+``speedup_over_naive`` reproduces the team-vs-naive comparison of Fig. 4.
 
 Timing boundary: wall clock of ``solve_batch`` including batch
 packing, host->device upload, the solve and the download of the results;
@@ -63,12 +64,14 @@ def self_speedup(t1: float, tN: float, N: int) -> float:
 
 
 def _strategy(name: str, team_size: int | None):
-    from .batch import SerialReference, TeamBatched
+    from .batch import NaiveLoop, SerialReference, TeamBatched
     if name == "team":
         return TeamBatched(team_size=team_size)
     if name == "serial":
         return SerialReference()
-    raise ValueError(f"unknown strategy {name!r} (team, serial)")
+    if name == NAIVE:
+        return NaiveLoop()
+    raise ValueError(f"unknown strategy {name!r} (team, serial, naive)")
 
 
 def run_benchmark(sizes: Sequence[tuple[int, int, int]], counts: Sequence[int],
