@@ -104,26 +104,42 @@ class Partition:
     ranks: list
 
 
+LEAVES_PER_ROUND = 64   # chain sums of 64 leaves take one round of a 512-thread CTA
+
+
 def cut_points(plan: np.ndarray, nf: int, C: int) -> list[int]:
     """DOF cut offsets (0 = c_0 < ... < c_C = nf) at leaf starts that are
-    multiples of 3; fewer ranks when the plan has too few such starts."""
+    multiples of 3 (node- and leaf-aligned), chosen to minimise the largest
+    rank -- the one every other rank waits for at the tree exchange: the most
+    own DOFs, and ranks of more than LEAVES_PER_ROUND leaves (an extra chain
+    round) only when unavoidable.  Exact min-max over the candidate cuts by
+    dynamic programming; fewer ranks when the plan has too few candidates."""
     p = PlanView(plan)
-    starts = [int(s) for s in p.leaf_start]
-    cand = sorted({s for s in starts if s % 3 == 0 and 0 < s < nf})
-    cuts = [0]
-    for r in range(1, C):
-        target = nf * r / C
-        best = None
-        for s in cand:
-            if s <= cuts[-1]:
-                continue
-            if best is None or abs(s - target) < abs(best - target):
-                best = s
-        if best is None:
-            break
-        cuts.append(best)
-    cuts.append(nf)
-    return cuts
+    starts = np.asarray(p.leaf_start, dtype=np.int64)
+    if nf == 0 or C <= 1 or len(starts) == 0:
+        return [0, nf]
+    ok = (starts % 3 == 0) & (starts > 0) & (starts < nf)
+    pos = np.r_[0, starts[ok], nf]                       # candidate cut DOFs
+    leaf = np.r_[0, np.flatnonzero(ok), len(starts)]     # first leaf after each cut
+    K = len(pos)
+    C = min(C, K - 1)
+    big = float(nf + 1)
+    # cost[i, j] of a rank spanning candidates i < j
+    span = pos[None, :] - pos[:, None]
+    nleaf = leaf[None, :] - leaf[:, None]
+    cost = np.where(span > 0, span + big * (nleaf > LEAVES_PER_ROUND), np.inf).astype(np.float64)
+    best = cost[0].copy()                                 # one rank covering [0, pos[j])
+    back = [np.zeros(K, dtype=np.int64)]
+    for _ in range(1, C):
+        cand = np.maximum(best[:, None], cost)           # previous ranks end at i, the next spans i..j
+        arg = np.argmin(cand, axis=0)
+        best = cand[arg, np.arange(K)]
+        back.append(arg)
+    cuts = [K - 1]
+    for k in range(C - 1, 0, -1):
+        cuts.append(int(back[k][cuts[-1]]))
+    cuts.append(0)
+    return [int(pos[i]) for i in reversed(cuts)]
 
 
 def partition(n_nodes: int, n_free: int, ia: np.ndarray, ib: np.ndarray, ell_other: np.ndarray,
