@@ -856,48 +856,30 @@ __device__ __forceinline__ Layout layout(const Rank& R) {
 }
 
 // Replay one combine program (plan.py _program: warp rounds of up to 32
-// independent lane ops, each folding up to two tree levels -- s[dst] =
-// (s[a] (+ s[b])) + (s[c] (+ s[d])) --, slot indices premultiplied by 3, idle
-// lanes folding their own scratch slots, one idle pad round) on
-// g_smem[o_slot + ...] with the calling warp: no branch in the loop, the
-// next round's words are fetched while the current one runs.  Not unrolled:
-// a single warp runs it while the rest of the CTA waits, so its code must
-// stay small.
+// independent ops, lane-packed, slot indices premultiplied by 3, idle lanes
+// folding their own scratch slots, one idle pad round) on g_smem[o_slot + ...] with
+// the calling warp: no branch in the loop, the next round's op is fetched
+// while the current one runs.  Not unrolled: a single warp runs it while
+// the rest of the CTA waits, so its code must stay small.
 __device__ __forceinline__ void run_prog(const int* prog, int o_slot, int lane) {
   const int nr = prog[0];
-  const int2* w = reinterpret_cast<const int2*>(prog + 2) + 2 * lane;  // 8-byte aligned (plan.py _program)
+  const int2* w = reinterpret_cast<const int2*>(prog + 2) + lane;  // 8-byte aligned (plan.py _program)
   double* const sl = &g_smem[o_slot];
-  int2 c0 = w[0], c1 = w[1];
+  int2 cur = w[0];
 #pragma unroll 1
   for (int r = 0; r < nr; ++r) {
-    w += 64;
-    const int2 n0 = w[0], n1 = w[1];
-    const bool il = (c0.x >> 16) & 1, ir = (c0.x >> 17) & 1;
-    const double* pa = sl + (c0.y & 0xffff);
-    const double* pb = sl + (c0.y >> 16);
-    const double* pc = sl + (c1.x & 0xffff);
-    const double* pd = sl + (c1.x >> 16);
-    double l0 = pa[0], l1 = pa[1], l2 = pa[2];
-    double r0 = pc[0], r1 = pc[1], r2 = pc[2];
+    w += 32;
+    const int2 nxt = w[0];
+    const double* pa = sl + (cur.y & 0xffff);
+    const double* pb = sl + (cur.y >> 16);
+    const double a0 = pa[0], a1 = pa[1], a2 = pa[2];
     const double b0 = pb[0], b1 = pb[1], b2 = pb[2];
-    const double d0 = pd[0], d1 = pd[1], d2 = pd[2];
-    if (il) {
-      l0 = dadd(l0, b0);
-      l1 = dadd(l1, b1);
-      l2 = dadd(l2, b2);
-    }
-    if (ir) {
-      r0 = dadd(r0, d0);
-      r1 = dadd(r1, d1);
-      r2 = dadd(r2, d2);
-    }
-    double* pdst = sl + (c0.x & 0xffff);
-    pdst[0] = dadd(l0, r0);
-    pdst[1] = dadd(l1, r1);
-    pdst[2] = dadd(l2, r2);
+    double* pd = sl + cur.x;
+    pd[0] = dadd(a0, b0);
+    pd[1] = dadd(a1, b1);
+    pd[2] = dadd(a2, b2);
     __syncwarp();
-    c0 = n0;
-    c1 = n1;
+    cur = nxt;
   }
 }
 

@@ -146,71 +146,31 @@ TREE_HEADER = 10
 PROG_LANES = 32
 
 
-PROG_WORDS = 4   # words per lane and round
-
-
-def _program(ops: list[tuple[int, int, int, int]], scratch: int, keep=()) -> np.ndarray:
-    """Combine program as warp rounds: [n_rounds, 0, (n_rounds + 1) x 32 x 4
-    words] (the extra idle round lets the device prefetch the next round
-    unconditionally).  Ops are (height, dst, left, right) with heights
-    counted inside the program; ops of one height are independent.
-
-    Two tree levels per round: an op at an even height 2k+2 whose child is an
-    op of height 2k+1 computes that child inline (left = s[a] + s[b]) instead
-    of reading it, so the child is not emitted -- unless it must be stored
-    (`keep`: the program's outputs, e.g. exported roots; a tree node has one
-    parent, so nothing else reads it).  Per lane the words are
-        (3 dst | inline_left << 16 | inline_right << 17,
-         3 a | 3 b << 16,  3 c | 3 d << 16,  0)
-    meaning s[dst] = (inline_left ? s[a] + s[b] : s[a]) +
-                     (inline_right ? s[c] + s[d] : s[c]),
-    slot indices premultiplied by the 3 components.  The additions and their
-    order are exactly the tree's, only fewer rounds separate them.  Idle
+def _program(ops: list[tuple[int, int, int, int]], scratch: int) -> np.ndarray:
+    """Combine program as warp rounds: [n_rounds, 0, (n_rounds + 1) x 32 x 2
+    words] (the pad keeps the word pairs 8-byte aligned on the device; the
+    extra idle round lets the device prefetch the next round unconditionally).
+    Ops (height, dst, left, right) of one height are independent; each round
+    holds up to 32 of them, one per lane, as the pair (3 dst, 3 left |
+    3 right << 16) -- slot indices premultiplied by the 3 components.  Idle
     lane l combines its own scratch slot `scratch + l` into itself, so the
-    device loop has no branch and no two lanes touch the same slot."""
-    keep = set(keep)
+    device loop has no branch and no two lanes touch the same slot.  Rounds
+    run in order with a __syncwarp between them."""
+    ops = sorted(ops, key=lambda o: o[0])
     assert 3 * (scratch + PROG_LANES - 1) < (1 << 16), "tree slot index exceeds 16 bits / 3"
-    by_dst = {d: (h, a, b) for h, d, a, b in ops}
-
-    def idle_words(lane):
-        x = 3 * (scratch + lane)
-        return [x, x | (x << 16), x | (x << 16), 0]
-
-    def word(d, left, right):
-        il, ir = isinstance(left, tuple), isinstance(right, tuple)
-        a, b = left if il else (left, 0)
-        c, e = right if ir else (right, 0)
-        assert 3 * max(d, a, b, c, e) < (1 << 16), "tree slot index exceeds 16 bits / 3"
-        return [3 * d | (int(il) << 16) | (int(ir) << 17), 3 * a | (3 * b << 16), 3 * c | (3 * e << 16), 0]
-
-    H = max((h for h, _, _, _ in ops), default=0)
-    absorbed = set()
-    macro_levels = []
-    for k in range(0, H, 2):
-        lo, hi = k + 1, k + 2
-        level = []
-        for h, d, a, b in sorted(o for o in ops if o[0] == hi):
-            left = a
-            right = b
-            if a in by_dst and by_dst[a][0] == lo and a not in keep:
-                left = (by_dst[a][1], by_dst[a][2])
-                absorbed.add(a)
-            if b in by_dst and by_dst[b][0] == lo and b not in keep:
-                right = (by_dst[b][1], by_dst[b][2])
-                absorbed.add(b)
-            level.append(word(d, left, right))
-        for h, d, a, b in sorted(o for o in ops if o[0] == lo):
-            if d not in absorbed:
-                level.append(word(d, a, b))
-        macro_levels.append(level)
+    idle = [w for lane in range(PROG_LANES)
+            for w in (3 * (scratch + lane), 3 * (scratch + lane) | (3 * (scratch + lane) << 16))]
     rounds = []
-    for level in macro_levels:
+    for h in sorted({o[0] for o in ops}):
+        level = [o for o in ops if o[0] == h]
         for i in range(0, len(level), PROG_LANES):
-            words = [w for lane in range(PROG_LANES) for w in idle_words(lane)]
-            for lane, wd in enumerate(level[i:i + PROG_LANES]):
-                words[PROG_WORDS * lane:PROG_WORDS * (lane + 1)] = wd
+            words = list(idle)
+            for lane, (_, d, a, b) in enumerate(level[i:i + PROG_LANES]):
+                assert 3 * max(d, a, b) < (1 << 16), "tree slot index exceeds 16 bits / 3"
+                words[2 * lane] = 3 * d
+                words[2 * lane + 1] = 3 * a | (3 * b << 16)
             rounds.append(words)
-    rounds.append([w for lane in range(PROG_LANES) for w in idle_words(lane)])
+    rounds.append(list(idle))
     return np.array([len(rounds) - 1, 0] + [w for r in rounds for w in r], dtype=np.int32)
 
 
@@ -218,22 +178,14 @@ MODE_QUAD = 4   # the rank's leaves fold in aligned quads inside the chain warps
 
 
 def run_program(prog: np.ndarray, slots: list) -> None:
-    """Host replay of a _program exactly as the device runs it (test helper)."""
+    """Host replay of a _program (test helper)."""
     n = int(prog[0])
-    step = PROG_WORDS * PROG_LANES
     for r in range(n):
-        words = prog[2 + step * r:2 + step * (r + 1)]
+        words = prog[2 + 2 * PROG_LANES * r:2 + 2 * PROG_LANES * (r + 1)]
         new = {}
         for lane in range(PROG_LANES):
-            w0, w1, w2 = (int(x) for x in words[PROG_WORDS * lane:PROG_WORDS * lane + 3])
-            d = (w0 & 0xffff) // 3
-            left = slots[(w1 & 0xffff) // 3]
-            if w0 & (1 << 16):
-                left = left + slots[(w1 >> 16) // 3]
-            right = slots[(w2 & 0xffff) // 3]
-            if w0 & (1 << 17):
-                right = right + slots[(w2 >> 16) // 3]
-            new[d] = left + right
+            d, w = int(words[2 * lane]), int(words[2 * lane + 1])
+            new[d // 3] = slots[(w & 0xffff) // 3] + slots[(w >> 16) // 3]
         for d, v in new.items():
             slots[d] = v
 
@@ -302,7 +254,7 @@ def tree_split(flat: np.ndarray, ranges: list[tuple[int, int]]) -> list[np.ndarr
         top_ops.append((h, int(top_of[d]), int(top_of[a]), int(top_of[b])))
     TS = E + len(top_internal) + PROG_LANES   # + a scratch slot per lane for idle lanes
     root_top = int(top_of[p.root])
-    tprog = _program(top_ops, TS - PROG_LANES, keep={root_top})
+    tprog = _program(top_ops, TS - PROG_LANES)
     blocks = []
     children = {int(p.op_dst[k]): (int(p.op_left[k]), int(p.op_right[k])) for k in range(K)}
     pending = []
@@ -353,7 +305,7 @@ def tree_split(flat: np.ndarray, ranges: list[tuple[int, int]]) -> list[np.ndarr
         pending.append((nl, lops, exp, mode))
     LS = max(nl for nl, _, _, _ in pending) + PROG_LANES   # + a scratch slot per lane for idle lanes
     for nl, lops, exp, mode in pending:
-        lprog = _program(lops, LS - PROG_LANES, keep=set(int(x) for x in exp[0::2]))
+        lprog = _program(lops, LS - PROG_LANES)
         lprog_off = TREE_HEADER
         tprog_off = lprog_off + len(lprog)
         exp_off = tprog_off + len(tprog)
