@@ -425,35 +425,10 @@ __device__ __forceinline__ bool element_coefs(int T, int first, int n_act, const
   bool bad = false;
   if (first >= n_act) return bad;
   const int last = n_act - 1;
-#ifdef FRB_F1_PIPE
-  // software pipeline: the next group's table words load while this group
-  // computes (the tables of the largest networks stream from L2)
-  uint32_t ab_n[kElem];
-  double L_n[kElem], EA_n[kElem];
-#pragma unroll
-  for (int q = 0; q < kElem; ++q) {
-    const int e = min(first + static_cast<int>(threadIdx.x) + q * T, last);
-    ab_n[q] = __ldg(act_ab + e);
-    L_n[q] = __ldg(act_L + e);
-    EA_n[q] = act_EA ? __ldg(act_EA + e) : ea;
-  }
-#endif
   for (int e0 = first + threadIdx.x; e0 < n_act; e0 += kElem * T) {
     uint32_t ab[kElem];
     double L[kElem], EA[kElem], l[kElem], cf[kElem];
     bool ok[kElem];
-#ifdef FRB_F1_PIPE
-#pragma unroll
-    for (int q = 0; q < kElem; ++q) {
-      ab[q] = ab_n[q];
-      L[q] = L_n[q];
-      EA[q] = EA_n[q];
-      const int e = min(e0 + kElem * T + q * T, last);
-      ab_n[q] = __ldg(act_ab + e);
-      L_n[q] = __ldg(act_L + e);
-      EA_n[q] = act_EA ? __ldg(act_EA + e) : ea;
-    }
-#else
 #pragma unroll
     for (int q = 0; q < kElem; ++q) {  // table loads of the whole group first
       const int e = min(e0 + q * T, last);
@@ -461,7 +436,6 @@ __device__ __forceinline__ bool element_coefs(int T, int first, int n_act, const
       L[q] = __ldg(act_L + e);
       EA[q] = act_EA ? __ldg(act_EA + e) : ea;
     }
-#endif
 #pragma unroll
     for (int q = 0; q < kElem; ++q) {  // independent chains: the scheduler interleaves them
       const double* pa = &g_smem[o_pos + 3 * static_cast<int>(ab[q] & 0xffffu)];
@@ -992,7 +966,8 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
     nt = lsize - 8 * q;
   }
 
-  // reference coordinates of the own DOFs stay in registers
+  // reference coordinates of the own DOFs stay in registers (re-reading
+  // them from global memory in U measured slower: C3 wave 63.3 vs 58.9 ms)
   double xr[MAXK];
 #pragma unroll
   for (int k = 0; k < MAXK; ++k) xr[k] = __ldg(Xg + dof0 + min(t + k * T, dl_max));
