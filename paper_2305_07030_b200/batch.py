@@ -442,8 +442,8 @@ def _group_threads(max_own_dofs: int, max_rank_leaves: int, n_problems: int, clu
     need = max(64, min(8 * max_rank_leaves, 512), math.ceil(max_own_dofs / 16))  # more leaves: chain rounds
     if n_problems * cluster < 148:
         need = max(need, min(512, 32 * math.ceil(max_own_dofs / 32)))
-    if fprv_global:  # 32^3 on 16 ranks: 512 threads (57.6 ms per wave of 7) beat 768 (58.5) and 256 (64)
-        need = max(need, int(os.environ.get("FRB_FG_THREADS", "512")))
+    if fprv_global:  # 32^3 on 16 ranks: 768 threads 144.3 networks/s, 512 143.4, 256 ~20 % slower
+        need = max(need, int(os.environ.get("FRB_FG_THREADS", "768")))
     threads = min(MAX_CTA_THREADS, 32 * math.ceil(need / 32))
     while max_own_dofs > dofs_per_thread_cap(threads, fprv_global) * threads and threads < MAX_CTA_THREADS:
         threads += 32

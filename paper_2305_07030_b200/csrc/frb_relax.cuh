@@ -952,19 +952,11 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
 #pragma unroll
   for (int k = 0; k < MAXK; ++k) u[k] = v[k] = 0.0;
 
-  // pairwise-chain role: thread t < 8 * own leaves sums chain j of leaf
-  // leaf0 + t/8; DOF offsets are relative to the rank's first DOF
-  const bool chain = t < 8 * R.n_leaves;
-  const int lloc = t >> 3, j = t & 7;
-  int lstart = 0, q = 0, nt = 0;
-  if (chain) {
-    const int* leaf_start = n.plan + 4;
-    const int* leaf_size = leaf_start + L;
-    lstart = leaf_start[R.leaf0 + lloc] - dof0;
-    const int lsize = leaf_size[R.leaf0 + lloc];
-    q = lsize >= 8 ? (lsize >> 3) : 0;
-    nt = lsize - 8 * q;
-  }
+  // pairwise-chain role: in chain round k thread t sums chain j = t % 8 of
+  // own leaf t / 8 + k T / 8; the leaves' (start, size) come from the tree
+  // block in shared memory each round (no per-problem registers)
+  const int j = t & 7;
+  const int2* const leaf_tab = reinterpret_cast<const int2*>(prog + R.tree[10]);
 
   // reference coordinates of the own DOFs stay in registers (re-reading
   // them from global memory in U measured slower: C3 wave 63.3 vs 58.9 ms)
@@ -1294,16 +1286,15 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
         g_smem[sl + 2] = r2;
       }
     };
-    if ((t & ~31) < 8 * R.n_leaves) chain_round(lloc, chain, lstart, q, nt);  // warp holds a chain
-    for (int l0 = (T >> 3) + ((t & ~31) >> 3); l0 < R.n_leaves; l0 += T >> 3) {  // rare extra rounds
+    for (int l0 = (t & ~31) >> 3; l0 < R.n_leaves; l0 += T >> 3) {  // warps holding a chain; rare extra rounds
       const int ll = l0 + (lane >> 3);
       const bool has = ll < R.n_leaves;
       int ls = 0, qn = 0, ntl = 0;
       if (has) {
-        ls = __ldg(n.plan + 4 + R.leaf0 + ll) - dof0;
-        const int lsize = __ldg(n.plan + 4 + L + R.leaf0 + ll);
-        qn = lsize >= 8 ? (lsize >> 3) : 0;
-        ntl = lsize - 8 * qn;
+        const int2 li = leaf_tab[ll];
+        ls = li.x;
+        qn = li.y >= 8 ? (li.y >> 3) : 0;
+        ntl = li.y - 8 * qn;
       }
       chain_round(ll, has, ls, qn, ntl);
     }

@@ -140,7 +140,7 @@ def evaluate(flat: np.ndarray, a) -> float:
 
 # ---------------------------------------------------------------- cluster split
 
-TREE_HEADER = 10
+TREE_HEADER = 12
 
 
 PROG_LANES = 32
@@ -202,8 +202,9 @@ def tree_split(flat: np.ndarray, ranges: list[tuple[int, int]]) -> list[np.ndarr
     NumPy's throughout; only where each addition happens changes.
 
     Returns one int32 block per rank:
-        [LS, TS, PI, lprog_off, tprog_off, exp_off, n_exp, root_top, E, 0,
-         local program, top program, exports (local slot, top slot) pairs]
+        [LS, TS, PI, lprog_off, tprog_off, exp_off, n_exp, root_top, E, mode, leaf_off, 0,
+         local program, top program, exports (local slot, top slot) pairs,
+         own leaves (start relative to the rank's first DOF, size) pairs]
     LS / PI are maxima over the ranks (uniform SMEM layout), TS = E + #top
     internal nodes, root_top = top slot of the root (-1: empty tree)."""
     p = PlanView(flat)
@@ -215,7 +216,8 @@ def tree_split(flat: np.ndarray, ranges: list[tuple[int, int]]) -> list[np.ndarr
             empty = _program([], 0)
             blocks.append(np.concatenate([
                 np.array([1, 1, TREE_HEADER + 2 * len(empty), TREE_HEADER, TREE_HEADER + len(empty),
-                          TREE_HEADER + 2 * len(empty), 0, -1, 0, 0], dtype=np.int32), empty, empty]))
+                          TREE_HEADER + 2 * len(empty), 0, -1, 0, 0, TREE_HEADER + 2 * len(empty), 0],
+                         dtype=np.int32), empty, empty]))
         return blocks
     n_slots = 2 * L - 1
     lo = np.zeros(n_slots, dtype=np.int64)
@@ -302,16 +304,24 @@ def tree_split(flat: np.ndarray, ranges: list[tuple[int, int]]) -> list[np.ndarr
         exp = np.array([(int(local_idx[sl]), int(top_of[sl])) for sl in exports if owner[sl] == r],
                        dtype=np.int32).reshape(-1)
         mode = MODE_QUAD if quad else 0
-        pending.append((nl, lops, exp, mode))
-    LS = max(nl for nl, _, _, _ in pending) + PROG_LANES   # + a scratch slot per lane for idle lanes
-    for nl, lops, exp, mode in pending:
+        # the chain role of the rank's leaves (C phase): (start - the rank's
+        # first DOF, size), read from shared memory instead of registers
+        ls = np.asarray(p.leaf_start[a:b], dtype=np.int64)
+        leaves = np.stack([ls - (ls[0] if len(ls) else 0), np.asarray(p.leaf_size[a:b], dtype=np.int64)],
+                          axis=1).reshape(-1)
+        pending.append((nl, lops, exp, mode, leaves))
+    LS = max(nl for nl, _, _, _, _ in pending) + PROG_LANES   # + a scratch slot per lane for idle lanes
+    for nl, lops, exp, mode, leaves in pending:
         lprog = _program(lops, LS - PROG_LANES)
         lprog_off = TREE_HEADER
         tprog_off = lprog_off + len(lprog)
         exp_off = tprog_off + len(tprog)
-        hdr = np.array([nl, TS, 0, lprog_off, tprog_off, exp_off, len(exp) // 2, root_top, E, mode],
+        leaf_off = exp_off + len(exp)
+        leaf_off += leaf_off & 1  # 8-byte aligned pairs
+        hdr = np.array([nl, TS, 0, lprog_off, tprog_off, exp_off, len(exp) // 2, root_top, E, mode, leaf_off, 0],
                        dtype=np.int32)
-        blocks.append(np.concatenate([hdr, lprog, tprog, exp]).astype(np.int32))
+        blocks.append(np.concatenate([hdr, lprog, tprog, exp, np.zeros(leaf_off - exp_off - len(exp), np.int32),
+                                      leaves]).astype(np.int32))
     PI = max(len(bk) for bk in blocks)
     for bk in blocks:
         bk[0] = LS
