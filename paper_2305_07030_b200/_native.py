@@ -15,7 +15,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("FRB_LIB") or os.path.join(HERE, "lib", "libfrb200.so")
 
-ABI_VERSION = 8
+ABI_VERSION = 9
 MAX_CLUSTER = 16
 FRB_OK, FRB_E_INVALID, FRB_E_TOO_LARGE, FRB_E_CUDA, FRB_E_UNSUPPORTED = 0, -1, -2, -3, -4
 STATUS_CONVERGED, STATUS_MAX_ITERS, STATUS_SINGULAR = 0, 1, 2
@@ -40,7 +40,7 @@ class FrbConfig(C.Structure):
 BATCH_POINTERS = ("groups", "problems", "parts", "order", "X", "node_mass", "inc_node", "inc",
                   "elem_ab", "elem_L", "elem_EA", "plans", "ell", "act_ab", "act_L",
                   "act_EA", "halo_g", "runs", "fix_g", "trees", "u", "f", "work", "results", "queue",
-                  "phase_cycles")
+                  "xchg", "phase_cycles")
 
 
 class FrbBatch(C.Structure):
@@ -67,9 +67,11 @@ PART_DTYPE = np.dtype([
 GROUP_DTYPE = np.dtype([
     ("cluster", "<i4"), ("first", "<i4"), ("count", "<i4"), ("block_threads", "<i4"),
     ("smem_bytes", "<i4"), ("max_own_dofs", "<i4"), ("grid_clusters", "<i4"), ("fprv_global", "<i4"),
-    ("max_rank_leaves", "<i4"), ("flags", "<i4"),
+    ("max_rank_leaves", "<i4"), ("flags", "<i4"), ("xchg_off", "<i8"), ("gm_cap", "<i4"),
+    ("gm_ex_stride", "<i4"), ("gm_mir_stride", "<i4"), ("pad", "<i4"),
 ])
 GF_SERIAL = 1
+GF_NO_VIRTUAL = 2
 SETUP_ITEM_DTYPE = np.dtype([
     ("coords", "<u8"), ("elements", "<u8"), ("materials", "<u8"), ("node_order", "<u8"), ("act_elem", "<u8"),
     ("X_out", "<u8"), ("mass_out", "<u8"), ("L_out", "<u8"), ("EA_out", "<u8"), ("act_L_out", "<u8"),
@@ -82,7 +84,7 @@ RESULT_DTYPE = np.dtype([
     ("avg_stress", "<f8", (9,)), ("energy", "<f8", (4,)),
 ])
 assert PROBLEM_DTYPE.itemsize == 184 and PART_DTYPE.itemsize == 120
-assert SETUP_ITEM_DTYPE.itemsize == 144 and GROUP_DTYPE.itemsize == 40 and RESULT_DTYPE.itemsize == 144
+assert SETUP_ITEM_DTYPE.itemsize == 144 and GROUP_DTYPE.itemsize == 64 and RESULT_DTYPE.itemsize == 144
 
 
 class NativeError(RuntimeError):

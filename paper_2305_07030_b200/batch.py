@@ -60,6 +60,11 @@ SMEM_BUDGET = 227 * 1024 - 4 * 1024
 # from 3400 to 8000 (profiles/r01_configs.md), because large clusters cost
 # SMs (a 16-CTA cluster fills a GPC) and exchange latency.
 DOFS_PER_RANK = int(os.environ.get("FRB_DOFS_PER_RANK", "8000"))
+# virtual clusters per launch group (frb200.h frb_group.gm_cap): groups of C
+# plain CTAs exchanging through L2 on the SMs that hardware clusters of 8 or
+# 16 CTAs leave idle (16-CTA clusters: 7 fit, 36 of 148 SMs idle -> 2 more).
+# FRB_VIRTUAL=0 turns them off.
+VIRTUAL_CAP = 4 if os.environ.get("FRB_VIRTUAL", "1") != "0" else 0
 
 
 def dofs_per_thread_cap(threads: int, fprv_global: bool = False) -> int:
@@ -603,6 +608,12 @@ def _pack(networks, bcs, probs, cluster: int | None = None) -> Batch:
         g["smem_bytes"], g["max_own_dofs"] = smem, own
         g["fprv_global"] = int(fglob)
         g["max_rank_leaves"] = leaves
+        if C >= 8:  # virtual clusters may run on the SMs these clusters leave idle (frb200.h frb_group)
+            pn = max(rt.n_local + rt.n_fix for i in ids for rt in part_of[i].ranks)
+            ts = max(int(rt.tree[1]) for i in ids for rt in part_of[i].ranks)
+            g["gm_cap"] = VIRTUAL_CAP
+            g["gm_ex_stride"] = 4 * math.ceil((3 * ts + 64) / 4)
+            g["gm_mir_stride"] = 2 * (2 * math.ceil(3 * pn / 2))
         groups.append(g)
         order.extend(ids)
     arrays = dict(
@@ -700,8 +711,17 @@ class DeviceBatch:
                 raise nat.NativeError(nat.FRB_E_TOO_LARGE,
                                       f"team_size {T} cannot hold {int(g['max_own_dofs'])} own DOFs")
 
+        # exchange scratch of the virtual clusters, one slice per eligible group
+        xoff = 0
+        for g in groups:
+            if int(g["gm_cap"]) > 0:
+                cap, C = int(g["gm_cap"]), int(g["cluster"])
+                g["xchg_off"] = xoff
+                xoff += 128 * cap + 8 * (cap * 2 * int(g["gm_ex_stride"]) + cap * C * int(g["gm_mir_stride"]))
+                xoff = 256 * math.ceil(xoff / 256)
         n = int(h.node_base[-1])
         dev = self.device
+        xchg = torch.empty(max(xoff, 1), dtype=torch.uint8, device=dev) if xoff else None
         u = torch.empty(3 * n, dtype=torch.float64, device=dev)
         f = torch.empty(3 * n, dtype=torch.float64, device=dev)
         work = torch.empty(3 * n + 1, dtype=torch.float64, device=dev)
@@ -722,6 +742,7 @@ class DeviceBatch:
         fb.problems = desc_t.data_ptr()
         fb.u, fb.f, fb.work = u.data_ptr(), f.data_ptr(), work.data_ptr()
         fb.results, fb.queue = res.data_ptr(), queue.data_ptr()
+        fb.xchg = xchg.data_ptr() if xchg is not None else None
         phase = None
         if phase_profile:
             phase = torch.zeros(nat.PHASES * 148 * 16, dtype=torch.int64, device=dev)
@@ -733,7 +754,7 @@ class DeviceBatch:
             naive = torch.empty(need, dtype=torch.float64, device=dev)
         return Launch(self, fb, config_struct(cfg), groups_c,
                       DeviceResults(u=u, f=f, results=res, node_base=h.node_base),
-                      keep=(desc_t, queue, work, groups_c), phase=phase, naive=naive)
+                      keep=(desc_t, queue, work, groups_c, xchg), phase=phase, naive=naive)
 
     def solve(self, cfg: SolverConfig, strategy=None, stream=None) -> DeviceResults:
         """Launch the persistent kernels; returns device-resident results

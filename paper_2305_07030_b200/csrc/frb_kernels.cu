@@ -95,8 +95,12 @@ int frb_max_dofs_per_thread(int block_threads, int fprv_global) { return dofs_ca
 namespace {
 
 // One launch group on stream s (validated, dispatched to its instantiation).
-int launch_one(const frb_batch* batch, const frb_config* cfg, int gi, int optin, cudaStream_t s) {
-  const frb_group& g = batch->groups[gi];
+// alone: the group has the GPU to itself, so its virtual clusters (which
+// need all their CTAs resident at once) can count on the SMs its hardware
+// clusters leave idle; groups running concurrently never use them.
+int launch_one(const frb_batch* batch, const frb_config* cfg, int gi, int optin, cudaStream_t s, bool alone) {
+  frb_group g = batch->groups[gi];
+  if (!alone) g.flags |= FRB_GF_NO_VIRTUAL;
   int rc = FRB_OK;
   if (g.cluster < 1 || g.cluster > FRB_MAX_CLUSTER) return set_err(FRB_E_INVALID, "cluster size out of range");
   if (g.block_threads < 32 || g.block_threads > kMaxThreads || g.block_threads % 32)
@@ -148,7 +152,7 @@ int frb_solve_batch(const frb_batch* batch, const frb_config* cfg, void* stream)
   }
   if (n_live <= 1 || serial) {
     for (int gi = 0; gi < batch->n_groups; ++gi)
-      if (batch->groups[gi].count > 0 && (rc = launch_one(batch, cfg, gi, optin, s))) return rc;
+      if (batch->groups[gi].count > 0 && (rc = launch_one(batch, cfg, gi, optin, s, n_live <= 1))) return rc;
     return FRB_OK;
   }
   // Several cluster sizes (heterogeneous batch): the groups run concurrently
@@ -165,7 +169,7 @@ int frb_solve_batch(const frb_batch* batch, const frb_config* cfg, void* stream)
     rc = cuda_check(cudaStreamCreateWithFlags(&gs, cudaStreamNonBlocking), "cudaStreamCreate");
     if (rc) break;
     rc = cuda_check(cudaStreamWaitEvent(gs, fork, 0), "cudaStreamWaitEvent");
-    if (!rc) rc = launch_one(batch, cfg, gi, optin, gs);
+    if (!rc) rc = launch_one(batch, cfg, gi, optin, gs, false);
     if (!rc) rc = cuda_check(cudaEventCreateWithFlags(&join, cudaEventDisableTiming), "cudaEventCreate");
     if (!rc) {
       rc = cuda_check(cudaEventRecord(join, gs), "cudaEventRecord");

@@ -183,6 +183,43 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   } while (!done);
 }
 
+// ------------------------------------------------------------------ global-memory exchange
+//
+// Virtual clusters (kGM): a 16-CTA cluster must sit inside one GPC, so only
+// 7 of them fit the GPU (112 of 148 SMs).  The remaining SMs run "virtual
+// clusters": C independent CTAs (one per SM, no cluster launch) that solve a
+// network together exchanging through L2 instead of DSMEM, with the same
+// tables, layout and arithmetic.  Each virtual cluster owns a slice of the
+// caller's exchange scratch (frb_batch.xchg, frb_group.xchg_off):
+//   cnt [32] int      [0..15] halo bytes received by rank r, [16] exports
+//                     arrived, [17] barrier arrivals, [18] current problem
+//   ex  [2][ex_stride] top-slot image (3 TS doubles) + 64 flag words, by
+//                     iteration parity
+//   mir [C][2][mir_stride/2] each rank's halo mirror: the bytes peers copy
+//                     into its position array, by iteration parity
+// Counters only grow: every wait is "counter >= the running expected value",
+// so nothing is reset between problems.  Spins are bounded (trap after ~20 s)
+// so a scheduling failure cannot hang the GPU.
+struct Gx {
+  int* cnt;
+  double* ex;
+  double* mir;
+  int ex_stride, mir_stride;
+};
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void gm_spin(const int* p, int target) {
+  const long long t0 = clock64();
+  while (ld_acquire(p) < target) {
+    if (clock64() - t0 > 40000000000LL) __trap();  // ~20 s: a virtual cluster that never assembled
+  }
+}
+
 // ------------------------------------------------------------------ problem views
 
 struct Net {
@@ -558,6 +595,7 @@ struct Scalars {
   double red[kMaxWarps * 9];
   int ired[kMaxWarps];
   int problem, done, converged, singular;
+  int gx_h, gx_s, gx_b;                  // kGM: expected counter values (thread 0)
   uint32_t peer_smem[FRB_MAX_CLUSTER];  // shared::cluster base of each rank's dynamic SMEM
   uint32_t peer_bar_h[FRB_MAX_CLUSTER]; // each rank's halo mbarrier
   uint32_t peer_bar_s[FRB_MAX_CLUSTER]; // each rank's leaf-sum mbarrier
@@ -699,6 +737,25 @@ __device__ __forceinline__ void csync(int C) {
     cg::this_cluster().sync();
   } else {
     __syncthreads();
+  }
+}
+
+// Barrier over the ranks of a problem: cluster barrier, or (virtual
+// cluster) an arrival counter in global memory.
+template <bool kGM>
+__device__ __forceinline__ void gsync(int C, Scalars& sc, const Gx& gx) {
+  if constexpr (kGM) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      atomicAdd(gx.cnt + 17, 1);
+      sc.gx_b += C;
+      gm_spin(gx.cnt + 17, sc.gx_b);
+      __threadfence();
+    }
+    __syncthreads();
+  } else {
+    csync(C);
   }
 }
 
@@ -877,9 +934,10 @@ __device__ __forceinline__ void drain(Mbar& mb, uint32_t halo_bytes, uint32_t le
   mb.ph_s ^= 1u;
 }
 
-template <int MAXK, bool kFG, bool kEnergy, int kT>
+template <int MAXK, bool kFG, bool kEnergy, int kT, bool kGM>
 __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, int rank, Scalars& sc, Mbar& mb,
-                              const Net& n, const Rank& R) {
+                              const Net& n, const Rank& R, const Gx& gx) {
+  static_assert(!(kGM && kEnergy), "the work ledger runs on hardware clusters only");
   // kT > 0: the kernel is launched with exactly kT threads, so every
   // DOF-strided index t + k T folds its stride into immediate offsets
   const int T = kT > 0 ? kT : static_cast<int>(blockDim.x);
@@ -975,6 +1033,7 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
   // before it reuses the own position slots as sq scratch.
   const uint32_t smem_base = smem_u32(g_smem);
   auto issue_halo = [&]() {
+    if constexpr (kGM) return;  // see gm_send_halo
     if (R.n_dst > 0) mbar_expect(mb.a, 8u * static_cast<uint32_t>(R.n_dst));
     for (int i = 0; i < R.n_runs; ++i) {
       const int4 run = __ldg(R.runs + i);
@@ -983,9 +1042,51 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
     }
   };
   auto ack_halo = [&]() {  // thread 0, after the halo wait
+    if constexpr (kGM) return;  // the mirrors are double-buffered: nothing to acknowledge
     for (uint32_t bits = R.ack_from; bits; bits &= bits - 1) {
       const int qr = __ffs(bits) - 1;
       st_async(sc.peer_smem[qr] + 8u * static_cast<uint32_t>(o.flag + 144 + rank), 0.0, sc.peer_bar_a[qr]);
+    }
+  };
+
+  // kGM halo exchange: every thread copies its share of the outgoing runs
+  // into the receivers' mirrors (16-byte stores), then thread 0 publishes the
+  // bytes with a release add on each receiver's counter; a receiver waits
+  // for its running total and copies its halo slots back from its mirror.
+  const int par_h_dummy = 0;
+  (void)par_h_dummy;
+  auto gm_send_halo = [&]() {
+    if constexpr (kGM) {
+      const int par = static_cast<int>(mb.ph_h);
+      for (int i = 0; i < R.n_runs; ++i) {
+        const int4 run = __ldg(R.runs + i);
+        const double2* src = reinterpret_cast<const double2*>(&g_smem[o.pos] + run.y / 8);
+        double2* dst = reinterpret_cast<double2*>(gx.mir + static_cast<int64_t>(run.x) * gx.mir_stride +
+                                                  par * (gx.mir_stride / 2) + run.z / 8);
+        for (int k = t; k < run.w / 16; k += T) dst[k] = src[k];
+      }
+      __syncthreads();
+      if (t == 0) {
+        __threadfence();
+        for (int i = 0; i < R.n_runs; ++i) {
+          const int4 run = __ldg(R.runs + i);
+          atomicAdd(gx.cnt + run.x, run.w);
+        }
+      }
+    }
+  };
+  auto gm_recv_halo = [&]() {
+    if constexpr (kGM) {
+      const int par = static_cast<int>(mb.ph_h);
+      if (t == 0) {
+        sc.gx_h += static_cast<int>(R.halo_bytes);
+        gm_spin(gx.cnt + rank, sc.gx_h);
+        __threadfence();
+      }
+      __syncthreads();
+      const double* src = gx.mir + static_cast<int64_t>(rank) * gx.mir_stride + par * (gx.mir_stride / 2);
+      for (int k = 3 * n_own + t; k < 3 * R.n_local; k += T) g_smem[o.pos + k] = __ldcg(src + k);
+      __syncthreads();
     }
   };
 
@@ -1025,7 +1126,7 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
 
   // ---- prologue: BCs, initial positions (microsolver.py:400-411) ---------
   // post the first halo and leaf-sum phases before any peer may send
-  if (C > 1 && t == 0) {
+  if (!kGM && C > 1 && t == 0) {
     mbar_expect(mb.h, R.halo_bytes);
     mbar_expect(mb.s, leaf_bytes);
   }
@@ -1038,11 +1139,11 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
   // initial free positions to global too (the all-element check reads posg)
   for (int l = t; l < n_own; l += T)
     for (int a = 0; a < 3; ++a) n.posg[3 * (R.node0 + l) + a] = dadd(Xg[3 * (R.node0 + l) + a], 0.0);
-  csync(C);
+  gsync<kGM>(C, sc, gx);
   if (check_elements(n, PosGlobalAll{n.posg}, true)) sc.singular = 1;
   __syncthreads();
   if (sc.singular) {
-    if (C > 1) drain(mb, R.halo_bytes, leaf_bytes);
+    if (!kGM && C > 1) drain(mb, R.halo_bytes, leaf_bytes);
     const int bad = singular_argmin(n, PosGlobalAll{n.posg}, sc);
     if (rank == 0 && t == 0) write_singular(b, p, bad, 0);
     return;
@@ -1063,7 +1164,7 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
       w[1] = dadd(w[1], step);
     }
   }
-  if (eramp) csync(C);  // rank 0 has read the initial positions before any rank drifts
+  if (eramp) csync(C);  // rank 0 has read the initial positions before any rank drifts (ledger: clusters only)
 
   // a = -f/m (:428-430), then iteration 0's kick + drift (:443-448)
   accel(0, T);
@@ -1104,10 +1205,15 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
     // they fly, then wait for the peers' copies, acknowledge them and
     // evaluate the elements cut by the rank boundary.
     if (C > 1 && t == 0) issue_halo();
+    if (C > 1) gm_send_halo();
     bool bad = element_coefs(T, 0, C > 1 ? R.n_int : n_act, act_ab, act_L, act_EA, ea, o.pos, o.cf);
     if (C > 1) {
       mark(sc, prof, PH_F1);
-      mbar_wait(mb.h, mb.ph_h);
+      if constexpr (kGM) {
+        gm_recv_halo();
+      } else {
+        mbar_wait(mb.h, mb.ph_h);
+      }
       mb.ph_h ^= 1u;
       if (t == 0) ack_halo();
       mark(sc, prof, PH_HALO);
@@ -1125,8 +1231,8 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
     // np.maximum(k_hat, 0) (:468-476); sq = (u k_hat) u, sq2 = (u m) u,
     // f f (:489) is formed by C.  Outputs: sq -> own position slot, sq2 -> cf,
     // f stays in fcur and is copied to fprv.
-    if (C > 1 && t == 0) mbar_expect(mb.h, R.halo_bytes);  // next halo phase
-    if (C > 1 && R.n_dst > 0) {  // the peers have read this rank's positions (they become sq below)
+    if (!kGM && C > 1 && t == 0) mbar_expect(mb.h, R.halo_bytes);  // next halo phase
+    if (!kGM && C > 1 && R.n_dst > 0) {  // the peers have read this rank's positions (they become sq below)
       mbar_wait(mb.a, mb.ph_a);
       mb.ph_a ^= 1u;
     }
@@ -1322,8 +1428,18 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
       mark(sc, prof, PH_TLP);
       // every (export, rank) pair on its own lane: the own copy for qr ==
       // rank, three st.async into the peer's top slots otherwise
+      // kGM: each export once into the virtual cluster's top-slot image (the
+      // own copy too: every rank reads the whole image back)
+      double* const gx_ex = kGM ? gx.ex + static_cast<int64_t>(mb.ph_s) * gx.ex_stride : nullptr;
 #pragma unroll 1
-      for (int x = lane; x < n_exp * C; x += 32) {
+      for (int x = lane; x < n_exp * (kGM ? 1 : C); x += 32) {
+        if constexpr (kGM) {
+          const int ls = o.lslot + 3 * exps[2 * x], ts = 3 * exps[2 * x + 1];
+          gx_ex[ts] = g_smem[ls];
+          gx_ex[ts + 1] = g_smem[ls + 1];
+          gx_ex[ts + 2] = g_smem[ls + 2];
+          continue;
+        }
         const int e = x / C, qr = x - e * C;
         const int ls = o.lslot + 3 * exps[2 * e], ts = 3 * exps[2 * e + 1];
         const double v0 = g_smem[ls], v1 = g_smem[ls + 1], v2 = g_smem[ls + 2];
@@ -1348,14 +1464,32 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
           for (int e = 0; e < 3; ++e)
             st_async(sc.peer_smem[0] + 8u * (o_fl + 16 + 3 * rank + e), e3[e], sc.peer_bar_s[0]);
       }
-      if (C > 1) {
+      if (kGM) {  // flag, then publish this rank's exports with a release add
+        if (lane == 0) {
+          gx_ex[3 * R.TS + rank] = sc.singular ? 1.0 : 0.0;
+          __threadfence();
+          atomicAdd(gx.cnt + 16, 1);
+        }
+      } else if (C > 1) {
         if (lane < C && lane != rank)  // this rank's singular flag, lane q -> rank q
           st_async(sc.peer_smem[lane] + 8u * (o_fl + rank), sc.singular ? 1.0 : 0.0, sc.peer_bar_s[lane]);
       }
 #ifndef FRB_NO_SHADOW
       if (T > 32) asm volatile("bar.arrive 1, %0;" : : "r"(T) : "memory");  // exports out: shadow work may start
 #endif
-      if (C > 1) {
+      if constexpr (kGM) {  // every rank's exports: wait for the count, copy the image back
+        if (lane == 0) {
+          sc.gx_s += C;
+          gm_spin(gx.cnt + 16, sc.gx_s);
+          __threadfence();
+        }
+        __syncwarp();
+        const int n_top = 3 * R.tree[8];  // the exported slots of the top array
+        for (int k = lane; k < n_top; k += 32) g_smem[o_ts + k] = __ldcg(gx_ex + k);
+        if (lane < C) g_smem[o_fl + lane] = __ldcg(gx_ex + 3 * R.TS + lane);
+        __syncwarp();
+        mark(sc, prof, PH_TW);
+      } else if (C > 1) {
         mbar_wait(mb.s, mb.ph_s);  // every peer's exports and flag
         if (lane == 0) mbar_expect(mb.s, leaf_bytes);  // next exchange phase
         mark(sc, prof, PH_TW);
@@ -1434,14 +1568,14 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
 #endif
     mark(sc, prof, PH_TT);
     if (sc.singular) {
-      if (C > 1) drain(mb, R.halo_bytes, leaf_bytes);
+      if (!kGM && C > 1) drain(mb, R.halo_bytes, leaf_bytes);
       // positions of every node to global memory, then the argmin over all
       // elements (each rank redundantly; rank 0 reports)
 #pragma unroll
       for (int k = 0; k < MAXK; ++k)
         if (t + k * T < nfo) n.posg[dof0 + t + k * T] = dadd(xr[k], u[k]);
       set_fixed_positions(n, rank, alpha, ramp);
-      csync(C);
+      gsync<kGM>(C, sc, gx);
       const int badi = singular_argmin(n, PosGlobalAll{n.posg}, sc);
       if (rank == 0 && t == 0) write_singular(b, p, badi, it);
       return;
@@ -1474,7 +1608,7 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
     __syncthreads();
     mark(sc, prof, PH_U);
   }
-  if (C > 1) drain(mb, R.halo_bytes, leaf_bytes);
+  if (!kGM && C > 1) drain(mb, R.halo_bytes, leaf_bytes);
   mark(sc, prof, PH_U);
 
   // ---- epilogue: outputs in solver order + stress (:549-564, :285-299) ----
@@ -1506,7 +1640,7 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
       *(C > 1 ? peer(dst, 0) : dst) = e;
     }
   }
-  csync(C);
+  gsync<kGM>(C, sc, gx);
   if (rank == 0 && energy && t == 0) {
     double e = 0.0;
     for (int qr = 0; qr < C; ++qr) e = dadd(e, g_smem[o.flag + 128 + qr]);
@@ -1517,20 +1651,35 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
   mark(sc, prof, PH_EPI);
 }
 
-template <int MAXK, int MAXT, bool kFG, bool kEnergy>
+template <int MAXK, int MAXT, bool kFG, bool kEnergy, bool kGM = false>
 __global__ void __launch_bounds__(MAXT, 1)
     frb_relax_kernel(const __grid_constant__ frb_batch b, const __grid_constant__ frb_config cfg, int first,
-                     int count, int32_t* queue) {
+                     int count, int32_t* queue, const __grid_constant__ frb_group grp) {
   __shared__ Scalars sc;
   __shared__ Net net;
   __shared__ Rank rk;
   __shared__ uint64_t bars[3];
-  const int C = static_cast<int>(cg::this_cluster().num_blocks());
-  const int rank = C > 1 ? static_cast<int>(cg::this_cluster().block_rank()) : 0;
+  // hardware cluster: its size and rank; virtual cluster (kGM): C
+  // consecutive CTAs of a non-cluster launch and their slice of the scratch
+  const int C = kGM ? grp.cluster : static_cast<int>(cg::this_cluster().num_blocks());
+  const int rank = kGM ? static_cast<int>(blockIdx.x) % C : (C > 1 ? static_cast<int>(cg::this_cluster().block_rank()) : 0);
+  Gx gx{nullptr, nullptr, nullptr, 0, 0};
+  if constexpr (kGM) {
+    const int vg = static_cast<int>(blockIdx.x) / C;
+    char* base = reinterpret_cast<char*>(b.xchg) + grp.xchg_off;
+    gx.ex_stride = grp.gm_ex_stride;
+    gx.mir_stride = grp.gm_mir_stride;
+    gx.cnt = reinterpret_cast<int*>(base) + 32 * vg;
+    double* ex0 = reinterpret_cast<double*>(base + 128 * static_cast<int64_t>(grp.gm_cap));
+    gx.ex = ex0 + static_cast<int64_t>(vg) * 2 * gx.ex_stride;
+    gx.mir = ex0 + static_cast<int64_t>(grp.gm_cap) * 2 * gx.ex_stride +
+             static_cast<int64_t>(vg) * C * gx.mir_stride;
+  }
   if (threadIdx.x == 0) {
     for (int k = 0; k < kPhases; ++k) sc.clk[k] = 0;
     sc.t_last = clock64();
-    if (C > 1) {
+    sc.gx_h = sc.gx_s = sc.gx_b = 0;
+    if (!kGM && C > 1) {
       mbar_init(&bars[0], 1);
       mbar_init(&bars[1], 1);
       mbar_init(&bars[2], 1);
@@ -1544,13 +1693,21 @@ __global__ void __launch_bounds__(MAXT, 1)
     }
   }
   Mbar mb{&bars[0], &bars[1], &bars[2], 0u, 0u, 0u};
-  csync(C);  // barriers initialised cluster-wide before any remote use
+  gsync<kGM>(C, sc, gx);  // barriers initialised cluster-wide before any remote use
   for (;;) {
     if (rank == 0 && threadIdx.x == 0) {
       const int idx = atomicAdd(queue, 1);
-      for (int q = 0; q < C; ++q) *(C > 1 ? peer(&sc.problem, q) : &sc.problem) = idx;
+      if constexpr (kGM) {
+        gx.cnt[18] = idx;  // published by the barrier's release
+      } else {
+        for (int q = 0; q < C; ++q) *(C > 1 ? peer(&sc.problem, q) : &sc.problem) = idx;
+      }
     }
-    csync(C);
+    gsync<kGM>(C, sc, gx);
+    if constexpr (kGM) {
+      if (threadIdx.x == 0) sc.problem = ld_acquire(gx.cnt + 18);
+      __syncthreads();
+    }
     const int idx = sc.problem;
     if (idx >= count) break;
     const int p = b.order[first + idx];
@@ -1562,8 +1719,8 @@ __global__ void __launch_bounds__(MAXT, 1)
       sc.threshold = __longlong_as_double(0x7ff0000000000000ULL);  // +inf until set
     }
     __syncthreads();
-    solve_problem<MAXK, kFG, kEnergy, kEnergy ? 0 : MAXT>(b, cfg, p, rank, sc, mb, net, rk);
-    csync(C);  // no rank reuses its SMEM before every peer is done with it
+    solve_problem<MAXK, kFG, kEnergy, kEnergy ? 0 : MAXT, kGM>(b, cfg, p, rank, sc, mb, net, rk, gx);
+    gsync<kGM>(C, sc, gx);  // no rank reuses its SMEM (or the problem slot) before every peer is done with it
   }
   if (b.phase_cycles && threadIdx.x == 0) {
     for (int k = 0; k < kPhases; ++k) b.phase_cycles[kPhases * blockIdx.x + k] = sc.clk[k];
@@ -1586,31 +1743,35 @@ int cuda_check(cudaError_t e, const char* where) {
 // the global-f_prev kernels of 256 threads, 16 otherwise up to 512 threads)
 int dofs_cap(int threads, bool fg) { return threads > 768 ? 8 : threads > 512 ? 12 : (threads > 256 || !fg) ? 16 : 24; }
 
+// Kernel attributes every launch of an instantiation needs.
+template <class K>
+int prepare_kernel(K kern, int smem_bytes, int C, bool cluster) {
+  int rc = cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes),
+                      "cudaFuncSetAttribute(smem)");
+  if (rc) return rc;
+  // smallest SMEM carveout that holds the rank: the rest of the 256 KB
+  // array is L1, which holds the loop's read-only tables
+  cudaFuncAttributes fa;
+  rc = cuda_check(cudaFuncGetAttributes(&fa, kern), "cudaFuncGetAttributes");
+  if (rc) return rc;
+  const int need = smem_bytes + static_cast<int>(fa.sharedSizeBytes) + 1024;
+  const int pct = (100 * need + 228 * 1024 - 1) / (228 * 1024);
+  rc = cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, pct < 100 ? pct : 100),
+                  "cudaFuncSetAttribute(carveout)");
+  if (rc) return rc;
+  if (cluster && C > 8)
+    rc = cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1),
+                    "cudaFuncSetAttribute(non-portable cluster)");
+  return rc;
+}
+
 template <int MAXK, int MAXT, bool kFG, bool kEnergy = false>
 int launch_group(const frb_batch* batch, const frb_config* cfg, const frb_group& g, int32_t* queue,
                  cudaStream_t s, int threads = 0) {
-  auto kern = frb_relax_kernel<MAXK, MAXT, kFG, kEnergy>;
+  auto kern = frb_relax_kernel<MAXK, MAXT, kFG, kEnergy, false>;
   const int C = g.cluster;
-  int rc = cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, g.smem_bytes),
-                      "cudaFuncSetAttribute(smem)");
+  int rc = prepare_kernel(kern, g.smem_bytes, C, true);
   if (rc) return rc;
-  {
-    // smallest SMEM carveout that holds the rank: the rest of the 256 KB
-    // array is L1, which holds the loop's read-only tables
-    cudaFuncAttributes fa;
-    rc = cuda_check(cudaFuncGetAttributes(&fa, kern), "cudaFuncGetAttributes");
-    if (rc) return rc;
-    const int need = g.smem_bytes + static_cast<int>(fa.sharedSizeBytes) + 1024;
-    const int pct = (100 * need + 228 * 1024 - 1) / (228 * 1024);
-    rc = cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, pct < 100 ? pct : 100),
-                    "cudaFuncSetAttribute(carveout)");
-    if (rc) return rc;
-  }
-  if (C > 8) {
-    rc = cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1),
-                    "cudaFuncSetAttribute(non-portable cluster)");
-    if (rc) return rc;
-  }
   cudaLaunchConfig_t lc = {};
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -1630,10 +1791,62 @@ int launch_group(const frb_batch* batch, const frb_config* cfg, const frb_group&
     if (clusters < 1) return set_err(FRB_E_TOO_LARGE, "cluster does not fit on the GPU");
   }
   if (clusters > g.count) clusters = g.count;
+  // virtual clusters on the SMs the hardware clusters leave idle (a cluster
+  // of 8+ CTAs sits in one GPC: 7 clusters of 16 use 112 of 148 SMs)
+  int gm = 0;
+  if constexpr (!kEnergy && (MAXT == 512 || MAXT == 768)) {
+    if (C >= 8 && batch->xchg && g.gm_cap > 0 && g.grid_clusters <= 0 && !(g.flags & FRB_GF_NO_VIRTUAL) &&
+        !batch->phase_cycles) {  // (phase profiles measure the hardware clusters)
+      int dev = 0, nsm = 0;
+      rc = cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+      if (!rc) rc = cuda_check(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev), "sm count");
+      if (rc) return rc;
+      gm = (nsm - clusters * C) / C;
+      if (gm > g.gm_cap) gm = g.gm_cap;
+      if (gm > g.count - clusters) gm = g.count - clusters;
+      if (gm < 0) gm = 0;
+    }
+  }
   lc.gridDim = dim3(clusters * C);
   rc = cuda_check(cudaMemsetAsync(queue, 0, sizeof(int32_t), s), "cudaMemsetAsync");
   if (rc) return rc;
-  rc = cuda_check(cudaLaunchKernelEx(&lc, kern, *batch, *cfg, g.first, g.count, queue), "cudaLaunchKernelEx");
+  if (gm > 0) {
+    rc = cuda_check(cudaMemsetAsync(reinterpret_cast<char*>(batch->xchg) + g.xchg_off, 0, 128 * g.gm_cap, s),
+                    "cudaMemsetAsync(xchg)");
+    if (rc) return rc;
+  }
+  if constexpr (!kEnergy && (MAXT == 512 || MAXT == 768)) {
+    if (gm > 0) {  // forked stream: both kernels pull from the same queue
+      auto vkern = frb_relax_kernel<MAXK, MAXT, kFG, kEnergy, true>;
+      rc = prepare_kernel(vkern, g.smem_bytes, C, false);
+      if (rc) return rc;
+      cudaEvent_t ev0, ev1;
+      cudaStream_t gs;
+      rc = cuda_check(cudaEventCreateWithFlags(&ev0, cudaEventDisableTiming), "cudaEventCreate");
+      if (rc) return rc;
+      rc = cuda_check(cudaEventCreateWithFlags(&ev1, cudaEventDisableTiming), "cudaEventCreate");
+      if (!rc) rc = cuda_check(cudaStreamCreateWithFlags(&gs, cudaStreamNonBlocking), "cudaStreamCreate");
+      if (!rc) rc = cuda_check(cudaEventRecord(ev0, s), "cudaEventRecord");
+      if (!rc) rc = cuda_check(cudaStreamWaitEvent(gs, ev0, 0), "cudaStreamWaitEvent");
+      if (!rc) rc = cuda_check(cudaLaunchKernelEx(&lc, kern, *batch, *cfg, g.first, g.count, queue, g),
+                               "cudaLaunchKernelEx");
+      cudaLaunchConfig_t vc = lc;
+      vc.gridDim = dim3(gm * C);
+      vc.stream = gs;
+      vc.attrs = nullptr;
+      vc.numAttrs = 0;
+      if (!rc) rc = cuda_check(cudaLaunchKernelEx(&vc, vkern, *batch, *cfg, g.first, g.count, queue, g),
+                               "cudaLaunchKernelEx(virtual clusters)");
+      if (!rc) rc = cuda_check(cudaEventRecord(ev1, gs), "cudaEventRecord");
+      if (!rc) rc = cuda_check(cudaStreamWaitEvent(s, ev1, 0), "cudaStreamWaitEvent");
+      cudaEventDestroy(ev0);
+      cudaEventDestroy(ev1);
+      cudaStreamDestroy(gs);
+      if (rc) return rc;
+      return cuda_check(cudaGetLastError(), "frb_relax_kernel launch");
+    }
+  }
+  rc = cuda_check(cudaLaunchKernelEx(&lc, kern, *batch, *cfg, g.first, g.count, queue, g), "cudaLaunchKernelEx");
   if (rc) return rc;
   return cuda_check(cudaGetLastError(), "frb_relax_kernel launch");
 }

@@ -26,10 +26,10 @@ def test_library_exports_every_declared_symbol():
 
 def test_struct_layouts():
     assert C.sizeof(nat.FrbConfig) == 48
-    assert C.sizeof(nat.FrbBatch) == 8 + 26 * 8
+    assert C.sizeof(nat.FrbBatch) == 8 + 27 * 8
     assert nat.PROBLEM_DTYPE.itemsize == 184
     assert nat.PART_DTYPE.itemsize == 120
-    assert nat.GROUP_DTYPE.itemsize == 40
+    assert nat.GROUP_DTYPE.itemsize == 64
     assert nat.RESULT_DTYPE.itemsize == 144
 
 
