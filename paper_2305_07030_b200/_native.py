@@ -72,6 +72,7 @@ GROUP_DTYPE = np.dtype([
 ])
 GF_SERIAL = 1
 GF_NO_VIRTUAL = 2
+GF_VIRTUAL_ONLY = 4
 SETUP_ITEM_DTYPE = np.dtype([
     ("coords", "<u8"), ("elements", "<u8"), ("materials", "<u8"), ("node_order", "<u8"), ("act_elem", "<u8"),
     ("X_out", "<u8"), ("mass_out", "<u8"), ("L_out", "<u8"), ("EA_out", "<u8"), ("act_L_out", "<u8"),

@@ -611,7 +611,9 @@ def _pack(networks, bcs, probs, cluster: int | None = None) -> Batch:
         if C >= 8:  # virtual clusters may run on the SMs these clusters leave idle (frb200.h frb_group)
             pn = max(rt.n_local + rt.n_fix for i in ids for rt in part_of[i].ranks)
             ts = max(int(rt.tree[1]) for i in ids for rt in part_of[i].ranks)
-            g["gm_cap"] = VIRTUAL_CAP
+            g["gm_cap"] = VIRTUAL_CAP if not os.environ.get("FRB_VIRTUAL_ONLY") else 9
+            if os.environ.get("FRB_VIRTUAL_ONLY"):
+                g["flags"] |= nat.GF_VIRTUAL_ONLY
             g["gm_ex_stride"] = 4 * math.ceil((3 * ts + 64) / 4)
             g["gm_mir_stride"] = 2 * (2 * math.ceil(3 * pn / 2))
         groups.append(g)
@@ -717,7 +719,7 @@ class DeviceBatch:
             if int(g["gm_cap"]) > 0:
                 cap, C = int(g["gm_cap"]), int(g["cluster"])
                 g["xchg_off"] = xoff
-                xoff += 128 * cap + 8 * (cap * 2 * int(g["gm_ex_stride"]) + cap * C * int(g["gm_mir_stride"]))
+                xoff += 4096 * cap + 8 * (cap * 2 * int(g["gm_ex_stride"]) + cap * C * int(g["gm_mir_stride"]))
                 xoff = 256 * math.ceil(xoff / 256)
         n = int(h.node_base[-1])
         dev = self.device

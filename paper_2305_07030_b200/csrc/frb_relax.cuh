@@ -191,8 +191,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 // network together exchanging through L2 instead of DSMEM, with the same
 // tables, layout and arithmetic.  Each virtual cluster owns a slice of the
 // caller's exchange scratch (frb_batch.xchg, frb_group.xchg_off):
-//   cnt [32] int      [0..15] halo bytes received by rank r, [16] exports
-//                     arrived, [17] barrier arrivals, [18] current problem
+//   cnt [32][32] int  one 128-byte line per counter (pollers of one counter
+//                     do not contend with the atomics of another): line r <
+//                     16 halo bytes received by rank r, 16 exports arrived,
+//                     17 barrier arrivals, 18 current problem
 //   ex  [2][ex_stride] top-slot image (3 TS doubles) + 64 flag words, by
 //                     iteration parity
 //   mir [C][2][mir_stride/2] each rank's halo mirror: the bytes peers copy
@@ -216,6 +218,7 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
 __device__ __forceinline__ void gm_spin(const int* p, int target) {
   const long long t0 = clock64();
   while (ld_acquire(p) < target) {
+    __nanosleep(20);  // back off: fewer polls contending with the producers' atomics
     if (clock64() - t0 > 40000000000LL) __trap();  // ~20 s: a virtual cluster that never assembled
   }
 }
@@ -745,12 +748,12 @@ __device__ __forceinline__ void csync(int C) {
 template <bool kGM>
 __device__ __forceinline__ void gsync(int C, Scalars& sc, const Gx& gx) {
   if constexpr (kGM) {
+    __threadfence();  // every thread's global writes (positions, outputs) before the arrival
     __syncthreads();
     if (threadIdx.x == 0) {
-      __threadfence();
-      atomicAdd(gx.cnt + 17, 1);
+      atomicAdd(gx.cnt + 32 * 17, 1);
       sc.gx_b += C;
-      gm_spin(gx.cnt + 17, sc.gx_b);
+      gm_spin(gx.cnt + 32 * 17, sc.gx_b);
       __threadfence();
     }
     __syncthreads();
@@ -1065,12 +1068,12 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
                                                   par * (gx.mir_stride / 2) + run.z / 8);
         for (int k = t; k < run.w / 16; k += T) dst[k] = src[k];
       }
+      __threadfence();  // each thread's mirror stores visible GPU-wide before the release below
       __syncthreads();
       if (t == 0) {
-        __threadfence();
         for (int i = 0; i < R.n_runs; ++i) {
           const int4 run = __ldg(R.runs + i);
-          atomicAdd(gx.cnt + run.x, run.w);
+          atomicAdd(gx.cnt + 32 * run.x, run.w);
         }
       }
     }
@@ -1080,12 +1083,20 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
       const int par = static_cast<int>(mb.ph_h);
       if (t == 0) {
         sc.gx_h += static_cast<int>(R.halo_bytes);
-        gm_spin(gx.cnt + rank, sc.gx_h);
+        gm_spin(gx.cnt + 32 * rank, sc.gx_h);
         __threadfence();
       }
       __syncthreads();
       const double* src = gx.mir + static_cast<int64_t>(rank) * gx.mir_stride + par * (gx.mir_stride / 2);
-      for (int k = 3 * n_own + t; k < 3 * R.n_local; k += T) g_smem[o.pos + k] = __ldcg(src + k);
+      const int hi = 3 * R.n_local;
+      for (int k0 = 3 * n_own + t; k0 < hi; k0 += 8 * T) {  // 8 L2 loads in flight per thread
+        double tmp[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) tmp[q] = k0 + q * T < hi ? __ldcg(src + k0 + q * T) : 0.0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          if (k0 + q * T < hi) g_smem[o.pos + k0 + q * T] = tmp[q];
+      }
       __syncthreads();
     }
   };
@@ -1465,11 +1476,10 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
             st_async(sc.peer_smem[0] + 8u * (o_fl + 16 + 3 * rank + e), e3[e], sc.peer_bar_s[0]);
       }
       if (kGM) {  // flag, then publish this rank's exports with a release add
-        if (lane == 0) {
-          gx_ex[3 * R.TS + rank] = sc.singular ? 1.0 : 0.0;
-          __threadfence();
-          atomicAdd(gx.cnt + 16, 1);
-        }
+        if (lane == 0) gx_ex[3 * R.TS + rank] = sc.singular ? 1.0 : 0.0;
+        __threadfence();  // every lane's export stores
+        __syncwarp();
+        if (lane == 0) atomicAdd(gx.cnt + 32 * 16, 1);
       } else if (C > 1) {
         if (lane < C && lane != rank)  // this rank's singular flag, lane q -> rank q
           st_async(sc.peer_smem[lane] + 8u * (o_fl + rank), sc.singular ? 1.0 : 0.0, sc.peer_bar_s[lane]);
@@ -1480,12 +1490,19 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
       if constexpr (kGM) {  // every rank's exports: wait for the count, copy the image back
         if (lane == 0) {
           sc.gx_s += C;
-          gm_spin(gx.cnt + 16, sc.gx_s);
+          gm_spin(gx.cnt + 32 * 16, sc.gx_s);
           __threadfence();
         }
         __syncwarp();
         const int n_top = 3 * R.tree[8];  // the exported slots of the top array
-        for (int k = lane; k < n_top; k += 32) g_smem[o_ts + k] = __ldcg(gx_ex + k);
+        for (int k0 = lane; k0 < n_top; k0 += 8 * 32) {  // 8 L2 loads in flight per lane
+          double tmp[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) tmp[q] = k0 + 32 * q < n_top ? __ldcg(gx_ex + k0 + 32 * q) : 0.0;
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            if (k0 + 32 * q < n_top) g_smem[o_ts + k0 + 32 * q] = tmp[q];
+        }
         if (lane < C) g_smem[o_fl + lane] = __ldcg(gx_ex + 3 * R.TS + lane);
         __syncwarp();
         mark(sc, prof, PH_TW);
@@ -1669,8 +1686,8 @@ __global__ void __launch_bounds__(MAXT, 1)
     char* base = reinterpret_cast<char*>(b.xchg) + grp.xchg_off;
     gx.ex_stride = grp.gm_ex_stride;
     gx.mir_stride = grp.gm_mir_stride;
-    gx.cnt = reinterpret_cast<int*>(base) + 32 * vg;
-    double* ex0 = reinterpret_cast<double*>(base + 128 * static_cast<int64_t>(grp.gm_cap));
+    gx.cnt = reinterpret_cast<int*>(base + 4096 * static_cast<int64_t>(vg));
+    double* ex0 = reinterpret_cast<double*>(base + 4096 * static_cast<int64_t>(grp.gm_cap));
     gx.ex = ex0 + static_cast<int64_t>(vg) * 2 * gx.ex_stride;
     gx.mir = ex0 + static_cast<int64_t>(grp.gm_cap) * 2 * gx.ex_stride +
              static_cast<int64_t>(vg) * C * gx.mir_stride;
@@ -1698,14 +1715,14 @@ __global__ void __launch_bounds__(MAXT, 1)
     if (rank == 0 && threadIdx.x == 0) {
       const int idx = atomicAdd(queue, 1);
       if constexpr (kGM) {
-        gx.cnt[18] = idx;  // published by the barrier's release
+        gx.cnt[32 * 18] = idx;  // published by the barrier's release
       } else {
         for (int q = 0; q < C; ++q) *(C > 1 ? peer(&sc.problem, q) : &sc.problem) = idx;
       }
     }
     gsync<kGM>(C, sc, gx);
     if constexpr (kGM) {
-      if (threadIdx.x == 0) sc.problem = ld_acquire(gx.cnt + 18);
+      if (threadIdx.x == 0) sc.problem = ld_acquire(gx.cnt + 32 * 18);
       __syncthreads();
     }
     const int idx = sc.problem;
@@ -1796,11 +1813,12 @@ int launch_group(const frb_batch* batch, const frb_config* cfg, const frb_group&
   int gm = 0;
   if constexpr (!kEnergy && (MAXT == 512 || MAXT == 768)) {
     if (C >= 8 && batch->xchg && g.gm_cap > 0 && g.grid_clusters <= 0 && !(g.flags & FRB_GF_NO_VIRTUAL) &&
-        !batch->phase_cycles) {  // (phase profiles measure the hardware clusters)
+        (!batch->phase_cycles || (g.flags & FRB_GF_VIRTUAL_ONLY))) {  // (phase profiles: hardware clusters)
       int dev = 0, nsm = 0;
       rc = cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
       if (!rc) rc = cuda_check(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev), "sm count");
       if (rc) return rc;
+      if (g.flags & FRB_GF_VIRTUAL_ONLY) clusters = 0;  // experiment: virtual clusters only
       gm = (nsm - clusters * C) / C;
       if (gm > g.gm_cap) gm = g.gm_cap;
       if (gm > g.count - clusters) gm = g.count - clusters;
@@ -1811,7 +1829,7 @@ int launch_group(const frb_batch* batch, const frb_config* cfg, const frb_group&
   rc = cuda_check(cudaMemsetAsync(queue, 0, sizeof(int32_t), s), "cudaMemsetAsync");
   if (rc) return rc;
   if (gm > 0) {
-    rc = cuda_check(cudaMemsetAsync(reinterpret_cast<char*>(batch->xchg) + g.xchg_off, 0, 128 * g.gm_cap, s),
+    rc = cuda_check(cudaMemsetAsync(reinterpret_cast<char*>(batch->xchg) + g.xchg_off, 0, 4096 * g.gm_cap, s),
                     "cudaMemsetAsync(xchg)");
     if (rc) return rc;
   }
@@ -1828,8 +1846,8 @@ int launch_group(const frb_batch* batch, const frb_config* cfg, const frb_group&
       if (!rc) rc = cuda_check(cudaStreamCreateWithFlags(&gs, cudaStreamNonBlocking), "cudaStreamCreate");
       if (!rc) rc = cuda_check(cudaEventRecord(ev0, s), "cudaEventRecord");
       if (!rc) rc = cuda_check(cudaStreamWaitEvent(gs, ev0, 0), "cudaStreamWaitEvent");
-      if (!rc) rc = cuda_check(cudaLaunchKernelEx(&lc, kern, *batch, *cfg, g.first, g.count, queue, g),
-                               "cudaLaunchKernelEx");
+      if (!rc && clusters > 0)
+        rc = cuda_check(cudaLaunchKernelEx(&lc, kern, *batch, *cfg, g.first, g.count, queue, g), "cudaLaunchKernelEx");
       cudaLaunchConfig_t vc = lc;
       vc.gridDim = dim3(gm * C);
       vc.stream = gs;
