@@ -15,12 +15,13 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("FRB_LIB") or os.path.join(HERE, "lib", "libfrb200.so")
 
-ABI_VERSION = 9
+ABI_VERSION = 10
 MAX_CLUSTER = 16
 FRB_OK, FRB_E_INVALID, FRB_E_TOO_LARGE, FRB_E_CUDA, FRB_E_UNSUPPORTED = 0, -1, -2, -3, -4
 STATUS_CONVERGED, STATUS_MAX_ITERS, STATUS_SINGULAR = 0, 1, 2
 DAMPING_ADAPTIVE, DAMPING_FIXED = 0, 1
 PF_EA_UNIFORM = 1
+PF_MASS_GLOBAL = 2
 PHASES = 12             # phase_cycles slots per CTA (frb200.h)
 PHASE_NAMES = ("F1 coefs", "F2 gather", "A per-DOF", "C chains", "T local+exp", "T exch wait",
                "T top+scal", "U update", "epilogue", "prologue", "halo wait", "T local tree")

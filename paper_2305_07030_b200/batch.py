@@ -151,13 +151,13 @@ class Topology:
                                       self.slots_a, self.slots_b, self.plan, C)
         return self.parts[C]
 
-    def chosen(self) -> tuple[Partition, bool]:
+    def chosen(self) -> tuple[Partition, bool, bool]:
         """choose_cluster(), computed once per topology."""
         if self._chosen is None:
             self._chosen = self.choose_cluster()
         return self._chosen
 
-    def choose_cluster(self) -> tuple[Partition, bool]:
+    def choose_cluster(self) -> tuple[Partition, bool, bool]:
         """Smallest cluster with at most DOFS_PER_RANK free DOFs per rank whose
         ranks fit the SMEM budget (more ranks if SMEM demands it), keeping
         f_prev in SMEM whenever some cluster size allows it; otherwise the
@@ -165,7 +165,9 @@ class Topology:
         nf = 3 * self.n_free_nodes
         want = max(1, math.ceil(nf / DOFS_PER_RANK))
         reasons = []
-        for fprv_global in (False, True):  # on-chip f_prev at any cluster size first
+        # on-chip f_prev at any cluster size first; then f_prev in global
+        # memory; then also the node masses (the largest networks)
+        for fprv_global, mass_global in ((False, False), (True, False), (True, True)):
             for C in CLUSTER_SIZES:
                 if C < want and C != CLUSTER_SIZES[-1]:
                     continue
@@ -174,10 +176,11 @@ class Topology:
                 except ValueError as e:  # e.g. a node that is halo to more than two ranks
                     reasons.append(f"C={C}: {e}")
                     continue
-                if partition_smem_bytes(part, fprv_global) <= SMEM_BUDGET:
-                    return part, fprv_global
-                reasons.append(f"C={C}{' (f_prev global)' if fprv_global else ''}: "
-                               f"{partition_smem_bytes(part, fprv_global)} B of SMEM per rank")
+                if partition_smem_bytes(part, fprv_global, mass_global) <= SMEM_BUDGET:
+                    return part, fprv_global, mass_global
+                reasons.append(f"C={C}{' (f_prev global)' if fprv_global else ''}"
+                               f"{' (masses global)' if mass_global else ''}: "
+                               f"{partition_smem_bytes(part, fprv_global, mass_global)} B of SMEM per rank")
         raise nat.NativeError(nat.FRB_E_TOO_LARGE,
                               f"network with {nf} free DOFs fits no cluster of {CLUSTER_SIZES} CTAs ("
                               + "; ".join(dict.fromkeys(reasons)) + ")")
@@ -474,11 +477,12 @@ def _pack(networks, bcs, probs, cluster: int | None = None) -> Batch:
     inc, plans, ell, act_ab, halo_g, runs, fix_g, trees, inc_node, elem_ab = ([] for _ in range(10))
     n_inc = n_plan = n_ell = n_act = n_halo = n_runs = n_fix = n_tree = n_tnode = n_telem = 0
     parts_rows = []
-    part_of, fglob_of, act_of, cols = [], [], [], []
+    part_of, fglob_of, mglob_of, act_of, cols = [], [], [], [], []
     n_parts = 0
     for i, p in enumerate(probs):
         t = p.topo
-        part, fglob = (t.partition(cluster), False) if cluster else t.chosen()
+        part, fglob, mglob = (t.partition(cluster), False, False) if cluster else t.chosen()
+        mglob_of.append(mglob)
         part_of.append(part)
         fglob_of.append(fglob)
         if p.topo_key not in topo_slot:
@@ -589,7 +593,7 @@ def _pack(networks, bcs, probs, cluster: int | None = None) -> Batch:
     uniform = [bool(p.ea.size == 0 or (p.ea == p.ea[0]).all()) for p in probs]
     any_nonuniform = not all(uniform)
     if P:
-        desc["flags"] = np.where(uniform, nat.PF_EA_UNIFORM, 0)
+        desc["flags"] = np.where(uniform, nat.PF_EA_UNIFORM, 0) | np.where(mglob_of, nat.PF_MASS_GLOBAL, 0)
         desc["volume"] = [p.volume for p in probs]
         desc["ea"] = [p.ea[0] if p.ea.size else 0.0 for p in probs]
 
@@ -599,7 +603,7 @@ def _pack(networks, bcs, probs, cluster: int | None = None) -> Batch:
     for C, fglob in sorted({(pt.C, fg) for pt, fg in zip(part_of, fglob_of)}):
         ids = [i for i in range(P) if part_of[i].C == C and fglob_of[i] == fglob]
         ids.sort(key=lambda i: -probs[i].n_nodes)
-        smem = max(partition_smem_bytes(part_of[i], fglob) for i in ids)
+        smem = max(partition_smem_bytes(part_of[i], fglob, mglob_of[i]) for i in ids)
         own = max(3 * rt.n_own for i in ids for rt in part_of[i].ranks)
         leaves = max(rt.n_leaves for i in ids for rt in part_of[i].ranks)
         g = np.zeros((), dtype=nat.GROUP_DTYPE)

@@ -81,9 +81,10 @@ int frb_device_info(int device, int* n_sm, int* smem_optin, int* cc_major, int* 
 }
 
 int64_t frb_rank_smem_bytes(int32_t n_pos, int32_t n_own, int32_t n_act, int32_t n_slots, int32_t n_prog,
-                            int32_t fprv_global) {
+                            int32_t mode) {
   const int64_t nf = 3 * static_cast<int64_t>(n_own);
-  return 8 * (3 * static_cast<int64_t>(n_pos) + (fprv_global ? 1 : 2) * nf + (nf > n_act ? nf : n_act) + 2 * n_own +
+  return 8 * (3 * static_cast<int64_t>(n_pos) + ((mode & 1) ? 1 : 2) * nf + (nf > n_act ? nf : n_act) +
+              ((mode & 2) ? 1 : 2) * n_own +
               3 * static_cast<int64_t>(n_slots) + 160) +
          4 * ((static_cast<int64_t>(n_prog) + 1) & ~1LL);
 }

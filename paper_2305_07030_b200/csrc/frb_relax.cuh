@@ -244,6 +244,7 @@ struct Net {
 
 struct Rank {
   int node0, n_own, n_local, n_fix, n_act, n_int;
+  int ms_on;                        // node masses in SMEM (else FRB_PF_MASS_GLOBAL: global memory)
   int S, SA, SB, leaf0, n_leaves;
   int PN, NFO, CF;  // uniform SMEM extents of the problem (max over ranks)
   int LS, TS, PI;   // tree: local slots, top slots, block words (uniform)
@@ -294,6 +295,7 @@ __device__ void load_views(Net& n, Rank& R, const frb_batch& b, int p, int r) {
   R.n_fix = Q.n_fix;
   R.n_act = Q.n_act;
   R.n_int = Q.n_int;
+  R.ms_on = (P.flags & FRB_PF_MASS_GLOBAL) ? 0 : 1;
   R.S = Q.ell_stride;
   R.SA = Q.slots_a;
   R.SB = Q.slots_b;
@@ -884,8 +886,8 @@ __device__ __forceinline__ Layout layout(const Rank& R) {
   o.tslot = o.lslot + 3 * R.LS;
   o.flag = o.tslot + 6 * R.TS;  // two parity buffers of top slots
   o.rm = o.flag + 2 * 64 + 32;    // two parity buffers of flags[16] + partials[16][3]; fin[16]; ack[16]
-  o.ms = o.rm + R.NFO / 3;          // refined reciprocal masses of the own nodes
-  o.prog = 2 * (o.ms + R.NFO / 3);  // the own nodes' masses
+  o.ms = o.rm + R.NFO / 3;                      // refined reciprocal masses of the own nodes
+  o.prog = 2 * (o.ms + (R.ms_on ? R.NFO / 3 : 0));  // the own nodes' masses (unless FRB_PF_MASS_GLOBAL)
   return o;
 }
 
@@ -980,11 +982,13 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
   // the rank's tree block (local + top programs, exports) lives in SMEM
   int* const prog = reinterpret_cast<int*>(g_smem) + o.prog;
   for (int k = t; k < R.tree_len; k += T) prog[k] = __ldg(R.tree + k);
+  const bool ms_on = R.ms_on != 0;
   for (int i = t; i < n_own; i += T) {
     const double m = __ldg(nmass + i);
-    g_smem[o.ms + i] = m;
+    if (ms_on) g_smem[o.ms + i] = m;
     g_smem[o.rm + i] = frb_arith::rcp_refined(m);
   }
+  auto MASS = [&](int i) -> double { return ms_on ? g_smem[o.ms + i] : __ldg(nmass + i); };
   const int* const lprog = prog + R.tree[3];
   const int* const tprog = prog + R.tree[4];
   const int* const exps = prog + R.tree[5];
@@ -1115,7 +1119,7 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
         // below, in program order), never another thread's slot
         const int dl = d0 + kk * nthr < nfo ? d0 + kk * nthr : d0;
         const int i = dl / 3;  // f of this iteration, left in fcur by A
-        q[kk] = frb_arith::div_fast_r(-g_smem[o.fcur + dl], g_smem[o.ms + i], g_smem[o.rm + i], ok[kk]);
+        q[kk] = frb_arith::div_fast_r(-g_smem[o.fcur + dl], MASS(i), g_smem[o.rm + i], ok[kk]);
       }
       bool all_ok = true;
 #pragma unroll
@@ -1124,7 +1128,7 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
 #pragma unroll
         for (int kk = 0; kk < kChunk; ++kk) {
           const int dl = d0 + kk * nthr;
-          if (!ok[kk] && dl < nfo) q[kk] = exact_div(-g_smem[o.fcur + dl], g_smem[o.ms + dl / 3]);
+          if (!ok[kk] && dl < nfo) q[kk] = exact_div(-g_smem[o.fcur + dl], MASS(dl / 3));
         }
       }
 #pragma unroll
@@ -1264,7 +1268,7 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
           const int dl = k0 + kk < nk ? t + (k0 + kk) * T : dl_last;
           f[kk] = g_smem[o.fcur + dl];
           kh[kk] = FPRV(dl);  // f_prev, until the quotient replaces it
-          m[kk] = g_smem[o.ms + dl / 3];
+          m[kk] = MASS(dl / 3);
         }
         if constexpr (kAd) {
 #pragma unroll

@@ -127,14 +127,21 @@ def cut_points(plan: np.ndarray, nf: int, C: int) -> list[int]:
     # cost[i, j] of a rank spanning candidates i < j
     span = pos[None, :] - pos[:, None]
     nleaf = leaf[None, :] - leaf[:, None]
-    cost = np.where(span > 0, span + big * (nleaf > LEAVES_PER_ROUND), np.inf).astype(np.float64)
-    best = cost[0].copy()                                 # one rank covering [0, pos[j])
-    back = [np.zeros(K, dtype=np.int64)]
-    for _ in range(1, C):
-        cand = np.maximum(best[:, None], cost)           # previous ranks end at i, the next spans i..j
-        arg = np.argmin(cand, axis=0)
-        best = cand[arg, np.arange(K)]
-        back.append(arg)
+
+    def solve(cost):
+        best = cost[0].copy()                             # one rank covering [0, pos[j])
+        back = [np.zeros(K, dtype=np.int64)]
+        for _ in range(1, C):
+            cand = np.maximum(best[:, None], cost)       # previous ranks end at i, the next spans i..j
+            arg = np.argmin(cand, axis=0)
+            best = cand[arg, np.arange(K)]
+            back.append(arg)
+        return best[K - 1], back
+
+    plain = np.where(span > 0, span, np.inf).astype(np.float64)
+    worst, back = solve(np.where(nleaf > LEAVES_PER_ROUND, plain + big, plain))
+    if worst >= big:  # no split keeps every rank within one chain round: plain min-max
+        worst, back = solve(plain)
     cuts = [K - 1]
     for k in range(C - 1, 0, -1):
         cuts.append(int(back[k][cuts[-1]]))
@@ -270,7 +277,7 @@ def partition(n_nodes: int, n_free: int, ia: np.ndarray, ib: np.ndarray, ell_oth
     return Partition(C=C, slots_a=slots_a, slots_b=slots_b, ranks=ranks)
 
 
-def rank_smem_bytes(rt: RankTables, fprv_global: bool = False) -> int:
+def rank_smem_bytes(rt: RankTables, fprv_global: bool = False, mass_global: bool = False) -> int:
     """Dynamic SMEM of one rank (mirror of frb_rank_smem_bytes):
     positions [n_local + n_fix][3] (a DOF's own position slot doubles as its
     sq entry between the force and update phases), f and -- unless it lives
@@ -281,20 +288,22 @@ def rank_smem_bytes(rt: RankTables, fprv_global: bool = False) -> int:
     words, one refined reciprocal mass and the mass per
     own node and the int32 tree block (programs + exports)."""
     return smem_bytes(rt.n_local + rt.n_fix, rt.n_own, rt.n_act, int(rt.tree[0]) + 2 * int(rt.tree[1]),
-                      int(rt.tree[2]), fprv_global)
+                      int(rt.tree[2]), fprv_global, mass_global)
 
 
-def partition_smem_bytes(part: "Partition", fprv_global: bool = False) -> int:
+def partition_smem_bytes(part: "Partition", fprv_global: bool = False, mass_global: bool = False) -> int:
     """Dynamic SMEM of every rank of a partitioned problem: the kernel lays
     all ranks out identically (peers address each other's buffers by the same
     offsets), each region sized by its maximum over the ranks."""
     rs = part.ranks
     return smem_bytes(max(r.n_local + r.n_fix for r in rs), max(r.n_own for r in rs),
                       max(r.n_act for r in rs), int(rs[0].tree[0]) + 2 * int(rs[0].tree[1]), int(rs[0].tree[2]),
-                      fprv_global)
+                      fprv_global, mass_global)
 
 
-def smem_bytes(n_pos: int, n_own: int, n_act: int, n_slots: int, n_prog: int, fprv_global: bool = False) -> int:
+def smem_bytes(n_pos: int, n_own: int, n_act: int, n_slots: int, n_prog: int, fprv_global: bool = False,
+               mass_global: bool = False) -> int:
     nf = 3 * n_own
-    return 8 * (3 * n_pos + (1 if fprv_global else 2) * nf + max(nf, n_act) + 2 * n_own + 3 * n_slots + 160) + \
+    return 8 * (3 * n_pos + (1 if fprv_global else 2) * nf + max(nf, n_act) + (1 if mass_global else 2) * n_own +
+                3 * n_slots + 160) + \
         4 * ((n_prog + 1) & ~1)

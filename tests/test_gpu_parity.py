@@ -246,10 +246,26 @@ def test_two_slot_network_vs_oracle(cuda_device):
     d = np.abs(X[E[:, 1]] - X[E[:, 0]])
     net2 = frb.FiberNetwork(X, E[d[:, 2] < 0.5 * np.maximum(d[:, 0], d[:, 1])], net.materials,
                             net.boundary_nodes, rve_volume=net.volume)
-    part, _ = fb.build_problem(net2, frb.AffineBC(np.eye(3))).topo.choose_cluster()
+    part, _, _ = fb.build_problem(net2, frb.AffineBC(np.eye(3))).topo.choose_cluster()
     assert (part.slots_a, part.slots_b) == (2, 2)
     F = np.diag([1.1, 1.0, 1.0])
     cfg = frb.SolverConfig(max_iters=400)
     r = frb.dynamic_relaxation_solve(net2, frb.AffineBC(F), cfg)
     o = orc.solve(net2, F, cfg)
     assert_matches(r, o.u, o.iters, o.converged, o.residual, o.r_ref, o.sigma, label="2-slot")
+
+
+def test_masses_in_global_memory_vs_oracle(cuda_device):
+    """A 31^3 network (c4's n = 7 + 24) fills a 16-CTA cluster even with
+    f_prev in global memory, so its node masses stay in global memory too
+    (FRB_PF_MASS_GLOBAL); 60 iterations bit-equal to the oracle, and the same
+    network to convergence on 2 of the shared code paths."""
+    from paper_2305_07030_b200 import _native as nat
+    net = frb.generate_lattice(31, 31, 31, 0.3, 76)
+    F = np.eye(3) + 0.2 * np.outer([1, 0, 0], [0, 1, 0])
+    cfg = frb.SolverConfig(max_iters=60)
+    batch = frb.pack_batch([net], [frb.AffineBC(F)])
+    assert int(batch.desc[0]["cluster"]) == 16 and int(batch.desc[0]["flags"]) & nat.PF_MASS_GLOBAL
+    r = frb.solve_batch(batch, config=cfg)[0]
+    o = orc.solve(net, F, cfg)
+    assert_matches(r, o.u, o.iters, o.converged, o.residual, o.r_ref, o.sigma, label="31^3")

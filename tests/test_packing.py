@@ -133,24 +133,24 @@ def test_partition_tables(net, C):
 def test_rank_smem_mirror_matches_library():
     from paper_2305_07030_b200.partition import smem_bytes
     for args in [(3375, 2197, 7098, 127, 700, 0), (1300, 1099, 3600, 80, 301, 1), (150, 150, 400, 7, 41, 0),
-                 (0, 0, 0, 0, 14, 0), (1, 1, 0, 1, 15, 1), (63, 63, 400, 3, 20, 0)]:
-        assert nat.lib().frb_rank_smem_bytes(*args) == smem_bytes(*args[:5], bool(args[5]))
+                 (0, 0, 0, 0, 14, 0), (1, 1, 0, 1, 15, 1), (63, 63, 400, 3, 20, 0), (3869, 1909, 6721, 482, 1302, 3)]:
+        assert nat.lib().frb_rank_smem_bytes(*args) == smem_bytes(*args[:5], bool(args[5] & 1), bool(args[5] & 2))
 
 
 def test_c2_networks_use_two_ranks_on_chip():
     """15^3 networks (config 2): a 2-CTA cluster keeps every array on chip
     (one CTA would need f_prev in global memory)."""
     t = fb.build_problem(frb.generate_lattice(15, 15, 15, 0.3, 0), frb.AffineBC(np.eye(3))).topo
-    part, fglob = t.choose_cluster()
-    assert part.C == 2 and not fglob
+    part, fglob, mglob = t.choose_cluster()
+    assert part.C == 2 and not fglob and not mglob
     assert partition_smem_bytes(part, False) <= fb.SMEM_BUDGET < partition_smem_bytes(t.partition(1), False)
 
 
 def test_c3_networks_fit_a_16_cluster_with_global_fprev():
     """100k-DOF networks (config 3): 16 ranks, f_prev in global memory."""
     t = fb.build_problem(frb.generate_lattice(32, 32, 32, 0.3, 0), frb.AffineBC(np.eye(3))).topo
-    part, fglob = t.choose_cluster()
-    assert part.C == 16 and fglob
+    part, fglob, mglob = t.choose_cluster()
+    assert part.C == 16 and fglob and not mglob
     assert partition_smem_bytes(part, True) <= fb.SMEM_BUDGET
 
 
