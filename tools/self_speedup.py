@@ -14,7 +14,7 @@ import paper_2305_07030_b200 as frb
 from paper_2305_07030_b200 import cli
 from paper_2305_07030_b200.benchmark import RAW_HEADER, SUMMARY_HEADER, emit_csv, run_benchmark, summarize
 
-out = os.path.join(ROOT, "profiles", "r02_self_speedup")
+out = os.path.join(ROOT, "gpurun_out", "r02_self_speedup")
 sizes = [(7, 7, 8), (15, 15, 15)]
 recs = run_benchmark(sizes, [1, 4, 16, 64, 148], strategies=("team", "naive"), reps=3)
 recs += run_benchmark(sizes, [256, 1024], strategies=("team",), reps=3)
@@ -35,7 +35,7 @@ for size in sizes:
         ts = []
         for _ in range(3):
             e0.record(); L.run(); e1.record(); torch.cuda.synchronize(); ts.append(e0.elapsed_time(e1) / 1e3)
-        lines.append(f"team,{3 * net.n_nodes},{N},{np.mean(ts)!r}")
+        lines.append(f"team,{3 * net.n_nodes},{N},{float(np.mean(ts))!r}")
 open(out + "_device.csv", "w").write("\n".join(lines) + "\n")
 for r in rows:
     print(r.strategy, r.n_dofs, r.n_problems, round(r.mean_seconds, 4), r.self_speedup and round(r.self_speedup, 2),
