@@ -269,3 +269,23 @@ def test_masses_in_global_memory_vs_oracle(cuda_device):
     r = frb.solve_batch(batch, config=cfg)[0]
     o = orc.solve(net, F, cfg)
     assert_matches(r, o.u, o.iters, o.converged, o.residual, o.r_ref, o.sigma, label="31^3")
+
+
+def test_randomly_renumbered_network_vs_oracle(cuda_device):
+    """Node ids in random order (no slab locality): the 4 ranks keep hundreds
+    of short halo runs each (odd starts and lengths widened to 16-byte bulk
+    copies) and nodes are halo to up to 3 ranks; 100 iterations bit-equal."""
+    net = frb.generate_lattice(16, 16, 16, 0.3, 1)
+    perm = np.random.default_rng(0).permutation(net.n_nodes)
+    el = net.elements.copy()
+    el[:, :2] = perm[el[:, :2]]
+    net2 = frb.FiberNetwork(net.node_coords[np.argsort(perm)], el, net.materials,
+                            frozenset(int(perm[b]) for b in net.boundary_nodes))
+    F = np.diag([1.1, 1.0, 1.05])
+    cfg = frb.SolverConfig(max_iters=100)
+    batch = frb.pack_batch([net2], [frb.AffineBC(F)])
+    assert int(batch.desc[0]["cluster"]) > 1
+    assert max(len(rt.runs) for rt in batch.problems[0].topo.chosen()[0].ranks) > 100
+    r = frb.solve_batch(batch, config=cfg)[0]
+    o = orc.solve(net2, F, cfg)
+    assert_matches(r, o.u, o.iters, o.converged, o.residual, o.r_ref, o.sigma, label="renumbered 16^3")

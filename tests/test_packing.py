@@ -277,3 +277,18 @@ def test_halo_runs_are_aligned_bulk_copies(n, C):
             assert sb // 24 + nb // 24 <= rt.n_local + rt.n_fix + 1
             recv[dst] += nb
     assert recv == [rt.halo_bytes for rt in part.ranks]
+
+
+def test_renumbered_network_packs_with_many_runs():
+    """Random node numbering: nodes are halo to more than two ranks, which the
+    run-based halo layout handles (round 1's two-target send table could not)."""
+    net = frb.generate_lattice(16, 16, 16, 0.3, 1)
+    perm = np.random.default_rng(0).permutation(net.n_nodes)
+    el = net.elements.copy()
+    el[:, :2] = perm[el[:, :2]]
+    net2 = frb.FiberNetwork(net.node_coords[np.argsort(perm)], el, net.materials,
+                            frozenset(int(perm[b]) for b in net.boundary_nodes))
+    b = frb.pack_batch([net2], [frb.AffineBC(np.eye(3))])
+    part = b.problems[0].topo.chosen()[0]
+    assert part.C > 2
+    assert sum(len(rt.runs) for rt in part.ranks) > 4 * part.C
