@@ -165,9 +165,9 @@ class Topology:
         nf = 3 * self.n_free_nodes
         want = max(1, math.ceil(nf / DOFS_PER_RANK))
         reasons = []
-        # on-chip f_prev at any cluster size first; then f_prev in global
-        # memory; then also the node masses (the largest networks)
-        for fprv_global, mass_global in ((False, False), (True, False), (True, True)):
+        # on-chip f_prev at any cluster size first; then f_prev (and the node
+        # masses, frb_relax.cuh layout) in global memory
+        for fprv_global, mass_global in ((False, False), (True, True)):
             for C in CLUSTER_SIZES:
                 if C < want and C != CLUSTER_SIZES[-1]:
                     continue
@@ -593,7 +593,7 @@ def _pack(networks, bcs, probs, cluster: int | None = None) -> Batch:
     uniform = [bool(p.ea.size == 0 or (p.ea == p.ea[0]).all()) for p in probs]
     any_nonuniform = not all(uniform)
     if P:
-        desc["flags"] = np.where(uniform, nat.PF_EA_UNIFORM, 0) | np.where(mglob_of, nat.PF_MASS_GLOBAL, 0)
+        desc["flags"] = np.where(uniform, nat.PF_EA_UNIFORM, 0) | np.where(mglob_of, nat.PF_MASS_GLOBAL, 0)  # informational
         desc["volume"] = [p.volume for p in probs]
         desc["ea"] = [p.ea[0] if p.ea.size else 0.0 for p in probs]
 

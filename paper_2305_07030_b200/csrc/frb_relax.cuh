@@ -244,7 +244,6 @@ struct Net {
 
 struct Rank {
   int node0, n_own, n_local, n_fix, n_act, n_int;
-  int ms_on;                        // node masses in SMEM (else FRB_PF_MASS_GLOBAL: global memory)
   int S, SA, SB, leaf0, n_leaves;
   int PN, NFO, CF;  // uniform SMEM extents of the problem (max over ranks)
   int LS, TS, PI;   // tree: local slots, top slots, block words (uniform)
@@ -295,7 +294,6 @@ __device__ void load_views(Net& n, Rank& R, const frb_batch& b, int p, int r) {
   R.n_fix = Q.n_fix;
   R.n_act = Q.n_act;
   R.n_int = Q.n_int;
-  R.ms_on = (P.flags & FRB_PF_MASS_GLOBAL) ? 0 : 1;
   R.S = Q.ell_stride;
   R.SA = Q.slots_a;
   R.SB = Q.slots_b;
@@ -875,6 +873,9 @@ struct Layout {
   int pos, fcur, fprv, cf, lslot, tslot, flag, rm, ms, prog;  // prog: int32 index
 };
 
+// kFG (the networks too large for on-chip f_prev) also read the node masses
+// from global memory: a runtime switch between the two cost 20 % on C3 (the
+// extra live state spills)
 template <bool kFG>
 __device__ __forceinline__ Layout layout(const Rank& R) {
   Layout o;
@@ -886,8 +887,8 @@ __device__ __forceinline__ Layout layout(const Rank& R) {
   o.tslot = o.lslot + 3 * R.LS;
   o.flag = o.tslot + 6 * R.TS;  // two parity buffers of top slots
   o.rm = o.flag + 2 * 64 + 32;    // two parity buffers of flags[16] + partials[16][3]; fin[16]; ack[16]
-  o.ms = o.rm + R.NFO / 3;                      // refined reciprocal masses of the own nodes
-  o.prog = 2 * (o.ms + (R.ms_on ? R.NFO / 3 : 0));  // the own nodes' masses (unless FRB_PF_MASS_GLOBAL)
+  o.ms = o.rm + R.NFO / 3;                    // refined reciprocal masses of the own nodes
+  o.prog = 2 * (o.ms + (kFG ? 0 : R.NFO / 3));  // the own nodes' masses (on chip unless kFG)
   return o;
 }
 
@@ -982,13 +983,18 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
   // the rank's tree block (local + top programs, exports) lives in SMEM
   int* const prog = reinterpret_cast<int*>(g_smem) + o.prog;
   for (int k = t; k < R.tree_len; k += T) prog[k] = __ldg(R.tree + k);
-  const bool ms_on = R.ms_on != 0;
   for (int i = t; i < n_own; i += T) {
     const double m = __ldg(nmass + i);
-    if (ms_on) g_smem[o.ms + i] = m;
+    if constexpr (!kFG) g_smem[o.ms + i] = m;
     g_smem[o.rm + i] = frb_arith::rcp_refined(m);
   }
-  auto MASS = [&](int i) -> double { return ms_on ? g_smem[o.ms + i] : __ldg(nmass + i); };
+  auto MASS = [&](int i) -> double {
+    if constexpr (kFG) {
+      return __ldg(nmass + i);
+    } else {
+      return g_smem[o.ms + i];
+    }
+  };
   const int* const lprog = prog + R.tree[3];
   const int* const tprog = prog + R.tree[4];
   const int* const exps = prog + R.tree[5];
@@ -1221,7 +1227,8 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
     // evaluate the elements cut by the rank boundary.
     if (C > 1 && t == 0) issue_halo();
     if (C > 1) gm_send_halo();
-    bool bad = element_coefs(T, 0, C > 1 ? R.n_int : n_act, act_ab, act_L, act_EA, ea, o.pos, o.cf);
+    bool bad = element_coefs(T, 0, C > 1 ? R.n_int : n_act, act_ab, act_L, act_EA,
+                             ea, o.pos, o.cf);
     if (C > 1) {
       mark(sc, prof, PH_F1);
       if constexpr (kGM) {
@@ -1232,7 +1239,8 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
       mb.ph_h ^= 1u;
       if (t == 0) ack_halo();
       mark(sc, prof, PH_HALO);
-      bad |= element_coefs(T, R.n_int, n_act, act_ab, act_L, act_EA, ea, o.pos, o.cf);
+      bad |= element_coefs(T, R.n_int, n_act, act_ab, act_L, act_EA, ea,
+                           o.pos, o.cf);
     }
     if (ramp && it < ramp_n && rank == 0) bad |= check_elements(n, PosFixed{&n, alpha, ramp}, false);
     __syncthreads();

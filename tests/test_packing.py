@@ -150,7 +150,7 @@ def test_c3_networks_fit_a_16_cluster_with_global_fprev():
     """100k-DOF networks (config 3): 16 ranks, f_prev in global memory."""
     t = fb.build_problem(frb.generate_lattice(32, 32, 32, 0.3, 0), frb.AffineBC(np.eye(3))).topo
     part, fglob, mglob = t.choose_cluster()
-    assert part.C == 16 and fglob and not mglob
+    assert part.C == 16 and fglob and mglob
     assert partition_smem_bytes(part, True) <= fb.SMEM_BUDGET
 
 
