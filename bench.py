@@ -375,10 +375,17 @@ def main():
     from paper_2305_07030_b200 import batch as fb
     from paper_2305_07030_b200.distributed import ShardedBatch, decode_records
 
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # FRB_BENCH_GPUS_PER_NODE=1 with FRB_DIST_BACKEND=gloo runs several ranks
+    # on one GPU (a functional check of the multi-rank path; not a measurement)
+    local_gpu = local % int(os.environ.get("FRB_BENCH_GPUS_PER_NODE", str(max(1, torch.cuda.device_count()))))
+    torch.cuda.set_device(local_gpu)
+    dev = torch.device("cuda", local_gpu)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        backend = os.environ.get("FRB_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
 
     def make(i):
         lat, F = network_spec(args.config, i)
@@ -416,7 +423,7 @@ def main():
     kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(args.steps)]
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clocks:
+    with ClockSampler(local_gpu) as clocks:
         torch.cuda.synchronize(dev)
         t_start.record(stream)
         for k in range(args.steps):

@@ -99,10 +99,12 @@ def gather_results(local, layout: ShardLayout, group=None, rows=None):
     out = torch.empty(world * m * RECORD_BYTES, dtype=torch.uint8, device=local.device)
     if world == 1:
         out.copy_(send)
-    elif local.is_cuda:
+    elif dist.get_backend(group) == "nccl":
         dist.all_gather_into_tensor(out, send, group=group)
-    else:  # gloo has no all_gather_into_tensor
-        dist.all_gather(list(out.view(world, -1).unbind(0)), send, group=group)
+    else:  # gloo (CPU tests, or several ranks sharing one GPU): a host round trip
+        host = torch.empty(world * m * RECORD_BYTES, dtype=torch.uint8)
+        dist.all_gather(list(host.view(world, -1).unbind(0)), send.cpu(), group=group)
+        out.copy_(host)
     return out.view(world * m, RECORD_BYTES).index_select(0, rows).reshape(-1)
 
 
