@@ -391,6 +391,7 @@ class Batch:
     node_base: np.ndarray              # (P+1,) int64 node offsets
     _packed_state: dict | None = field(default=None, repr=False)
     _orig_rows: np.ndarray | None = field(default=None, repr=False)  # solver -> original node rows
+    _orig_rows_dev: dict = field(default_factory=dict, repr=False)    # the same per device
     _u_pinned: object = field(default=None, repr=False)               # reused pinned download buffer
     pinned: dict | None = field(default=None, repr=False)
     setup_s: float = math.nan
@@ -817,19 +818,24 @@ def results_to_solve_results(batch: Batch, dres: DeviceResults, raise_singular: 
     """Download and unpermute (DofMap.unpermute, dofmap.py:33-38)."""
     torch = _torch()
     rec = dres.host_results()
-    # one pinned download, one row gather for every problem (solver -> original node order)
-    u_pin = batch._u_pinned
-    if u_pin is None or u_pin.shape != dres.u.shape:
-        u_pin = batch._u_pinned = torch.empty(dres.u.shape, dtype=dres.u.dtype, pin_memory=True)
-    u_pin.copy_(dres.u)
-    u_rows = u_pin.numpy().view(np.dtype((np.void, 24)))  # one 24-byte record per node: a fast row gather
+    # solver -> original node order as one row gather on the device, then one
+    # pinned download and a copy the results own (the pinned buffer is reused)
     if batch._orig_rows is None:
         rows = np.empty(int(batch.node_base[-1]), dtype=np.int64)
         for i, p in enumerate(batch.problems):
             b0 = int(batch.node_base[i])
             rows[b0 + p.node_order] = b0 + np.arange(len(p.node_order))
         batch._orig_rows = rows
-    u_orig = u_rows[batch._orig_rows].view(np.float64)
+    key = str(dres.u.device)
+    rows_t = batch._orig_rows_dev.get(key)
+    if rows_t is None:
+        rows_t = batch._orig_rows_dev[key] = torch.from_numpy(batch._orig_rows).to(dres.u.device)
+    u_dev = dres.u.view(-1, 3).index_select(0, rows_t).view(-1)
+    u_pin = batch._u_pinned
+    if u_pin is None or u_pin.shape != u_dev.shape:
+        u_pin = batch._u_pinned = torch.empty(u_dev.shape, dtype=u_dev.dtype, pin_memory=True)
+    u_pin.copy_(u_dev)
+    u_orig = u_pin.numpy().copy()
     out = []
     first_bad = None
     for i, p in enumerate(batch.problems):
