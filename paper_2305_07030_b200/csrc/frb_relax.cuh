@@ -983,18 +983,19 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
   // the rank's tree block (local + top programs, exports) lives in SMEM
   int* const prog = reinterpret_cast<int*>(g_smem) + o.prog;
   for (int k = t; k < R.tree_len; k += T) prog[k] = __ldg(R.tree + k);
+  // kFG: the one per-node SMEM slot holds the mass itself (A reads it every
+  // iteration); (-f)/m then runs the full division in the shadow of the tree
+  // phase.  Otherwise both the mass and its refined reciprocal are on chip.
   for (int i = t; i < n_own; i += T) {
     const double m = __ldg(nmass + i);
-    if constexpr (!kFG) g_smem[o.ms + i] = m;
-    g_smem[o.rm + i] = frb_arith::rcp_refined(m);
-  }
-  auto MASS = [&](int i) -> double {
     if constexpr (kFG) {
-      return __ldg(nmass + i);
+      g_smem[o.rm + i] = m;
     } else {
-      return g_smem[o.ms + i];
+      g_smem[o.ms + i] = m;
+      g_smem[o.rm + i] = frb_arith::rcp_refined(m);
     }
-  };
+  }
+  auto MASS = [&](int i) -> double { return g_smem[(kFG ? o.rm : o.ms) + i]; };
   const int* const lprog = prog + R.tree[3];
   const int* const tprog = prog + R.tree[4];
   const int* const exps = prog + R.tree[5];
@@ -1125,7 +1126,11 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
         // below, in program order), never another thread's slot
         const int dl = d0 + kk * nthr < nfo ? d0 + kk * nthr : d0;
         const int i = dl / 3;  // f of this iteration, left in fcur by A
-        q[kk] = frb_arith::div_fast_r(-g_smem[o.fcur + dl], MASS(i), g_smem[o.rm + i], ok[kk]);
+        if constexpr (kFG) {
+          q[kk] = frb_arith::div_fast(-g_smem[o.fcur + dl], MASS(i), ok[kk]);
+        } else {
+          q[kk] = frb_arith::div_fast_r(-g_smem[o.fcur + dl], MASS(i), g_smem[o.rm + i], ok[kk]);
+        }
       }
       bool all_ok = true;
 #pragma unroll
