@@ -599,6 +599,10 @@ struct Scalars {
   int ired[kMaxWarps];
   int problem, done, converged, singular;
   int gx_h, gx_s, gx_b;                  // kGM: expected counter values (thread 0)
+  // tree-phase context (warp 0 re-reads it from shared memory each
+  // iteration: held in registers across the loop it spilled to local memory,
+  // and every reload cost an L2 round trip on the serial critical path)
+  int tp_lprog, tp_tprog, tp_exps, tp_n_exp, tp_root, tp_lslot, tp_tslot, tp_flag, tp_TS;
   uint32_t peer_smem[FRB_MAX_CLUSTER];  // shared::cluster base of each rank's dynamic SMEM
   uint32_t peer_bar_h[FRB_MAX_CLUSTER]; // each rank's halo mbarrier
   uint32_t peer_bar_s[FRB_MAX_CLUSTER]; // each rank's leaf-sum mbarrier
@@ -996,10 +1000,17 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
     }
   }
   auto MASS = [&](int i) -> double { return g_smem[(kFG ? o.rm : o.ms) + i]; };
-  const int* const lprog = prog + R.tree[3];
-  const int* const tprog = prog + R.tree[4];
-  const int* const exps = prog + R.tree[5];
-  const int n_exp = R.n_exp, root_top = R.root_top;
+  if (t == 0) {
+    sc.tp_lprog = o.prog + R.tree[3];
+    sc.tp_tprog = o.prog + R.tree[4];
+    sc.tp_exps = o.prog + R.tree[5];
+    sc.tp_n_exp = R.n_exp;
+    sc.tp_root = R.root_top;
+    sc.tp_lslot = o.lslot;
+    sc.tp_tslot = o.tslot;
+    sc.tp_flag = o.flag;
+    sc.tp_TS = R.TS;
+  }
   const bool quad_mode = (R.tree[9] & 4) != 0;  // plan.py MODE_QUAD
 
   const bool adaptive = cfg.damping == FRB_DAMPING_ADAPTIVE;
@@ -1450,9 +1461,15 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
     }
 #endif
     if (t < 32) {
+      const volatile Scalars& vs = sc;
+      const int* const gi = reinterpret_cast<const int*>(g_smem);
+      const int* const lprog = gi + vs.tp_lprog;
+      const int* const tprog = gi + vs.tp_tprog;
+      const int* const exps = gi + vs.tp_exps;
+      const int n_exp = vs.tp_n_exp, root_top = vs.tp_root, o_lslot = vs.tp_lslot, TSv = vs.tp_TS;
       const int ob = static_cast<int>(mb.ph_s);  // exchange buffer of this iteration's parity
-      const int o_ts = o.tslot + ob * 3 * R.TS, o_fl = o.flag + ob * 64;
-      run_prog(lprog, o.lslot, lane);
+      const int o_ts = vs.tp_tslot + ob * 3 * TSv, o_fl = vs.tp_flag + ob * 64;
+      run_prog(lprog, o_lslot, lane);
       mark(sc, prof, PH_TLP);
       // every (export, rank) pair on its own lane: the own copy for qr ==
       // rank, three st.async into the peer's top slots otherwise
@@ -1462,14 +1479,14 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
 #pragma unroll 1
       for (int x = lane; x < n_exp * (kGM ? 1 : C); x += 32) {
         if constexpr (kGM) {
-          const int ls = o.lslot + 3 * exps[2 * x], ts = 3 * exps[2 * x + 1];
+          const int ls = o_lslot + 3 * exps[2 * x], ts = 3 * exps[2 * x + 1];
           gx_ex[ts] = g_smem[ls];
           gx_ex[ts + 1] = g_smem[ls + 1];
           gx_ex[ts + 2] = g_smem[ls + 2];
           continue;
         }
         const int e = x / C, qr = x - e * C;
-        const int ls = o.lslot + 3 * exps[2 * e], ts = 3 * exps[2 * e + 1];
+        const int ls = o_lslot + 3 * exps[2 * e], ts = 3 * exps[2 * e + 1];
         const double v0 = g_smem[ls], v1 = g_smem[ls + 1], v2 = g_smem[ls + 2];
         if (qr == rank) {
           g_smem[o_ts + ts] = v0;
@@ -1493,7 +1510,7 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
             st_async(sc.peer_smem[0] + 8u * (o_fl + 16 + 3 * rank + e), e3[e], sc.peer_bar_s[0]);
       }
       if (kGM) {  // flag, then publish this rank's exports with a release add
-        if (lane == 0) gx_ex[3 * R.TS + rank] = sc.singular ? 1.0 : 0.0;
+        if (lane == 0) gx_ex[3 * TSv + rank] = sc.singular ? 1.0 : 0.0;
         __threadfence();  // every lane's export stores
         __syncwarp();
         if (lane == 0) atomicAdd(gx.cnt + 32 * 16, 1);
@@ -1520,7 +1537,7 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
           for (int q = 0; q < 8; ++q)
             if (k0 + 32 * q < n_top) g_smem[o_ts + k0 + 32 * q] = tmp[q];
         }
-        if (lane < C) g_smem[o_fl + lane] = __ldcg(gx_ex + 3 * R.TS + lane);
+        if (lane < C) g_smem[o_fl + lane] = __ldcg(gx_ex + 3 * TSv + lane);
         __syncwarp();
         mark(sc, prof, PH_TW);
       } else if (C > 1) {
