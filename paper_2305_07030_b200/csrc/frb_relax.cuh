@@ -1078,8 +1078,6 @@ __device__ void solve_problem(const frb_batch& b, const frb_config& cfg, int p, 
   // into the receivers' mirrors (16-byte stores), then thread 0 publishes the
   // bytes with a release add on each receiver's counter; a receiver waits
   // for its running total and copies its halo slots back from its mirror.
-  const int par_h_dummy = 0;
-  (void)par_h_dummy;
   auto gm_send_halo = [&]() {
     if constexpr (kGM) {
       const int par = static_cast<int>(mb.ph_h);
