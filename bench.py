@@ -346,6 +346,20 @@ def traffic_per_launch(config: str, n_networks: int):
     return t["bytes"] * n_networks / t["networks"], t["source"]
 
 
+def pipe_utilisation(config: str):
+    """FP64-pipe, issue and warp occupancy percentages of the relaxation
+    kernel from the same committed ncu capture (the compute side of the
+    roofline: the streaming fraction is an effective bandwidth)."""
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    if not os.path.exists(path):
+        return None
+    with open(path) as fh:
+        t = json.load(fh).get(config)
+    if not isinstance(t, dict) or "fp64_pipe_pct" not in t:
+        return None
+    return {k: t[k] for k in ("fp64_pipe_pct", "issue_active_pct", "warps_active_pct")} | {"source": t["source"].split(":")[0] + " (ncu --set full)"}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -518,7 +532,8 @@ def main():
         "gpu_launches": args.steps * int((launch.groups["count"] > 0).sum()),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
-                     "peak_source": peak_src, "kernel": "frb_relax_kernel", "kernel_ms": 1e3 * kern_mean,
+                     "peak_source": peak_src, "compute": pipe_utilisation(args.config),
+                     "kernel": "frb_relax_kernel", "kernel_ms": 1e3 * kern_mean,
                      "alg_bytes_per_launch": alg_all / world,
                      "alg_bytes_model": "sum over networks of iters * (48 N + 48 nf + 24 M) (SURVEY.md 8d)"},
         "parity_spot_check": spot,
