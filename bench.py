@@ -479,7 +479,9 @@ def main():
             if world > 1:
                 sb.gather(dres.results)
             return out
-        e2e_step()
+        for _ in range(max(2, min(args.warmup, 3))):  # steady state: two result buffers in the host cache
+            res = e2e_step()
+        res = None
         torch.cuda.synchronize(dev)
         if world > 1:
             dist.barrier()

@@ -392,7 +392,6 @@ class Batch:
     _packed_state: dict | None = field(default=None, repr=False)
     _orig_rows: np.ndarray | None = field(default=None, repr=False)  # solver -> original node rows
     _orig_rows_dev: dict = field(default_factory=dict, repr=False)    # the same per device
-    _u_pinned: object = field(default=None, repr=False)               # reused pinned download buffer
     pinned: dict | None = field(default=None, repr=False)
     setup_s: float = math.nan
 
@@ -831,27 +830,33 @@ def results_to_solve_results(batch: Batch, dres: DeviceResults, raise_singular: 
     if rows_t is None:
         rows_t = batch._orig_rows_dev[key] = torch.from_numpy(batch._orig_rows).to(dres.u.device)
     u_dev = dres.u.view(-1, 3).index_select(0, rows_t).view(-1)
-    u_pin = batch._u_pinned
-    if u_pin is None or u_pin.shape != u_dev.shape:
-        u_pin = batch._u_pinned = torch.empty(u_dev.shape, dtype=u_dev.dtype, pin_memory=True)
+    # one D2H into a fresh pinned buffer that the results own (their u are
+    # views of it; torch's host allocator caches the block, so once the
+    # previous call's results are dropped the next call reuses it: no host
+    # copy and no page-locking per call)
+    u_pin = torch.empty(u_dev.shape, dtype=u_dev.dtype, pin_memory=True)
     u_pin.copy_(u_dev)
-    u_orig = u_pin.numpy().copy()
+    u_orig = u_pin.numpy()
+    nb = (3 * batch.node_base).tolist()
+    status = rec["status"].tolist()
+    conv = rec["converged"].astype(bool).tolist()
+    iters = rec["iters"].tolist()
+    fres = rec["final_residual"].tolist()
+    rref = rec["r_ref"].tolist()
+    eres = rec["energy_residual"].tolist()
+    stress = np.array(rec["avg_stress"], dtype=np.float64).reshape(-1, 3, 3)
     out = []
     first_bad = None
-    for i, p in enumerate(batch.problems):
-        r = rec[i]
-        if r["status"] == nat.STATUS_SINGULAR:
+    for i in range(batch.n_problems):
+        if status[i] == nat.STATUS_SINGULAR:
             if first_bad is None:
-                first_bad = (i, int(r["bad_element"]))
+                first_bad = (i, int(rec["bad_element"][i]))
             out.append(None)
             continue
-        u = u_orig[3 * int(batch.node_base[i]):3 * int(batch.node_base[i + 1])]
-        e = float(r["energy_residual"])
-        out.append(SolveResult(converged=bool(r["converged"]), iters=int(r["iters"]),
-                               final_residual=float(r["final_residual"]), u=u,
-                               avg_stress=np.array(r["avg_stress"], dtype=np.float64).reshape(3, 3),
-                               energy_residual=None if math.isnan(e) else e,
-                               r_ref=float(r["r_ref"])))
+        e = eres[i]
+        out.append(SolveResult(converged=conv[i], iters=iters[i], final_residual=fres[i], u=u_orig[nb[i]:nb[i + 1]],
+                               avg_stress=stress[i], energy_residual=None if math.isnan(e) else e,
+                               r_ref=rref[i]))
     if first_bad is not None and raise_singular:
         i, e = first_bad
         raise SingularElementError(f"element {e}: current length collapsed", element=e, problem=i)
