@@ -626,14 +626,15 @@ def _pack(networks, bcs, probs, cluster: int | None = None) -> Batch:
         X=X, node_mass=mass,
         inc_node=_cat(inc_node, np.int32, 2), inc=_cat(inc, np.int32, 2),
         elem_ab=_cat(elem_ab, np.int32, 2), elem_L=EL,
-        elem_EA=EA, plans=_cat(plans, np.int32),
+        plans=_cat(plans, np.int32),
         ell=_cat(ell, np.uint32).view(np.int32), fix_g=_cat(fix_g, np.int32),
         act_ab=_cat(act_ab, np.uint32).view(np.int32), act_L=act_L,
         halo_g=_cat(halo_g, np.int32), runs=_cat(runs, np.int32, RUN_WORDS), trees=_cat(trees, np.int32),
         order=np.asarray(order, dtype=np.int32),
         problems=desc.view(np.uint8).copy(), parts=parts.view(np.uint8).copy(),
     )
-    if any_nonuniform:
+    if any_nonuniform:  # otherwise E*A travels in the descriptor (FRB_PF_EA_UNIFORM)
+        arrays["elem_EA"] = EA
         arrays["act_EA"] = act_EA
     return Batch(networks=networks, bcs=bcs, problems=probs, desc=desc, parts=parts,
                  groups=np.array(groups, dtype=nat.GROUP_DTYPE), arrays=arrays, node_base=node_base)

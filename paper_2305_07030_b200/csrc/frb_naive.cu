@@ -75,7 +75,7 @@ __global__ void __launch_bounds__(kNT) nv_coefs(const __grid_constant__ frb_batc
     const double dz = dsub(pos(ab.y, 2), pos(ab.x, 2));
     const double l = seg_len(dx, dy, dz);
     const double L = n.EL[e];
-    coef[e] = ddiv(dmul(n.EA[e], dsub(l, L)), dmul(L, l));
+    coef[e] = ddiv(dmul(elem_ea(n, e), dsub(l, L)), dmul(L, l));
     bad |= l < dmul(kCollapse, L);
   }
   if (bad) st->singular = 1;

@@ -281,7 +281,7 @@ __device__ void load_views(Net& n, Rank& R, const frb_batch& b, int p, int r) {
   n.inc = reinterpret_cast<const int2*>(b.inc) + P.inc_base;
   n.eab = reinterpret_cast<const int2*>(b.elem_ab) + P.telem_base;
   n.EL = b.elem_L + P.elem_base;
-  n.EA = b.elem_EA + P.elem_base;
+  n.EA = b.elem_EA ? b.elem_EA + P.elem_base : nullptr;
   n.plan = b.plans + P.plan_base;
   n.L = n.plan[0];
   n.n_levels = n.plan[1];
@@ -403,6 +403,10 @@ __device__ __forceinline__ bool element_force(double dx, double dy, double dz, d
   return l < dmul(kCollapse, L);
 }
 
+// E*A of element e: the descriptor's value when uniform (the per-element
+// array is then not uploaded: frb_batch.elem_EA may be null)
+__device__ __forceinline__ double elem_ea(const Net& n, int e) { return n.ea_uniform ? n.ea : n.EA[e]; }
+
 // Internal force at node i from the CSR incidence lists (all nodes, solver
 // numbering; used by the epilogue, the singular path and internal_forces).
 template <class Pos>
@@ -420,12 +424,12 @@ __device__ __noinline__ bool node_force_csr(const Net& n, const Pos& pos, int i,
     const double ox = pos(e.x, 0), oy = pos(e.x, 1), oz = pos(e.x, 2);
     double nx, ny, nz;
     if (k < na) {
-      bad |= element_force(dsub(ox, px), dsub(oy, py), dsub(oz, pz), n.EL[e.y], n.EA[e.y], nx, ny, nz);
+      bad |= element_force(dsub(ox, px), dsub(oy, py), dsub(oz, pz), n.EL[e.y], elem_ea(n, e.y), nx, ny, nz);
       ax = dsub(ax, nx);  // bincount(ia, -nd): 0 + (-nd) + ...
       ay = dsub(ay, ny);
       az = dsub(az, nz);
     } else {
-      bad |= element_force(dsub(px, ox), dsub(py, oy), dsub(pz, oz), n.EL[e.y], n.EA[e.y], nx, ny, nz);
+      bad |= element_force(dsub(px, ox), dsub(py, oy), dsub(pz, oz), n.EL[e.y], elem_ea(n, e.y), nx, ny, nz);
       bx = dadd(bx, nx);  // bincount(ib, nd)
       by = dadd(by, ny);
       bz = dadd(bz, nz);
