@@ -9,6 +9,6 @@ timeout 900 python bench.py --config c2 --steps 5 --warmup 3 > gpurun_out/final_
 python -c "import json; d=json.load(open('gpurun_out/final_c2.json')); print('c2', d['value'], d['roofline']['frac'], d['e2e']['value'], d['cpu_baseline']['value'])"
 timeout 1500 python bench.py --config c5 --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/final_c5.json 2> gpurun_out/final_c5.err
 python -c "import json; d=json.load(open('gpurun_out/final_c5.json')); print('c5', d['value'], d['roofline']['frac'], d['e2e']['value'])"
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:frb_relax -s 3 -c 1 -f -o gpurun_out/final_prof_c3 python bench.py --config c3 --limit 7 --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > /dev/null 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:frb_relax -s 3 -c 1 -f -o gpurun_out/final_prof_c2 python bench.py --config c2 --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > /dev/null 2>&1
-ls gpurun_out/final_prof_*
+#timeout 900 ncu --set full --clock-control none --import-source on -k regex:frb_relax -s 3 -c 1 -f -o gpurun_out/final_prof_c3 python bench.py --config c3 --limit 7 --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > /dev/null 2>&1
+#timeout 900 ncu --set full --clock-control none --import-source on -k regex:frb_relax -s 3 -c 1 -f -o gpurun_out/final_prof_c2 python bench.py --config c2 --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > /dev/null 2>&1
+#ls gpurun_out/final_prof_*
