@@ -156,15 +156,23 @@ int frb_solve_batch(const frb_batch* batch, const frb_config* cfg, void* stream)
       if (batch->groups[gi].count > 0 && (rc = launch_one(batch, cfg, gi, optin, s, n_live <= 1))) return rc;
     return FRB_OK;
   }
-  // Several cluster sizes (heterogeneous batch): the groups run concurrently
-  // on forked streams, largest clusters launched first, joined back into s,
-  // so small networks fill the SMs the large clusters leave free.
+  // Several cluster sizes (heterogeneous batch).  Groups of 16-CTA clusters
+  // that may use virtual clusters run last, one after another, each alone
+  // (7 hardware clusters + virtual clusters on the 36 SMs they leave idle);
+  // concurrently with smaller groups those 36 SMs were all the small
+  // networks got (c4: 2.27 s against 0.52 s + the 16-CTA groups alone).
+  // The other groups run concurrently on forked streams, largest clusters
+  // launched first, joined back into s.
+  auto last = [&](const frb_group& g) {
+    return g.cluster >= 16 && g.gm_cap > 0 && batch->xchg && !(g.flags & FRB_GF_NO_VIRTUAL) &&
+           cfg->energy_check_interval <= 0 && !batch->phase_cycles;
+  };
   cudaEvent_t fork;
   rc = cuda_check(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming), "cudaEventCreate");
   if (rc) return rc;
   rc = cuda_check(cudaEventRecord(fork, s), "cudaEventRecord");
   for (int gi = batch->n_groups - 1; gi >= 0 && !rc; --gi) {
-    if (batch->groups[gi].count == 0) continue;
+    if (batch->groups[gi].count == 0 || last(batch->groups[gi])) continue;
     cudaStream_t gs;
     cudaEvent_t join;
     rc = cuda_check(cudaStreamCreateWithFlags(&gs, cudaStreamNonBlocking), "cudaStreamCreate");
@@ -180,6 +188,8 @@ int frb_solve_batch(const frb_batch* batch, const frb_config* cfg, void* stream)
     cudaStreamDestroy(gs);     // likewise: pending work still runs
   }
   cudaEventDestroy(fork);
+  for (int gi = batch->n_groups - 1; gi >= 0 && !rc; --gi)  // after every forked group (stream order on s)
+    if (batch->groups[gi].count > 0 && last(batch->groups[gi])) rc = launch_one(batch, cfg, gi, optin, s, true);
   return rc;
 }
 
