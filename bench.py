@@ -531,7 +531,7 @@ def main():
         "node_updates_per_s": node_updates_all / (elapsed / args.steps),
         "iters_mean": float(iters.mean()),
         "e2e": e2e,
-        "gpu_launches": args.steps * int((launch.groups["count"] > 0).sum()),
+        "gpu_launches": args.steps * launch.kernel_launches,  # frb_solve_launches() per step
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
                      "peak_source": peak_src, "compute": pipe_utilisation(args.config),

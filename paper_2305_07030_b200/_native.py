@@ -26,7 +26,7 @@ PHASES = 12             # phase_cycles slots per CTA (frb200.h)
 PHASE_NAMES = ("F1 coefs", "F2 gather", "A per-DOF", "C chains", "T local+exp", "T exch wait",
                "T top+scal", "U update", "epilogue", "prologue", "halo wait", "T local tree")
 
-EXPORTS = ("frb_abi_version", "frb_last_error", "frb_device_info", "frb_rank_smem_bytes",
+EXPORTS = ("frb_abi_version", "frb_last_error", "frb_solve_launches", "frb_device_info", "frb_rank_smem_bytes",
            "frb_max_dofs_per_thread", "frb_solve_batch", "frb_internal_forces",
            "frb_selftest_arith", "frb_setup_problem", "frb_setup_batch",
            "frb_naive_solve", "frb_naive_scratch_doubles")
@@ -109,6 +109,7 @@ def lib() -> C.CDLL:
     h = C.CDLL(LIB_PATH)
     h.frb_abi_version.restype = C.c_int
     h.frb_last_error.restype = C.c_char_p
+    h.frb_solve_launches.restype = C.c_int
     h.frb_device_info.argtypes = [C.c_int] + [C.POINTER(C.c_int)] * 4
     h.frb_rank_smem_bytes.restype = C.c_int64
     h.frb_rank_smem_bytes.argtypes = [C.c_int32] * 6

@@ -790,6 +790,7 @@ class Launch:
     keep: tuple = ()
     phase: object = None
     naive: object = None          # NaiveLoop scratch (per-operation strategy)
+    kernel_launches: int = 0      # relaxation kernels the last run() launched
 
     @property
     def threads(self) -> int:
@@ -806,6 +807,7 @@ class Launch:
                                                     C.c_void_p(s.cuda_stream)))
             return
         nat.check(nat.lib().frb_solve_batch(C.byref(self.fb), C.byref(self.fc), C.c_void_p(s.cuda_stream)))
+        self.kernel_launches = int(nat.lib().frb_solve_launches())  # hardware + virtual cluster kernels
 
 
 def config_struct(cfg: SolverConfig) -> nat.FrbConfig:

@@ -7,6 +7,7 @@
 
 namespace frb_tu {
 thread_local char g_err[512] = "";
+thread_local int g_launches = 0;
 }  // namespace frb_tu
 
 using frb_tu::g_err;
@@ -68,6 +69,8 @@ extern "C" {
 int frb_abi_version(void) { return FRB_ABI_VERSION; }
 
 const char* frb_last_error(void) { return g_err; }
+
+int frb_solve_launches(void) { return frb_tu::g_launches; }
 
 int frb_device_info(int device, int* n_sm, int* smem_optin, int* cc_major, int* cc_minor) {
   cudaDeviceProp prop;
@@ -134,6 +137,7 @@ extern "C" {
 
 int frb_solve_batch(const frb_batch* batch, const frb_config* cfg, void* stream) {
   if (!batch || !cfg) return set_err(FRB_E_INVALID, "null batch or config");
+  frb_tu::g_launches = 0;
   if (batch->n_problems < 0 || batch->n_groups < 0) return set_err(FRB_E_INVALID, "negative counts");
   if (batch->n_problems == 0) return FRB_OK;
   if (!batch->groups || !batch->queue || !batch->work) return set_err(FRB_E_INVALID, "groups/queue/work missing");

@@ -92,6 +92,7 @@ namespace cg = cooperative_groups;
 
 namespace frb_tu {
 extern thread_local char g_err[512];
+extern thread_local int g_launches;  // frb_solve_launches()
 }
 
 namespace {
@@ -1889,8 +1890,10 @@ int launch_group(const frb_batch* batch, const frb_config* cfg, const frb_group&
       vc.stream = gs;
       vc.attrs = nullptr;
       vc.numAttrs = 0;
+      if (!rc) frb_tu::g_launches += clusters > 0;
       if (!rc) rc = cuda_check(cudaLaunchKernelEx(&vc, vkern, *batch, *cfg, g.first, g.count, queue, g),
                                "cudaLaunchKernelEx(virtual clusters)");
+      if (!rc) ++frb_tu::g_launches;
       if (!rc) rc = cuda_check(cudaEventRecord(ev1, gs), "cudaEventRecord");
       if (!rc) rc = cuda_check(cudaStreamWaitEvent(s, ev1, 0), "cudaStreamWaitEvent");
       cudaEventDestroy(ev0);
@@ -1902,6 +1905,7 @@ int launch_group(const frb_batch* batch, const frb_config* cfg, const frb_group&
   }
   rc = cuda_check(cudaLaunchKernelEx(&lc, kern, *batch, *cfg, g.first, g.count, queue, g), "cudaLaunchKernelEx");
   if (rc) return rc;
+  ++frb_tu::g_launches;
   return cuda_check(cudaGetLastError(), "frb_relax_kernel launch");
 }
 

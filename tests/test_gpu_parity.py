@@ -289,3 +289,18 @@ def test_randomly_renumbered_network_vs_oracle(cuda_device):
     r = frb.solve_batch(batch, config=cfg)[0]
     o = orc.solve(net2, F, cfg)
     assert_matches(r, o.u, o.iters, o.converged, o.residual, o.r_ref, o.sigma, label="renumbered 16^3")
+
+
+def test_solve_reports_its_kernel_launches(cuda_device):
+    """frb_solve_launches: one relaxation kernel per launch group (these
+    groups have no virtual clusters: 1- and 2-CTA clusters)."""
+    one = fb.pack_batch([frb.generate_lattice(6, 6, 6, 0.3, s) for s in range(3)],
+                        [frb.AffineBC(np.diag([1.1, 1.0, 1.0]))] * 3)
+    L = one.to_device().prepare(frb.SolverConfig(), frb.TeamBatched())
+    L.run()
+    assert L.kernel_launches == 1
+    mixed = fb.pack_batch([frb.generate_lattice(6, 6, 6, 0.3, 0), frb.generate_lattice(15, 15, 15, 0.3, 0)],
+                          [frb.AffineBC(np.diag([1.1, 1.0, 1.0]))] * 2)
+    L = mixed.to_device().prepare(frb.SolverConfig(), frb.TeamBatched())
+    L.run()
+    assert len(mixed.groups) == 2 and L.kernel_launches == 2
