@@ -76,8 +76,8 @@ def test_big_cases_are_the_baseline_configs():
 
 
 def test_full_length_heterogeneous_batch(cuda_device):
-    """All large cases in ONE batch: the 16-, 8- and 2-CTA groups run
-    concurrently (c4's execution mode), each to convergence."""
+    """All large cases in ONE batch (c4's execution mode: the 8- and 2-CTA
+    groups concurrently, then the 16-CTA groups), each to convergence."""
     from paper_2305_07030_b200 import batch as fb
     names = sorted(BIG)
     cases = [_case(n) for n in names]
@@ -108,3 +108,21 @@ def test_c3_batch_replicas(cuda_device):
     dres = batch.to_device().solve(frb.SolverConfig())
     for i, r in enumerate(fb.results_to_solve_results(batch, dres)):
         _check(f"c3 copy {i}", rec, r, _forces(batch, dres, i))
+
+
+def test_heterogeneous_batch_with_virtual_clusters(cuda_device):
+    """Nine C3 networks next to 8- and 2-CTA networks: the smaller groups run
+    concurrently, then the 16-CTA group alone on 7 hardware + 2 virtual
+    clusters (9 networks: the virtual clusters get work).  Two kernels for the
+    16-CTA group, one per smaller group; every network equals the reference."""
+    from paper_2305_07030_b200 import batch as fb
+    names = ["c3_32cube_seed0"] * 9 + sorted(n for n in BIG if n != "c3_32cube_seed0" and BIG[n]["lattice"][0] < 26)
+    cases = [_case(n) for n in names]
+    batch = frb.pack_batch([c[0] for c in cases], [frb.AffineBC(c[1]) for c in cases])
+    launch = batch.to_device().prepare(frb.SolverConfig(), frb.TeamBatched())
+    launch.run()
+    n_groups = int((batch.groups["count"] > 0).sum())
+    assert launch.kernel_launches == n_groups + 1  # + the virtual clusters of the 16-CTA group
+    res = fb.results_to_solve_results(batch, launch.out)
+    for i, (name, (_, _, rec), r) in enumerate(zip(names, cases, res)):
+        _check(f"{name} #{i}", rec, r, _forces(batch, launch.out, i))
