@@ -826,7 +826,11 @@ def config_struct(cfg: SolverConfig) -> nat.FrbConfig:
 
 
 def results_to_solve_results(batch: Batch, dres: DeviceResults, raise_singular: bool = True):
-    """Download and unpermute (DofMap.unpermute, dofmap.py:33-38)."""
+    """Download and unpermute (DofMap.unpermute, dofmap.py:33-38).
+
+    The results' ``u`` are views of one page-locked buffer per call (no host
+    copy); it is released when the last of them is dropped, so a caller that
+    keeps a few results of a large batch should keep ``np.copy(r.u)``."""
     torch = _torch()
     rec = dres.host_results()
     # solver -> original node order as one row gather on the device, then one
