@@ -604,9 +604,13 @@ def _pack(networks, bcs, probs, cluster: int | None = None) -> Batch:
     # with the network's linear size) x the load |F - I|, which sets how far
     # the relaxation has to travel (32^3: uniaxial 2,519, shear 6,805
     # iterations); it only orders the queue, results do not depend on it.
+    if P:
+        Fs = np.stack([np.asarray(p.F, dtype=np.float64).reshape(3, 3) for p in probs])
+        load = np.maximum(np.linalg.norm(Fs - np.eye(3), axis=(1, 2)), 1e-3)
+        est = np.array([p.n_nodes for p in probs], dtype=np.float64) ** (4.0 / 3.0) * load
+
     def cost(i):
-        F = np.asarray(probs[i].F, dtype=np.float64).reshape(3, 3)
-        return -(probs[i].n_nodes ** (4.0 / 3.0)) * max(float(np.linalg.norm(F - np.eye(3))), 1e-3)
+        return -est[i]
 
     order, groups = [], []
     for C, fglob in sorted({(pt.C, fg) for pt, fg in zip(part_of, fglob_of)}):
