@@ -27,3 +27,9 @@ def timed(batch, label):
 timed(full, "c4 all")
 timed(frb.pack_batch([nets[i] for i in big], [bcs[i] for i in big]), f"c4 C16 only ({len(big)})")
 timed(frb.pack_batch([nets[i] for i in rest], [bcs[i] for i in rest]), f"c4 rest ({len(rest)})")
+
+# each smaller group alone (is the concurrent phase 1 better than one after another?)
+if os.environ.get("C4_GROUPS"):
+    for C in (8, 4, 2, 1):
+        ids = [i for i in rest if int(full.desc["cluster"][i]) == C]
+        timed(frb.pack_batch([nets[i] for i in ids], [bcs[i] for i in ids]), f"c4 C{C} alone ({len(ids)})")
