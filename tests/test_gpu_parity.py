@@ -304,3 +304,19 @@ def test_solve_reports_its_kernel_launches(cuda_device):
     L = mixed.to_device().prepare(frb.SolverConfig(), frb.TeamBatched())
     L.run()
     assert len(mixed.groups) == 2 and L.kernel_launches == 2
+
+
+def test_energy_ledger_heterogeneous_batch(cuda_device):
+    """The ledger kernels on a batch of several cluster sizes (1- and 2-CTA
+    groups launched concurrently): every network equals its own oracle run."""
+    nets = [frb.generate_lattice(6, 6, 6, 0.3, 1), frb.generate_lattice(16, 16, 16, 0.3, 4),
+            frb.generate_lattice(7, 6, 8, 0.3, 5)]
+    Fs = [np.diag([1.1, 1.0, 1.05]), np.eye(3) + 0.05 * np.eye(3)[:, [1, 2, 0]], np.diag([1.05, 1.05, 1.0])]
+    cfg = frb.SolverConfig(energy_check_interval=1, max_iters=300)
+    batch = fb.pack_batch(nets, [frb.AffineBC(F) for F in Fs])
+    assert len({int(c) for c in batch.desc["cluster"]}) >= 2
+    res = frb.solve_batch(batch, config=cfg)
+    for i, (net, F, r) in enumerate(zip(nets, Fs, res)):
+        o = orc.solve(net, F, cfg)
+        assert_matches(r, o.u, o.iters, o.converged, o.residual, o.r_ref, o.sigma, label=f"net {i}")
+        assert abs(r.energy_residual - o.energy_residual) <= 1e-10 * abs(o.energy_residual)
